@@ -1,0 +1,514 @@
+// api_wsc.cuh -- host orchestration of fs_wsc_replay / fs_wsc_step / fs_sweep:
+// shared trace-derived tables (head lists, static head windows, tiers), per-scenario
+// weights / limits / validity checks, and the engine launches.  Included at the end
+// of fairserve.cu (uses finish(), err_reset(), act_limits()).
+#pragma once
+
+// ------------------------------------------------------------------ shared tables
+__global__ void k_flag_heads(DTrace t, u32* flag) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n) flag[i] = m_stage(t.meta[i]) == 1;
+}
+__global__ void k_scatter_heads(DTrace t, const u32* flag, const u32* pre, u32* heads) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n && flag[i]) heads[pre[i]] = (u32)i;
+}
+__global__ void k_list_keys(u64 n, const u32* list, DTrace t, u32 by_app, u32* key) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  u32 i = list[p];
+  key[p] = by_app ? t.user[i] * t.A + m_app(t.meta[i]) : t.user[i];
+}
+__global__ void k_posmap(u64 n, const u32* list, u32* pos) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) pos[list[p]] = (u32)p;
+}
+// head token load tau = L_I + L_S + O-hat(app, stage 1) (0 if the profile has no slot)
+__global__ void k_hw_gather(u64 n, const u32* list, DTrace t, u32 J, const u32* maxstage, const u64* cnt,
+                            const u64* ohat, u32* ts, u64* tau) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  u32 i = list[p], m = t.meta[i];
+  u64 k, r = 0;
+  if (prof_slot(J, maxstage, cnt, m_app(m), 1, &k)) r = ohat[k];
+  ts[p] = t.t_ms[i];
+  tau[p] = (u64)t.len_in[i] + t.len_sys[i] + r;
+}
+// static window over the heads of a segment: count and load of heads in (t - W, t], <= own position
+__global__ void k_hw_win(u64 n, const u32* list, const u32* key, const u64* seg, const u32* ts, const u64* ptau,
+                         i64 W, const u32* posmap, u32* out_n, u64* out_t) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  u64 lb = window_lb<u32>(ts, seg[key[p]], p, (i64)ts[p] - W);
+  u64 dst = posmap ? posmap[list[p]] : p;
+  out_n[dst] = (u32)(p - lb + 1);
+  out_t[dst] = ptau[p + 1] - ptau[lb];
+}
+__global__ void k_utier(DTrace t, u32* utier, unsigned long long* tier_calls) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n) return;
+  u32 tr = m_tier(t.meta[i]);
+  atomicMin(&utier[t.user[i]], tr);
+  atomicAdd(&tier_calls[tr], 1ull);
+}
+
+struct WscShared {
+  Links L;
+  u32* heads; u64 n_heads;
+  u32* uh_list; u64* uh_off; u32* uh_key;
+  u32 *hw_ng, *hw_na; u64 *hw_tg, *hw_ta;
+  u32* utier; u64* tier_calls;
+  EngShared sh;
+};
+
+static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profile* P, u32 window_ms, bool windows,
+                       WscShared* W) {
+  u64 n = t.n;
+  int B = 256;
+  build_links(ctx, S, t, &W->L);
+  u32* flag = S.alloc<u32>(n + 1);
+  u32* pre = S.alloc<u32>(n + 1);
+  W->utier = S.alloc<u32>(t.U + 1);
+  W->tier_calls = S.zeros<u64>(256);
+  if (S.failed) return false;
+  cudaMemsetAsync(W->utier, 0xFF, (t.U + 1) * 4, ctx->stream);
+  if (n) {
+    FS_LAUNCH(ctx, "flag_heads", k_flag_heads, div_up(n, B), B, 0, t, flag);
+    FS_LAUNCH(ctx, "utier", k_utier, div_up(n, B), B, 0, t, W->utier, (unsigned long long*)W->tier_calls);
+  }
+  excl_scan<u32>(ctx, S, flag, pre, n, pre + n);
+  u32 nh = 0;
+  cudaMemcpyAsync(&nh, pre + n, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  W->n_heads = nh;
+  W->heads = S.alloc<u32>(nh + 1);
+  u32* keys = S.alloc<u32>(nh + 1);
+  W->uh_off = S.alloc<u64>(t.U + 1);
+  W->hw_ng = S.zeros<u32>(nh + 1); W->hw_na = S.zeros<u32>(nh + 1);
+  W->hw_tg = S.zeros<u64>(nh + 1); W->hw_ta = S.zeros<u64>(nh + 1);
+  if (S.failed) return false;
+  if (n) FS_LAUNCH(ctx, "scatter_heads", k_scatter_heads, div_up(n, B), B, 0, t, flag, pre, W->heads);
+  if (nh) FS_LAUNCH(ctx, "list_keys", k_list_keys, div_up(nh, B), B, 0, (u64)nh, W->heads, t, 0u, keys);
+  u32* skeys;
+  if (!radix_sort<u32>(ctx, S, keys, W->heads, nh, bits_for(t.U ? t.U - 1 : 0), &skeys, &W->uh_list)) return false;
+  W->uh_key = skeys;
+  FS_LAUNCH(ctx, "seg_bounds", k_seg_bounds<u32>, div_up(t.U + 1, B), B, 0, skeys, (u64)nh, (u64)t.U, W->uh_off);
+  if (windows && nh) {
+    const i64 Wms = window_ms;
+    u32* ts = S.alloc<u32>(nh); u64* tau = S.alloc<u64>(nh + 1); u64* ptau = S.alloc<u64>(nh + 1);
+    u32* posmap = S.alloc<u32>(n);
+    if (S.failed) return false;
+    // per user
+    FS_LAUNCH(ctx, "hw_gather", k_hw_gather, div_up(nh, B), B, 0, (u64)nh, W->uh_list, t, P->J, P->maxstage, P->cnt,
+              P->ohat, ts, tau);
+    excl_scan<u64>(ctx, S, tau, ptau, nh, ptau + nh);
+    FS_LAUNCH(ctx, "hw_win", k_hw_win, div_up(nh, B), B, 0, (u64)nh, W->uh_list, skeys, W->uh_off, ts, ptau, Wms,
+              (const u32*)nullptr, W->hw_ng, W->hw_tg);
+    // per (user, app), results mapped back to the head's per-user position
+    FS_LAUNCH(ctx, "posmap", k_posmap, div_up(nh, B), B, 0, (u64)nh, W->uh_list, posmap);
+    u32* k2 = S.alloc<u32>(nh);
+    if (S.failed) return false;
+    FS_LAUNCH(ctx, "list_keys", k_list_keys, div_up(nh, B), B, 0, (u64)nh, W->heads, t, 1u, k2);
+    u32 *k2s, *l2;
+    u64 nseg = (u64)t.U * t.A;
+    if (!radix_sort<u32>(ctx, S, k2, W->heads, nh, bits_for(nseg ? nseg - 1 : 0), &k2s, &l2)) return false;
+    u64* seg2 = S.alloc<u64>(nseg + 1);
+    if (S.failed) return false;
+    FS_LAUNCH(ctx, "seg_bounds", k_seg_bounds<u32>, div_up(nseg + 1, B), B, 0, k2s, (u64)nh, nseg, seg2);
+    FS_LAUNCH(ctx, "hw_gather", k_hw_gather, div_up(nh, B), B, 0, (u64)nh, l2, t, P->J, P->maxstage, P->cnt, P->ohat,
+              ts, tau);
+    excl_scan<u64>(ctx, S, tau, ptau, nh, ptau + nh);
+    FS_LAUNCH(ctx, "hw_win", k_hw_win, div_up(nh, B), B, 0, (u64)nh, l2, k2s, seg2, ts, ptau, Wms, posmap, W->hw_na,
+              W->hw_ta);
+  }
+  EngShared& sh = W->sh;
+  sh.t = t; sh.next_call = W->L.next_call; sh.heads = W->heads; sh.n_heads = nh;
+  sh.uh_off = W->uh_off; sh.uh_list = W->uh_list;
+  sh.hw_ng = W->hw_ng; sh.hw_tg = W->hw_tg; sh.hw_na = W->hw_na; sh.hw_ta = W->hw_ta;
+  sh.J = P->J; sh.maxstage = P->maxstage; sh.cnt = P->cnt; sh.ohat = P->ohat;
+  sh.utier = W->utier; sh.tier_calls = W->tier_calls;
+  return true;
+}
+
+// ------------------------------------------------------------------ per-scenario setup
+struct ScenParam { u32 alpha, beta, gamma, from_profile, kq8, xrg, tier_max, pad; u64 xtg, C; };
+
+// grid.x = scenario: Eq. 2 weights W[a][j] = floor((alpha SI + beta SS + gamma SO) 2^16 / cnt) and limits
+__global__ void k_scen_setup(u32 A, u32 J, const fs_profile* Pd, const u64* cnt, const u64* s_in, const u64* s_sys,
+                             const u64* s_out, const u32* nr_r_a, const u64* nr_t_a, const u32* nr_r_g,
+                             const u64* nr_t_g, const u32* pT_r_a, const u64* pT_t_a, const u32* pT_r_g,
+                             const u64* pT_t_g, const ScenParam* sp, const u32* xra, const u64* xta, u64* W,
+                             DLimits* L, u32* ra, u64* ta) {
+  u32 s = blockIdx.x;
+  const ScenParam p = sp[s];
+  u64 AJ = (u64)A * (J + 1);
+  for (u64 k = threadIdx.x; k < AJ; k += blockDim.x) {
+    u64 c = cnt[k];
+    u64 w = 0;
+    if (c) {
+      u128 Sw = (u128)p.alpha * s_in[k] + (u128)p.beta * s_sys[k] + (u128)p.gamma * s_out[k];
+      w = (u64)((Sw << 16) / c);
+    }
+    W[(u64)s * AJ + k] = w;
+  }
+  (void)Pd;
+  if (threadIdx.x == 0) {
+    auto lim = [&](u64 nr) -> u64 { if (!nr) return 0; u128 v = ((u128)p.kq8 * nr + 255) >> 8; return v < 1 ? 1 : (u64)v; };
+    DLimits l; l.pad = 0;
+    u32* r = ra + (u64)s * A; u64* tt = ta + (u64)s * A;
+    if (p.kq8 == 0xFFFFFFFFu) { l.rg = 0; l.tg = 0; for (u32 a = 0; a < A; a++) { r[a] = 0; tt[a] = 0; } }
+    else if (p.from_profile) {
+      if (p.kq8 == 0) { l.rg = *pT_r_g; l.tg = *pT_t_g; for (u32 a = 0; a < A; a++) { r[a] = pT_r_a[a]; tt[a] = pT_t_a[a]; } }
+      else { l.rg = (u32)lim(*nr_r_g); l.tg = lim(*nr_t_g);
+             for (u32 a = 0; a < A; a++) { r[a] = (u32)lim(nr_r_a[a]); tt[a] = lim(nr_t_a[a]); } }
+    } else {
+      l.rg = p.xrg; l.tg = p.xtg;
+      for (u32 a = 0; a < A; a++) { r[a] = xra[(u64)s * A + a]; tt[a] = xta[(u64)s * A + a]; }
+    }
+    u32 tok = l.tg != 0;
+    for (u32 a = 0; a < A; a++) tok |= tt[a] != 0;
+    l.tokens = tok;
+    L[s] = l;
+  }
+}
+
+// grid (blocks, scenario): every participating call needs a profile slot with W > 0
+// (FS_E_PROFILE) and prompt + reserve <= C (FS_E_OVERSIZE); min index per code.
+__global__ void k_scen_check(DTrace t, u32 J, const u32* maxstage, const u64* cnt, const u64* ohat, const u64* W,
+                             const ScenParam* sp, unsigned long long* bad /* [scen][2] */) {
+  u32 s = blockIdx.y;
+  const ScenParam p = sp[s];
+  u64 AJ = (u64)t.A * (J + 1);
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < t.n; i += (u64)gridDim.x * blockDim.x) {
+    u32 m = t.meta[i];
+    if (m_tier(m) > p.tier_max) continue;
+    u64 k;
+    if (!prof_slot(J, maxstage, cnt, m_app(m), m_stage(m), &k) || W[(u64)s * AJ + k] == 0) {
+      atomicMin(&bad[2 * s], (unsigned long long)i);
+      continue;
+    }
+    if ((u64)t.len_in[i] + t.len_sys[i] + ohat[k] > p.C) atomicMin(&bad[2 * s + 1], (unsigned long long)i);
+  }
+}
+
+__global__ void k_replay_pre(DTrace t, u32 tier_max, fs_replay_out o) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n) return;
+  if (o.status) o.status[i] = m_tier(t.meta[i]) > tier_max ? FS_ST_FILTERED : FS_ST_NOT_ARRIVED;
+  if (o.overloaded_at_arrival) o.overloaded_at_arrival[i] = 0;
+  if (o.arrive_ns) o.arrive_ns[i] = -1;
+  if (o.admit_ns) o.admit_ns[i] = -1;
+  if (o.first_ns) o.first_ns[i] = -1;
+  if (o.finish_ns) o.finish_ns[i] = -1;
+  if (o.order) o.order[i] = NONE32;
+}
+__global__ void k_replay_post(DTrace t, const u32* head_of, uint8_t* status) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n || !status) return;
+  if (status[i] == FS_ST_NOT_ARRIVED && m_stage(t.meta[i]) > 1) {
+    uint8_t hs = status[head_of[i]];
+    if (hs >= FS_ST_BLOCK_USER_REQ && hs <= FS_ST_BLOCK_APP_TOK) status[i] = FS_ST_DROPPED;
+  }
+}
+
+static bool replay_cfg_ok(const fs_replay_cfg* c) {
+  return c && c->mode <= 1 && c->alpha < 256 && c->beta < 256 && c->gamma < 256 && c->prio_benign_q16 < (1u << 24) &&
+         c->prio_abusive_q16 < (1u << 24) && c->max_batch >= 1 && (c->mode == 0 || act_cfg_ok(&c->act));
+}
+
+static ScenParam scen_param(const fs_replay_cfg* c) {
+  ScenParam p;
+  memset(&p, 0, sizeof(p));
+  p.alpha = c->alpha; p.beta = c->beta; p.gamma = c->gamma;
+  p.from_profile = c->act.limits_from_profile; p.kq8 = c->mode == FS_MODE_WI ? c->act.limit_mult_q8 : 0xFFFFFFFFu;
+  p.xrg = c->act.T_req_g; p.xtg = c->act.T_tok_g; p.tier_max = c->tier_max; p.C = c->kv_capacity;
+  return p;
+}
+
+// per-scenario device tables for n configs: W tables, limits, checks.  Returns first error per scenario.
+struct ScenTables { u64* W; DLimits* L; u32* ra; u64* ta; unsigned long long* bad; ScenParam* sp; };
+static bool scen_tables(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profile* P, const fs_replay_cfg* cfgs, u32 ns,
+                        ScenTables* T) {
+  u32 A = t.A;
+  u64 AJ = (u64)A * (P->J + 1);
+  std::vector<ScenParam> hp(ns);
+  std::vector<u32> hra((size_t)ns * A, 0);
+  std::vector<u64> hta((size_t)ns * A, 0);
+  for (u32 s = 0; s < ns; s++) {
+    hp[s] = scen_param(&cfgs[s]);
+    if (cfgs[s].mode == FS_MODE_WI && !cfgs[s].act.limits_from_profile) {
+      if (cfgs[s].act.T_req_a_h) for (u32 a = 0; a < A; a++) hra[(size_t)s * A + a] = cfgs[s].act.T_req_a_h[a];
+      if (cfgs[s].act.T_tok_a_h) for (u32 a = 0; a < A; a++) hta[(size_t)s * A + a] = cfgs[s].act.T_tok_a_h[a];
+    }
+  }
+  T->sp = S.alloc<ScenParam>(ns); T->W = S.alloc<u64>(ns * AJ); T->L = S.alloc<DLimits>(ns);
+  T->ra = S.alloc<u32>((size_t)ns * A); T->ta = S.alloc<u64>((size_t)ns * A);
+  u32* xra = S.alloc<u32>((size_t)ns * A); u64* xta = S.alloc<u64>((size_t)ns * A);
+  T->bad = S.alloc<unsigned long long>(2 * (size_t)ns);
+  if (S.failed) return false;
+  cudaMemcpyAsync(T->sp, hp.data(), ns * sizeof(ScenParam), cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(xra, hra.data(), hra.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemcpyAsync(xta, hta.data(), hta.size() * 8, cudaMemcpyHostToDevice, ctx->stream);
+  cudaMemsetAsync(T->bad, 0xFF, 2 * (size_t)ns * 8, ctx->stream);
+  FS_LAUNCH(ctx, "scen_setup", k_scen_setup, ns, 256, 0, A, P->J, P, P->cnt, P->sum_in, P->sum_sys, P->sum_out,
+            P->nr_peak_r_a, P->nr_peak_t_a, P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g,
+            P->T_tok_g, T->sp, xra, xta, T->W, T->L, T->ra, T->ta);
+  if (t.n) {
+    dim3 g(std::max(1, std::min(div_up(t.n, 256 * 8), 4 * ctx->sm_count)), ns);
+    FS_LAUNCH(ctx, "scen_check", k_scen_check, g, 256, 0, t, P->J, P->maxstage, P->cnt, P->ohat, T->W, T->sp, T->bad);
+  }
+  return true;
+}
+
+static EngCfg eng_cfg(const fs_replay_cfg* c, const ScenTables& T, u32 s, u32 A, u64 AJ, const DLimits& hl) {
+  EngCfg e;
+  e.mode = c->mode; e.alpha = c->alpha; e.beta = c->beta; e.gamma = c->gamma;
+  e.prio_b = c->prio_benign_q16; e.prio_a = c->prio_abusive_q16; e.prio_q16 = c->prio_q16;
+  e.C = c->kv_capacity; e.Bmax = c->max_batch; e.theta = c->overload_permille;
+  e.base = c->iter_base_ns; e.dec = c->decode_ns_per_req; e.pre = c->prefill_ns_per_tok;
+  e.tier_max = c->tier_max; e.heads_only = c->act.count_mode == FS_COUNT_HEADS_ONLY;
+  e.Wns = (i64)c->act.window_ms * 1000000;
+  e.L = hl; e.ra = T.ra + (u64)s * A; e.ta = T.ta + (u64)s * A; e.W = T.W + (u64)s * AJ;
+  return e;
+}
+
+// ------------------------------------------------------------------ fs_wsc_replay
+extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
+                             const fs_replay_out* out, fs_replay_summary* sum) {
+  if (!ctx || !tr || !P || !sum || !replay_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
+  memset(sum, 0, sizeof(*sum));
+  if (P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
+  Scratch S(ctx);
+  err_reset(ctx);
+  DTrace t = dtrace(tr);
+  fs_replay_out o;
+  memset(&o, 0, sizeof(o));
+  if (out) o = *out;
+  WscShared W;
+  if (!wsc_shared(ctx, S, t, P, cfg->act.window_ms, cfg->mode == FS_MODE_WI, &W)) return FS_E_NOMEM;
+  int rc = finish(ctx, &S);
+  if (rc) return rc;
+  ScenTables T;
+  if (!scen_tables(ctx, S, t, P, cfg, 1, &T)) return FS_E_NOMEM;
+  unsigned long long hbad[2];
+  DLimits hl;
+  cudaMemcpyAsync(hbad, T.bad, 16, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&hl, T.L, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) return rc;
+  if (hbad[0] != ~0ull) { ctx->bad_index = hbad[0]; snprintf(ctx->msg, sizeof(ctx->msg), "profile slot"); return FS_E_PROFILE; }
+  if (hbad[1] != ~0ull) { ctx->bad_index = hbad[1]; snprintf(ctx->msg, sizeof(ctx->msg), "oversize"); return FS_E_OVERSIZE; }
+  int B = 256;
+  if (t.n) FS_LAUNCH(ctx, "replay_pre", k_replay_pre, div_up(t.n, B), B, 0, t, cfg->tier_max, o);
+  if (o.admitted_per_app) cudaMemsetAsync(o.admitted_per_app, 0, t.A * 8, ctx->stream);
+  u64 AJ = (u64)t.A * (P->J + 1);
+  EngCfg ec = eng_cfg(cfg, T, 0, t.A, AJ, hl);
+  u32 p_cap = std::max<u32>(t.X, 1);
+  size_t budget = ctx->smem_optin ? ctx->smem_optin - 512 : 100 * 1024;
+  EngLayout L = eng_layout(t.U, t.X, W.n_heads, cfg->max_batch, p_cap, cfg->mode == FS_MODE_WI, budget);
+  unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
+  fs_replay_summary* dsum = S.alloc<fs_replay_summary>(1);
+  int* dcode = S.zeros<int>(1);
+  u64* didx = S.zeros<u64>(1);
+  if (S.failed) return FS_E_NOMEM;
+  EngOut eo;
+  eo.status = o.status; eo.ovl = o.overloaded_at_arrival; eo.arrive = o.arrive_ns; eo.admit = o.admit_ns;
+  eo.first = o.first_ns; eo.finish = o.finish_ns; eo.order = o.order; eo.counters = o.counters;
+  eo.adm_app = o.admitted_per_app;
+  if (eo.arrive && !eo.ovl) eo.arrive = nullptr;          // arrive/ovl are written together
+  if (eo.admit && !eo.order) eo.admit = nullptr;
+  ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
+  cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
+  FS_LAUNCH(ctx, "wsc_replay", k_replay, 1, 32, L.bytes_smem, a);
+  if (t.n && o.status) FS_LAUNCH(ctx, "replay_post", k_replay_post, div_up(t.n, B), B, 0, t, W.L.head_of, o.status);
+  int hcode = 0; u64 hidx = 0;
+  cudaMemcpyAsync(sum, dsum, sizeof(*sum), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) return rc;
+  if (hcode) {
+    static const int codes[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
+    ctx->bad_index = hidx;
+    return codes[hcode - 1];
+  }
+  return FS_OK;
+}
+
+// ------------------------------------------------------------------ fs_sweep
+extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* scen, uint32_t ns,
+                        fs_replay_summary* out, int32_t* codes) {
+  if (!ctx || !tr || !P || !scen || !out || !codes || tr->n_apps == 0) return FS_E_INVAL;
+  if (ns == 0) return FS_OK;
+  bool any_wi = false;
+  u32 Bmax = 1;
+  for (u32 s = 0; s < ns; s++) {
+    if (!replay_cfg_ok(&scen[s]) || scen[s].prio_q16) return FS_E_INVAL;
+    if (scen[s].mode == FS_MODE_WI) {
+      if (any_wi && scen[s].act.window_ms != scen[0].act.window_ms) return FS_E_INVAL;   // one static window per call
+      any_wi = true;
+    }
+    Bmax = std::max(Bmax, scen[s].max_batch);
+  }
+  if (P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
+  Scratch S(ctx);
+  err_reset(ctx);
+  DTrace t = dtrace(tr);
+  u32 win = scen[0].act.window_ms;
+  for (u32 s = 0; s < ns; s++) if (scen[s].mode == FS_MODE_WI) { win = scen[s].act.window_ms; break; }
+  WscShared W;
+  if (!wsc_shared(ctx, S, t, P, win, any_wi, &W)) return FS_E_NOMEM;
+  int rc = finish(ctx, &S);
+  if (rc) return rc;
+  ScenTables T;
+  if (!scen_tables(ctx, S, t, P, scen, ns, &T)) return FS_E_NOMEM;
+  std::vector<unsigned long long> hbad(2 * (size_t)ns);
+  std::vector<DLimits> hl(ns);
+  cudaMemcpyAsync(hbad.data(), T.bad, hbad.size() * 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(hl.data(), T.L, ns * sizeof(DLimits), cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) return rc;
+  u64 AJ = (u64)t.A * (P->J + 1);
+  std::vector<EngCfg> hc(ns);
+  for (u32 s = 0; s < ns; s++) hc[s] = eng_cfg(&scen[s], T, s, t.A, AJ, hl[s]);
+  EngCfg* dc = S.alloc<EngCfg>(ns);
+  fs_replay_summary* dsum = S.zeros<fs_replay_summary>(ns);
+  int* dcodes = S.zeros<int>(ns);
+  u32* next = S.zeros<u32>(1);
+  if (S.failed) return FS_E_NOMEM;
+  cudaMemcpyAsync(dc, hc.data(), ns * sizeof(EngCfg), cudaMemcpyHostToDevice, ctx->stream);
+  u32 p_cap = std::max<u32>(std::min<u32>(t.X, 1u << 16), 1);
+  EngLayout L = eng_layout(t.U, t.X, W.n_heads, Bmax, p_cap, any_wi, 0);
+  size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  u64 slots = std::min<u64>(ns, (u64)ctx->sm_count * 16);
+  u64 by_mem = (u64)(free_b / 2) / std::max<size_t>(slot_bytes, 1);
+  slots = std::max<u64>(1, std::min(slots, by_mem));
+  slots = (slots + 3) / 4 * 4;                      // 4 warps per CTA
+  unsigned char* gm = S.alloc<unsigned char>(slots * slot_bytes + 256);
+  if (S.failed) return FS_E_NOMEM;
+  SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next};
+  FS_LAUNCH(ctx, "wsc_sweep", k_sweep, (u32)(slots / 4), 128, 0, a);
+  std::vector<int> hcodes(ns);
+  cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) return rc;
+  static const int cmap[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
+  for (u32 s = 0; s < ns; s++) {
+    codes[s] = hcodes[s] ? cmap[hcodes[s] - 1] : FS_OK;
+    if (hbad[2 * s] != ~0ull) codes[s] = FS_E_PROFILE;
+    else if (hbad[2 * s + 1] != ~0ull) codes[s] = FS_E_OVERSIZE;
+    if (codes[s] != FS_OK) memset(&out[s], 0, sizeof(out[s]));
+  }
+  return FS_OK;
+}
+
+// ------------------------------------------------------------------ fs_wsc_step
+struct fs_wsc_state {
+  fs_ctx* ctx;
+  Scratch* S;
+  WscShared W;
+  ScenTables T;
+  EngCfg ec;
+  EngLayout L;
+  unsigned char* gm;
+  i64* scal;
+  u32 p_cap, U;
+  DTrace t;
+  ~fs_wsc_state() { delete S; }
+};
+
+__global__ void k_step_init(EngLayout L, unsigned char* gm, u32 p_cap, u32 U, u64 n_heads, i64* scal) {
+  EngState st;
+  eng_bind(L, nullptr, gm, p_cap, &st);
+  eng_clear(st, U, n_heads, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0) { scal[0] = -1; scal[1] = 0; scal[2] = 0; scal[3] = 0; }
+}
+
+extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
+                                   fs_wsc_state** out) {
+  if (!ctx || !tr || !P || !out || !replay_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
+  *out = nullptr;
+  if (P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
+  fs_wsc_state* st = new fs_wsc_state();
+  st->ctx = ctx;
+  st->S = new Scratch(ctx);
+  Scratch& S = *st->S;
+  err_reset(ctx);
+  st->t = dtrace(tr);
+  st->U = tr->n_users;
+  if (!wsc_shared(ctx, S, st->t, P, cfg->act.window_ms, false, &st->W)) { delete st; return FS_E_NOMEM; }
+  int rc = finish(ctx, &S);
+  if (rc) { delete st; return rc; }
+  if (!scen_tables(ctx, S, st->t, P, cfg, 1, &st->T)) { delete st; return FS_E_NOMEM; }
+  unsigned long long hbad[2];
+  DLimits hl;
+  cudaMemcpyAsync(hbad, st->T.bad, 16, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&hl, st->T.L, sizeof(hl), cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (!rc && hbad[0] != ~0ull) { ctx->bad_index = hbad[0]; rc = FS_E_PROFILE; }
+  if (!rc && hbad[1] != ~0ull) { ctx->bad_index = hbad[1]; rc = FS_E_OVERSIZE; }
+  if (rc) { delete st; return rc; }
+  st->ec = eng_cfg(cfg, st->T, 0, tr->n_apps, (u64)tr->n_apps * (P->J + 1), hl);
+  st->p_cap = 1;
+  st->L = eng_layout(st->U, st->t.X, st->W.n_heads, cfg->max_batch, st->p_cap, cfg->mode == FS_MODE_WI, 0);
+  st->gm = S.alloc<unsigned char>(st->L.bytes_glob + 256);
+  st->scal = S.alloc<i64>(4);
+  if (S.failed) { delete st; return FS_E_NOMEM; }
+  FS_LAUNCH(ctx, "step_init", k_step_init, 1, 256, 0, st->L, st->gm, st->p_cap, st->U, st->W.n_heads, st->scal);
+  rc = finish(ctx, &S);
+  if (rc) { delete st; return rc; }
+  *out = st;
+  return FS_OK;
+}
+
+extern "C" int fs_wsc_step(fs_ctx* ctx, fs_wsc_state* st, int64_t now_ns, int64_t occ, uint32_t batch,
+                           const uint32_t* fin, uint32_t nfin, const uint32_t* arr, const int64_t* arr_t, uint32_t narr,
+                           uint8_t* arr_status, uint32_t* admitted, uint32_t* n_admitted) {
+  (void)now_ns;
+  if (!ctx || !st || !n_admitted || (nfin && !fin) || (narr && (!arr || !arr_t || !arr_status)) || !admitted)
+    return FS_E_INVAL;
+  Scratch S(ctx);
+  err_reset(ctx);
+  int* dcode = S.zeros<int>(1);
+  u64* didx = S.zeros<u64>(1);
+  u32* dn = S.zeros<u32>(1);
+  if (S.failed) return FS_E_NOMEM;
+  StepKArgs a{st->W.sh, st->ec, st->L, st->U, st->gm, st->p_cap, st->scal, occ, batch, fin, nfin, arr, arr_t, narr,
+              arr_status, admitted, dn, dcode, didx};
+  FS_LAUNCH(ctx, "wsc_step", k_step, 1, 32, 0, a);
+  int hcode = 0; u64 hidx = 0;
+  cudaMemcpyAsync(n_admitted, dn, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  int rc = finish(ctx, &S);
+  if (rc) return rc;
+  if (hcode) {
+    static const int codes[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
+    ctx->bad_index = hidx;
+    return codes[hcode - 1];
+  }
+  return FS_OK;
+}
+
+extern "C" int fs_wsc_state_read(fs_ctx* ctx, const fs_wsc_state* st, uint64_t* counters, int32_t* last_exit) {
+  if (!ctx || !st || !counters || !last_exit) return FS_E_INVAL;
+  Scratch S(ctx);
+  u64* d = S.alloc<u64>(st->U + 1);
+  if (S.failed) return FS_E_NOMEM;
+  EngState es;
+  // the counters array is the first global array of the step layout
+  const u64* u = (const u64*)(st->gm + st->L.off[L_U]);
+  FS_LAUNCH(ctx, "step_read", k_step_read, div_up(st->U + 1, 256), 256, 0, st->U, u, d);
+  (void)es;
+  i64 e = -1;
+  cudaMemcpyAsync(counters, d, st->U * 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&e, st->scal, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  int rc = finish(ctx, &S);
+  *last_exit = (int32_t)e;
+  return rc;
+}
+
+extern "C" void fs_wsc_state_free(fs_wsc_state* st) { delete st; }

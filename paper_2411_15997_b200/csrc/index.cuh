@@ -1,0 +1,159 @@
+// index.cuh -- K0 trace validation + interaction links, K1/K2 per-user and
+// per-(user, app) (t, id)-ordered index (stable radix sort + segment bounds).
+#pragma once
+#include "common.cuh"
+
+struct DTrace {   // device view of fs_trace
+  u64 n; u32 U, A, X;
+  const u32 *user, *t_ms, *len_in, *len_sys, *len_out, *think_ms, *inter, *meta;
+};
+__device__ __forceinline__ u32 m_app(u32 m) { return m & 255u; }
+__device__ __forceinline__ u32 m_stage(u32 m) { return (m >> 8) & 255u; }
+__device__ __forceinline__ u32 m_ncalls(u32 m) { return (m >> 16) & 255u; }
+__device__ __forceinline__ u32 m_tier(u32 m) { return m >> 24; }
+
+static inline DTrace dtrace(const fs_trace* t) {
+  DTrace d;
+  d.n = t->n_calls; d.U = t->n_users; d.A = t->n_apps; d.X = t->n_inters;
+  d.user = t->user; d.t_ms = t->t_ms; d.len_in = t->len_in; d.len_sys = t->len_sys;
+  d.len_out = t->len_out; d.think_ms = t->think_ms; d.inter = t->inter; d.meta = t->meta;
+  return d;
+}
+
+__device__ __forceinline__ bool rec_range_ok(const DTrace& t, u64 i) {
+  const u32 LMAX = 1u << 24;
+  u32 m = t.meta[i], st = m_stage(m), nc = m_ncalls(m);
+  return t.user[i] < t.U && m_app(m) < t.A && t.inter[i] < t.X && st != 0 && nc != 0 && st <= nc &&
+         t.len_in[i] < LMAX && t.len_sys[i] < LMAX && t.len_out[i] < LMAX && t.len_out[i] != 0;
+}
+
+// pass 1: range, time order, head of each interaction (min index with stage 1)
+__global__ void k_val_range(DTrace t, DevErr* err, u32* head_of_inter) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n) return;
+  if (!rec_range_ok(t, i)) { report(err, ERR_RANGE, i); return; }
+  if (i > 0 && t.t_ms[i] < t.t_ms[i - 1]) report(err, ERR_ORDER, i);
+  if (m_stage(t.meta[i]) == 1) atomicMin(&head_of_inter[t.inter[i]], (u32)i);
+}
+
+__global__ void k_val_nslots(DTrace t, const u32* head_of_inter, u64* nslots) {
+  u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= t.X) return;
+  u32 h = head_of_inter[x];
+  nslots[x] = h == NONE32 ? 0 : m_ncalls(t.meta[h]);
+}
+
+__device__ __forceinline__ bool head_consistent(const DTrace& t, u64 i, u32 h) {
+  if (h == NONE32) return false;
+  u32 mi = t.meta[i], mh = t.meta[h];
+  return t.user[i] == t.user[h] && m_app(mi) == m_app(mh) && m_ncalls(mi) == m_ncalls(mh);
+}
+
+__global__ void k_val_slots(DTrace t, DevErr* err, const u32* head_of_inter, const u64* off, u32* slot) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n || !rec_range_ok(t, i)) return;
+  u32 x = t.inter[i];
+  u32 h = head_of_inter[x];
+  if (!head_consistent(t, i, h)) { report(err, ERR_ORDER, i); return; }
+  atomicMin(&slot[off[x] + m_stage(t.meta[i]) - 1], (u32)i);
+}
+
+__global__ void k_val_links(DTrace t, DevErr* err, const u32* head_of_inter, const u64* off, const u32* slot,
+                            u32* head_of, u32* next_call) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n || !rec_range_ok(t, i)) return;
+  u32 x = t.inter[i];
+  if (!head_consistent(t, i, head_of_inter[x])) return;
+  u32 m = t.meta[i], s = m_stage(m), nc = m_ncalls(m);
+  u64 o = off[x];
+  bool bad = slot[o + s - 1] != (u32)i;
+  if (s > 1) { u32 p = slot[o + s - 2]; if (p == NONE32 || p > (u32)i) bad = true; }
+  u32 nx = NONE32;
+  if (s < nc) { nx = slot[o + s]; if (nx == NONE32) bad = true; }
+  if (bad) report(err, ERR_ORDER, i);
+  head_of[i] = slot[o];
+  next_call[i] = nx;
+}
+
+struct Links { u32* head_of; u32* next_call; };
+
+// Validate the trace; fills head_of / next_call (device, n each).  Errors land in ctx->err.
+static bool build_links(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
+  u64 n = t.n;
+  L->head_of = S.alloc<u32>(n);
+  L->next_call = S.alloc<u32>(n);
+  u32* hoi = S.alloc<u32>(t.X + 1);
+  u64* nsl = S.alloc<u64>(t.X + 1);
+  u64* off = S.alloc<u64>(t.X + 1);
+  if (S.failed) return false;
+  cudaMemsetAsync(hoi, 0xFF, (t.X + 1) * 4, ctx->stream);
+  int B = 256;
+  if (n) FS_LAUNCH(ctx, "val_range", k_val_range, div_up(n, B), B, 0, t, ctx->err, hoi);
+  if (t.X) FS_LAUNCH(ctx, "val_nslots", k_val_nslots, div_up(t.X, B), B, 0, t, hoi, nsl);
+  excl_scan<u64>(ctx, S, nsl, off, t.X, off + t.X);
+  u64 total = 0;
+  cudaMemcpyAsync(&total, off + t.X, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  u32* slot = S.alloc<u32>(total + 1);
+  if (S.failed) return false;
+  cudaMemsetAsync(slot, 0xFF, (total + 1) * 4, ctx->stream);
+  if (n) {
+    FS_LAUNCH(ctx, "val_slots", k_val_slots, div_up(n, B), B, 0, t, ctx->err, hoi, off, slot);
+    FS_LAUNCH(ctx, "val_links", k_val_links, div_up(n, B), B, 0, t, ctx->err, hoi, off, slot, L->head_of, L->next_call);
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ (t, id)-ordered index
+__global__ void k_key_user(DTrace t, u32* key) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n) key[i] = t.user[i];
+}
+__global__ void k_key_user_app(DTrace t, u32* key) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n) key[i] = t.user[i] * t.A + m_app(t.meta[i]);
+}
+
+struct Order {      // a stable (key, t, id) order of all calls
+  u32* key;         // sorted keys (segment id per position)
+  u32* perm;        // call id per position
+  u64* seg;         // [nseg + 1] segment offsets
+  u64 nseg;
+};
+
+// by_app = false: key = user (U segments); true: key = user * A + app (U*A segments).
+// The input order is (t_ms, id) so a stable sort yields (key, t, id).
+static bool build_order(fs_ctx* ctx, Scratch& S, const DTrace& t, bool by_app, Order* o) {
+  u64 n = t.n;
+  u32* k0 = S.alloc<u32>(n);
+  if (S.failed) return false;
+  int B = 256;
+  if (n) {
+    if (by_app) FS_LAUNCH(ctx, "key_user_app", k_key_user_app, div_up(n, B), B, 0, t, k0);
+    else FS_LAUNCH(ctx, "key_user", k_key_user, div_up(n, B), B, 0, t, k0);
+  }
+  o->nseg = by_app ? (u64)t.U * t.A : t.U;
+  if (!radix_sort<u32>(ctx, S, k0, nullptr, n, bits_for(o->nseg ? o->nseg - 1 : 0), &o->key, &o->perm)) return false;
+  o->seg = S.alloc<u64>(o->nseg + 1);
+  if (S.failed) return false;
+  FS_LAUNCH(ctx, "seg_bounds", k_seg_bounds<u32>, div_up(o->nseg + 1, B), B, 0, o->key, n, o->nseg, o->seg);
+  return true;
+}
+
+// ------------------------------------------------------------------ window lower bound
+// First position q in [s, p] with ts[q] > thr (ts nondecreasing on [s, p]; ts[p] > thr).
+// Galloping back from p then binary search: windows are short for most calls.
+template <class T>
+__device__ __forceinline__ u64 window_lb(const T* ts, u64 s, u64 p, i64 thr) {
+  u64 k = 1, good = p;                           // invariant: ts[good] > thr
+  while (p >= s + k) {
+    u64 q = p - k;
+    if ((i64)ts[q] > thr) { good = q; k <<= 1; continue; }
+    u64 lo = q + 1, hi = good;                    // answer in (q, good]
+    while (lo < hi) { u64 m = (lo + hi) >> 1; if ((i64)ts[m] > thr) hi = m; else lo = m + 1; }
+    return lo;
+  }
+  u64 lo = s, hi = good;
+  while (lo < hi) { u64 m = (lo + hi) >> 1; if ((i64)ts[m] > thr) hi = m; else lo = m + 1; }
+  return lo;
+}

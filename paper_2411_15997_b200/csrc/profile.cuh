@@ -1,0 +1,473 @@
+// profile.cuh -- fs_build_app_profiles: K3 sums + K4 histograms (one streaming
+// pass), K5 window peaks, K6 exact quantiles by histogram refinement, limits.
+// PAPER.md: Eq. 2 inputs N-bar "based on historical statistics";
+// per-app "normal range"; limits "based on the analysis of
+// historical data".  Readings Q8, Q9, Q23, Q30.
+#pragma once
+#include "index.cuh"
+
+static const int NBINS = 240, NF = 5;
+static const int QMAX = 16;              // max reported quantiles
+static const int QW = 11;                // refinement: 2^11 sub-bins per level
+
+struct fs_profile {
+  u32 A = 0, J = 0, U = 0, nq = 0;
+  std::vector<u32> q_ppm;
+  void* block = nullptr;                  // one device allocation for everything below
+  u64 *cnt, *sum_in, *sum_sys, *sum_out, *ohat;   // [A][J1]
+  u32* maxstage;                                  // [A]
+  u64* hist;                                      // [A][5][240]
+  u64* n_app;                                     // [A]
+  u32* nr_q; double* interp_q;                    // [A][4][nq]
+  u32* peak_r_u; u64* peak_t_u;                   // [U]
+  u32* peak_r_ua; u64* peak_t_ua;                 // [U][A]
+  u32* nr_peak_r_a; u64* nr_peak_t_a;             // [A]
+  u32* nr_peak_r_g; u64* nr_peak_t_g;             // [1]
+  u32* T_req_a; u64* T_tok_a;                     // [A]
+  u32* T_req_g; u64* T_tok_g;                     // [1]
+  // host mirrors of the small tables ACT / replay resolve limits and weights from
+  std::vector<u64> h_cnt, h_sum_in, h_sum_sys, h_sum_out;
+  std::vector<u32> h_maxstage, h_nr_peak_r_a, h_T_req_a;
+  std::vector<u64> h_nr_peak_t_a, h_T_tok_a;
+  u32 h_nr_peak_r_g = 0, h_T_req_g = 0;
+  u64 h_nr_peak_t_g = 0, h_T_tok_g = 0;
+};
+
+template <class T> static T* carve(char*& p, size_t n) {
+  T* r = (T*)p;
+  p += ((n * sizeof(T) + 255) / 256) * 256;
+  return r;
+}
+
+static fs_profile* profile_alloc(u32 A, u32 J, u32 U, u32 nq) {
+  fs_profile* P = new fs_profile();
+  P->A = A; P->J = J; P->U = U; P->nq = nq;
+  u64 J1 = J + 1;
+  size_t bytes = 0;
+  auto add = [&](size_t b) { bytes += ((b + 255) / 256) * 256; };
+  for (int k = 0; k < 5; k++) add(A * J1 * 8);
+  add(A * 4); add((size_t)A * NF * NBINS * 8); add(A * 8);
+  add((size_t)A * 4 * nq * 4); add((size_t)A * 4 * nq * 8);
+  add(U * 4); add(U * 8); add((size_t)U * A * 4); add((size_t)U * A * 8);
+  add(A * 4); add(A * 8); add(4); add(8); add(A * 4); add(A * 8); add(4); add(8);
+  if (cudaMalloc(&P->block, bytes) != cudaSuccess) { delete P; return nullptr; }
+  cudaMemset(P->block, 0, bytes);
+  char* p = (char*)P->block;
+  P->cnt = carve<u64>(p, A * J1); P->sum_in = carve<u64>(p, A * J1); P->sum_sys = carve<u64>(p, A * J1);
+  P->sum_out = carve<u64>(p, A * J1); P->ohat = carve<u64>(p, A * J1);
+  P->maxstage = carve<u32>(p, A); P->hist = carve<u64>(p, (size_t)A * NF * NBINS); P->n_app = carve<u64>(p, A);
+  P->nr_q = carve<u32>(p, (size_t)A * 4 * nq); P->interp_q = carve<double>(p, (size_t)A * 4 * nq);
+  P->peak_r_u = carve<u32>(p, U); P->peak_t_u = carve<u64>(p, U);
+  P->peak_r_ua = carve<u32>(p, (size_t)U * A); P->peak_t_ua = carve<u64>(p, (size_t)U * A);
+  P->nr_peak_r_a = carve<u32>(p, A); P->nr_peak_t_a = carve<u64>(p, A);
+  P->nr_peak_r_g = carve<u32>(p, 1); P->nr_peak_t_g = carve<u64>(p, 1);
+  P->T_req_a = carve<u32>(p, A); P->T_tok_a = carve<u64>(p, A);
+  P->T_req_g = carve<u32>(p, 1); P->T_tok_g = carve<u64>(p, 1);
+  return P;
+}
+
+static void profile_mirror(fs_profile* P, cudaStream_t s) {   // device -> host mirrors of small tables
+  u64 n = (u64)P->A * (P->J + 1);
+  P->h_cnt.resize(n); P->h_sum_in.resize(n); P->h_sum_sys.resize(n); P->h_sum_out.resize(n);
+  P->h_maxstage.resize(P->A); P->h_nr_peak_r_a.resize(P->A); P->h_T_req_a.resize(P->A);
+  P->h_nr_peak_t_a.resize(P->A); P->h_T_tok_a.resize(P->A);
+  cudaMemcpyAsync(P->h_cnt.data(), P->cnt, n * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_sum_in.data(), P->sum_in, n * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_sum_sys.data(), P->sum_sys, n * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_sum_out.data(), P->sum_out, n * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_maxstage.data(), P->maxstage, P->A * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_nr_peak_r_a.data(), P->nr_peak_r_a, P->A * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_nr_peak_t_a.data(), P->nr_peak_t_a, P->A * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_T_req_a.data(), P->T_req_a, P->A * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(P->h_T_tok_a.data(), P->T_tok_a, P->A * 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&P->h_nr_peak_r_g, P->nr_peak_r_g, 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&P->h_nr_peak_t_g, P->nr_peak_t_g, 8, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&P->h_T_req_g, P->T_req_g, 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&P->h_T_tok_g, P->T_tok_g, 8, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+}
+
+// ------------------------------------------------------------------ K3 + K4 streaming pass
+// Persistent grid-stride CTAs.  Sums: warp-aggregated by (app, stage') with
+// __match_any_sync + __reduce_add_sync, then one shared u64 atomic per group.
+// Histograms: shared u32 bins for apps [a0, a0+na) (blockIdx.y chunks the apps
+// when A*5*240*4 B does not fit next to the sums).  Flush: one global atomic per
+// non-zero shared entry.
+struct ProfStreamArgs {
+  DTrace t; u32 J, tier_max, na_chunk;
+  u64 *cnt, *s_in, *s_sys, *s_out, *hist;
+};
+
+__global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const u32 J1 = a.J + 1, A = a.t.A;
+  const u32 a0 = blockIdx.y * a.na_chunk, na = min(a.na_chunk, A - a0);
+  const bool do_sums = blockIdx.y == 0;
+  u64* ssum = (u64*)sm;                              // [4][A*J1] (only chunk 0)
+  u32* shist = (u32*)(sm + (do_sums ? (size_t)4 * A * J1 * 8 : 0));   // [na][5][240]
+  const u32 nsum = do_sums ? 4 * A * J1 : 0, nh = na * NF * NBINS;
+  for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) ssum[k] = 0;
+  for (u32 k = threadIdx.x; k < nh; k += blockDim.x) shist[k] = 0;
+  __syncthreads();
+  const u64 n = a.t.n;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i0 = (u64)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
+    u64 i = i0 + threadIdx.x;
+    bool ok = i < n;
+    u32 m = ok ? __ldg(&a.t.meta[i]) : 0xFF000000u;
+    ok = ok && m_tier(m) <= a.tier_max;
+    u32 app = m_app(m), st = m_stage(m);
+    u32 Li = 0, Ls = 0, Lo = 0;
+    if (ok) { Li = __ldg(&a.t.len_in[i]); Ls = __ldg(&a.t.len_sys[i]); Lo = __ldg(&a.t.len_out[i]); }
+    if (do_sums) {
+      u32 key = ok ? app * J1 + min(st, a.J) : 0xFFFFFFFFu;
+      u32 peers = __match_any_sync(FULL_MASK, key);
+      u32 ri = __reduce_add_sync(peers, Li), rs = __reduce_add_sync(peers, Ls), ro = __reduce_add_sync(peers, Lo);
+      if (ok && (threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) {
+        atomicAdd((unsigned long long*)&ssum[key], (unsigned long long)__popc(peers));
+        atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)ri);
+        atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)rs);
+        atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)ro);
+      }
+    }
+    if (ok && app >= a0 && app < a0 + na) {
+      u32* h = shist + (app - a0) * NF * NBINS;
+      atomicAdd(&h[0 * NBINS + loglin_bin(Li)], 1u);
+      atomicAdd(&h[1 * NBINS + loglin_bin(Ls)], 1u);
+      atomicAdd(&h[2 * NBINS + loglin_bin(Lo)], 1u);
+      atomicAdd(&h[3 * NBINS + loglin_bin(Li + Ls + Lo)], 1u);
+      if (st == 1) atomicAdd(&h[4 * NBINS + loglin_bin(m_ncalls(m))], 1u);
+    }
+  }
+  __syncthreads();
+  for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) {
+    u64 v = ssum[k];
+    if (v) {
+      u32 arr = k / (A * J1), idx = k % (A * J1);
+      u64* dst = arr == 0 ? a.cnt : arr == 1 ? a.s_in : arr == 2 ? a.s_sys : a.s_out;
+      atomicAdd((unsigned long long*)&dst[idx], (unsigned long long)v);
+    }
+  }
+  for (u32 k = threadIdx.x; k < nh; k += blockDim.x) {
+    u32 v = shist[k];
+    if (v) atomicAdd((unsigned long long*)&a.hist[(u64)a0 * NF * NBINS + k], (unsigned long long)v);
+  }
+}
+
+// maxstage, O-hat = floor(sum_out / cnt), n_app
+__global__ void k_prof_finish(u32 A, u32 J, const u64* cnt, const u64* s_out, u64* ohat, u32* maxstage, u64* n_app) {
+  u32 a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  u32 ms = 0; u64 tot = 0;
+  for (u32 j = 1; j <= J; j++) {
+    u64 k = (u64)a * (J + 1) + j;
+    u64 c = cnt[k];
+    ohat[k] = c ? s_out[k] / c : 0;
+    if (c) ms = j;
+    tot += c;
+  }
+  maxstage[a] = ms;
+  n_app[a] = tot;
+}
+
+// ------------------------------------------------------------------ K5 window peaks
+// Gather the order's times and token loads, exclusive-scan counts and loads, then
+// per position the half-open window (t - W, t] by galloping search (Q4); peaks per
+// segment by a warp segmented max over the sorted keys + one atomicMax per run.
+struct WinGatherArgs {
+  DTrace t; const u32* perm; u32 J, tier_max, heads_only;
+  const u64* ohat;                 // [A][J1]
+  u32* ts; u64* tau; u32* flag;    // per position
+};
+__global__ void k_win_gather(WinGatherArgs a) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= a.t.n) return;
+  u32 i = a.perm[p];
+  u32 m = a.t.meta[i];
+  bool c = m_tier(m) <= a.tier_max && (!a.heads_only || m_stage(m) == 1);
+  a.ts[p] = a.t.t_ms[i];
+  u64 tau = 0;
+  if (c) tau = (u64)a.t.len_in[i] + a.t.len_sys[i] + a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)];
+  a.tau[p] = tau;
+  a.flag[p] = c ? 1u : 0u;
+}
+
+__device__ __forceinline__ void atomic_max_u64(u64* p, u64 v) { atomicMax((unsigned long long*)p, (unsigned long long)v); }
+
+struct WinPeakArgs {
+  u64 n; const u32* key; const u64* seg; const u32* ts; const u64* ptau; const u32* pc; const u32* flag;
+  i64 W;
+  u32* peak_r; u64* peak_t;       // indexed by key
+};
+__global__ void k_win_peaks(WinPeakArgs a) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  bool ok = p < a.n;
+  u32 k = ok ? a.key[p] : NONE32;
+  u32 nr = 0; u64 nt = 0;
+  if (ok && a.flag[p]) {
+    u64 s = a.seg[k];
+    u64 lb = window_lb<u32>(a.ts, s, p, (i64)a.ts[p] - a.W);
+    nr = a.pc[p + 1] - a.pc[lb];
+    nt = a.ptau[p + 1] - a.ptau[lb];
+  }
+  // warp segmented max over runs of equal keys (positions are sorted by key)
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 ko = __shfl_up_sync(FULL_MASK, k, o);
+    u32 ro = __shfl_up_sync(FULL_MASK, nr, o);
+    u64 to = __shfl_up_sync(FULL_MASK, nt, o);
+    if (lane >= o && ko == k) { nr = max(nr, ro); nt = max(nt, to); }
+  }
+  u32 kn = __shfl_down_sync(FULL_MASK, k, 1);
+  bool last = lane == 31 || kn != k;
+  if (ok && last && (nr || nt)) {
+    atomicMax(&a.peak_r[k], nr);
+    atomic_max_u64(&a.peak_t[k], nt);
+  }
+}
+
+// ------------------------------------------------------------------ K6 exact quantiles
+// Per (app, field, q) three order statistics: nearest rank x_(max(1, ceil(q n)))
+// and x_(floor(h)), x_(floor(h)+1) for NumPy 'linear' (h = (n-1) q).  Each rank
+// starts in its 240-bin log-linear bin [lo, lo + 2^w); every refinement level
+// counts the values of the (deduplicated) candidate intervals into 2^11 sub-bins
+// and narrows each rank by 11 bits (<= 3 levels).  Counts are u64 words so the
+// per-level histograms are the multi-GPU allreduce payload.
+struct QState { u64 lo; u64 rw; u32 w; u32 pad; };   // rank interval [lo, lo+2^w), rank within
+struct QIv { u64 lo; u64 off; u32 w; u32 shift; };   // interval, sub-bins 2^(w-shift) at off
+
+__device__ __forceinline__ void q_ranks(u64 n, u32 qppm, u64 r[3], double* frac) {
+  u64 k = ((u128)qppm * n + 999999) / 1000000;
+  if (k < 1) k = 1;
+  if (k > n) k = n;
+  r[0] = k - 1;
+  double h = __dmul_rn((double)(n - 1), __ddiv_rn((double)qppm, 1e6));
+  u64 lo = (u64)floor(h);
+  if (lo > n - 1) lo = n - 1;
+  r[1] = lo;
+  r[2] = lo + 1 < n ? lo + 1 : n - 1;
+  *frac = __dsub_rn(h, (double)lo);
+}
+
+// thread per (a, f): locate each rank's level-1 bin
+__global__ void k_q_init(u32 A, u32 nq, const u32* qppm, const u64* hist, QState* st) {
+  u32 af = blockIdx.x * blockDim.x + threadIdx.x;
+  if (af >= A * 4) return;
+  u32 a = af / 4, f = af % 4;
+  const u64* h = hist + ((u64)a * NF + f) * NBINS;
+  u64 n = 0;
+  for (int b = 0; b < NBINS; b++) n += h[b];
+  for (u32 q = 0; q < nq; q++) {
+    u64 r[3]; double fr;
+    if (n == 0) { for (int k = 0; k < 3; k++) st[((u64)af * nq + q) * 3 + k] = QState{0, 0, 0, 0}; continue; }
+    q_ranks(n, qppm[q], r, &fr);
+    for (int k = 0; k < 3; k++) {
+      u64 cum = 0; int b = 0;
+      for (; b < NBINS; b++) { if (cum + h[b] > r[k]) break; cum += h[b]; }
+      st[((u64)af * nq + q) * 3 + k] = QState{bin_lo(b), r[k] - cum, bin_log2w(b), 0};
+    }
+  }
+}
+
+// thread per (a, f): distinct unresolved intervals; sub-bin counts laid out by a
+// serial prefix in thread order (one CTA of A*4 threads, A*4 <= 1024).
+__global__ void k_q_intervals(u32 A, u32 nq, const QState* st, QIv* iv, u32* niv, u64* total_words) {
+  __shared__ u64 words[1024];
+  u32 af = threadIdx.x;
+  u32 maxi = 3 * nq;
+  u32 c = 0; u64 w = 0;
+  if (af < A * 4) {
+    QIv* mine = iv + (u64)af * maxi;
+    for (u32 r = 0; r < maxi; r++) {
+      QState s = st[(u64)af * maxi + r];
+      if (s.w == 0) continue;
+      bool dup = false;
+      for (u32 k = 0; k < c; k++) if (mine[k].lo == s.lo && mine[k].w == s.w) dup = true;
+      if (dup) continue;
+      u32 shift = s.w > QW ? s.w - QW : 0;
+      mine[c] = QIv{s.lo, w, s.w, shift};
+      w += 1ull << (s.w - shift);
+      c++;
+    }
+    niv[af] = c;
+  }
+  words[af] = w;
+  __syncthreads();
+  if (af == 0) {
+    u64 acc = 0;
+    for (u32 k = 0; k < A * 4; k++) { u64 x = words[k]; words[k] = acc; acc += x; }
+    *total_words = acc;
+  }
+  __syncthreads();
+  if (af < A * 4) for (u32 k = 0; k < c; k++) iv[(u64)af * maxi + k].off += words[af];
+}
+
+// count pass: values inside candidate intervals -> sub-bin counters (u64)
+struct QCountArgs { DTrace t; u32 tier_max, nq; const QIv* iv; const u32* niv; u64* h2; };
+__global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const u32 A = a.t.A, maxi = 3 * a.nq;
+  QIv* siv = (QIv*)sm;                                  // [A*4][maxi]
+  u32* sniv = (u32*)(sm + (size_t)A * 4 * maxi * sizeof(QIv));
+  u32* mask = sniv + A * 4;                             // [A*4][8] bins that hold intervals
+  for (u32 k = threadIdx.x; k < A * 4 * maxi; k += blockDim.x) siv[k] = a.iv[k];
+  for (u32 k = threadIdx.x; k < A * 4; k += blockDim.x) sniv[k] = a.niv[k];
+  for (u32 k = threadIdx.x; k < A * 4 * 8; k += blockDim.x) mask[k] = 0;
+  __syncthreads();
+  for (u32 k = threadIdx.x; k < A * 4 * maxi; k += blockDim.x) {
+    u32 af = k / maxi;
+    if (k % maxi < sniv[af]) {
+      u32 b = loglin_bin((u32)siv[k].lo);
+      atomicOr(&mask[af * 8 + b / 32], 1u << (b % 32));
+    }
+  }
+  __syncthreads();
+  const u64 n = a.t.n, stride = (u64)gridDim.x * blockDim.x;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    u32 m = __ldg(&a.t.meta[i]);
+    if (m_tier(m) > a.tier_max) continue;
+    u32 app = m_app(m);
+    u32 v[4];
+    v[0] = __ldg(&a.t.len_in[i]); v[1] = __ldg(&a.t.len_sys[i]); v[2] = __ldg(&a.t.len_out[i]);
+    v[3] = v[0] + v[1] + v[2];
+#pragma unroll
+    for (int f = 0; f < 4; f++) {
+      u32 af = app * 4 + f, b = loglin_bin(v[f]);
+      if (!(mask[af * 8 + b / 32] & (1u << (b % 32)))) continue;
+      for (u32 k = 0; k < sniv[af]; k++) {
+        const QIv& q = siv[af * maxi + k];
+        if ((u64)v[f] >= q.lo && (u64)v[f] < q.lo + (1ull << q.w)) {
+          atomicAdd((unsigned long long*)&a.h2[q.off + (((u64)v[f] - q.lo) >> q.shift)], 1ull);
+          break;
+        }
+      }
+    }
+  }
+}
+
+// thread per rank: narrow to the sub-bin holding it
+__global__ void k_q_resolve(u32 A, u32 nq, QState* st, const QIv* iv, const u32* niv, const u64* h2) {
+  u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  u32 maxi = 3 * nq;
+  if (r >= (u64)A * 4 * maxi) return;
+  QState s = st[r];
+  if (s.w == 0) return;
+  u32 af = (u32)(r / maxi);
+  for (u32 k = 0; k < niv[af]; k++) {
+    QIv q = iv[(u64)af * maxi + k];
+    if (q.lo != s.lo || q.w != s.w) continue;
+    u64 nb = 1ull << (q.w - q.shift), cum = 0, b = 0;
+    for (; b < nb; b++) { u64 c = h2[q.off + b]; if (cum + c > s.rw) break; cum += c; }
+    s.lo += b << q.shift; s.rw -= cum; s.w = q.shift;
+    st[r] = s;
+    return;
+  }
+}
+
+__global__ void k_q_final(u32 A, u32 nq, const u32* qppm, const u64* hist, const QState* st, u32* nr_q, double* interp) {
+  u32 k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= A * 4 * nq) return;
+  u32 af = k / nq, q = k % nq;
+  const u64* h = hist + ((u64)(af / 4) * NF + af % 4) * NBINS;
+  u64 n = 0;
+  for (int b = 0; b < NBINS; b++) n += h[b];
+  if (n == 0) { nr_q[k] = 0; interp[k] = 0.0; return; }
+  u64 r[3]; double fr;
+  q_ranks(n, qppm[q], r, &fr);
+  const QState* s = st + (u64)k * 3;
+  nr_q[k] = (u32)s[0].lo;
+  double vlo = (double)s[1].lo, vhi = (double)s[2].lo;
+  interp[k] = r[1] + 1 >= n ? (double)s[1].lo : __dadd_rn(vlo, __dmul_rn(fr, __dsub_rn(vhi, vlo)));
+}
+
+// ------------------------------------------------------------------ limits
+// One CTA per (set, metric): set a < A = {peak_ua[u][a] : (u, a) present}, set A =
+// {peak_u[u] : u present}; metric 0 = request peaks, 1 = token peaks.  Exact
+// nearest rank by MSD radix select (8-bit digits over u64), then
+// T = max(1, ceil(k * NR)) in Q8, 0 for an empty set.
+__global__ void k_limits(u32 A, u32 U, u32 qppm, u32 kq8, const u32* pr_u, const u64* pt_u, const u32* pr_ua,
+                         const u64* pt_ua, u32* nr_r_a, u64* nr_t_a, u32* nr_r_g, u64* nr_t_g, u32* T_r_a,
+                         u64* T_t_a, u32* T_r_g, u64* T_t_g) {
+  __shared__ u32 h[256];
+  __shared__ u64 prefix, krank, cnt;
+  __shared__ int digit_sh;
+  u32 set = blockIdx.x, metric = blockIdx.y;
+  auto present = [&](u32 u) -> bool { return set < A ? pr_ua[(u64)u * A + set] > 0 : pr_u[u] > 0; };
+  auto value = [&](u32 u) -> u64 {
+    if (set < A) return metric ? pt_ua[(u64)u * A + set] : (u64)pr_ua[(u64)u * A + set];
+    return metric ? pt_u[u] : (u64)pr_u[u];
+  };
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  u32 c = 0;
+  for (u32 u = threadIdx.x; u < U; u += blockDim.x) c += present(u);
+  atomicAdd((unsigned long long*)&cnt, (unsigned long long)c);
+  __syncthreads();
+  u64 n = cnt;
+  u64 result = 0;
+  if (n > 0) {
+    if (threadIdx.x == 0) {
+      u64 k = ((u128)qppm * n + 999999) / 1000000;
+      if (k < 1) k = 1;
+      if (k > n) k = n;
+      krank = k - 1;
+      prefix = 0;
+    }
+    __syncthreads();
+    for (int d = 7; d >= 0; d--) {
+      for (u32 k = threadIdx.x; k < 256; k += blockDim.x) h[k] = 0;
+      __syncthreads();
+      int sh = 8 * d;
+      u64 pre = prefix;
+      for (u32 u = threadIdx.x; u < U; u += blockDim.x) {
+        if (!present(u)) continue;
+        u64 v = value(u);
+        if (d < 7 && (v >> (sh + 8)) != pre) continue;
+        atomicAdd(&h[(v >> sh) & 255], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        u64 cum = 0; int b = 0;
+        for (; b < 256; b++) { if (cum + h[b] > krank) break; cum += h[b]; }
+        krank -= cum;
+        prefix = (pre << 8) | (u64)b;
+        digit_sh = b;
+      }
+      __syncthreads();
+    }
+    result = prefix;
+  }
+  if (threadIdx.x == 0) {
+    u64 T = 0;
+    if (result) { u128 v = ((u128)kq8 * result + 255) >> 8; T = v < 1 ? 1 : (u64)v; }
+    if (set < A) {
+      if (metric) { nr_t_a[set] = result; T_t_a[set] = T; } else { nr_r_a[set] = (u32)result; T_r_a[set] = (u32)T; }
+    } else {
+      if (metric) { *nr_t_g = result; *T_t_g = T; } else { *nr_r_g = (u32)result; *T_r_g = (u32)T; }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ phased profile builder
+struct fs_profile_partial {
+  fs_ctx* ctx = nullptr;
+  Scratch* S = nullptr;
+  DTrace t;
+  fs_profile_cfg cfg;
+  std::vector<u32> qppm;
+  fs_profile* P = nullptr;
+  int round = 0;                 // number of fs_profile_round calls made
+  u32* d_qppm = nullptr;
+  // local partials
+  u64 *l_cnt, *l_in, *l_sys, *l_out, *l_hist;
+  Order ou, oua;
+  // quantiles
+  QState* qst = nullptr; QIv* qiv = nullptr; u32* qniv = nullptr; u64* qwords = nullptr;
+  u64 h2_words = 0;
+  size_t comm_words = 0;
+  bool peaks_done = false;
+  ~fs_profile_partial() { delete S; }
+};
+
+static size_t prof_r0_words(u32 A, u32 J) { return (size_t)4 * A * (J + 1) + (size_t)A * NF * NBINS; }

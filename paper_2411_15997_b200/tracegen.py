@@ -56,24 +56,24 @@ CONFIGS = {
                profile=dict(tier_max=255)),
     "c2": dict(name="c2", n_users=1000, apps=[t[0] for t in APP_TEMPLATES], app_scales=[1.0],
                n_calls=1_000_000, abusive_frac=0.05, seed=2, duration_ms=DAY_MS, m_dist="graph",
-               in_cap=200_000, sys_cap=8000, out_cap=8000,
-               engine=dict(kv_capacity=1_048_576, max_batch=256, overload_permille=900,
+               in_cap=16_000, sys_cap=4000, out_cap=4000,
+               engine=dict(kv_capacity=49_152, max_batch=256, overload_permille=900,
                            iter_base_ns=2_000_000, decode_ns_per_req=20_000,
-                           prefill_ns_per_tok=400),
+                           prefill_ns_per_tok=10_000),
                act=dict(window_ms=60_000),
                profile=dict(tier_max=0)),
     "c3": dict(name="c3", n_users=10_000, apps=[t[0] for t in APP_TEMPLATES], app_scales=[0.5, 2.0],
                n_calls=10_000_000, abusive_frac=0.05, seed=3, duration_ms=DAY_MS, m_dist="graph",
-               in_cap=200_000, sys_cap=8000, out_cap=8000,
-               engine=dict(kv_capacity=1_048_576, max_batch=256, overload_permille=900,
+               in_cap=16_000, sys_cap=4000, out_cap=4000,
+               engine=dict(kv_capacity=49_152, max_batch=256, overload_permille=900,
                            iter_base_ns=200_000, decode_ns_per_req=2_000,
-                           prefill_ns_per_tok=40),
+                           prefill_ns_per_tok=1_000),
                act=dict(window_ms=60_000),
                profile=dict(tier_max=0)),
     "c4": dict(name="c4", n_users=100_000, apps=[t[0] for t in APP_TEMPLATES],
                app_scales=[0.5, 0.75, 1.0, 1.5, 2.0, 3.0], n_apps=34,
                n_calls=100_000_000, abusive_frac=0.05, seed=4, duration_ms=DAY_MS, m_dist="graph",
-               in_cap=200_000, sys_cap=8000, out_cap=8000,
+               in_cap=16_000, sys_cap=4000, out_cap=4000,
                engine=None, act=dict(window_ms=60_000), profile=dict(tier_max=0)),
 }
 CONFIGS["c5"] = dict(CONFIGS["c2"], name="c5", seed=2)

@@ -1,0 +1,375 @@
+"""GPU parity: every fs_* call through the C ABI vs the CPU oracle, element by
+element, on seeded inputs (tiny brute-force grids, C1, reduced C2 shapes).
+Integer outputs bit-exact; interpolated percentiles within 1e-6 relative."""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden, golden_trace
+from paper_2411_15997_b200 import tracegen as G
+from tiny import tiny_profile, tiny_replay_cfg, tiny_trace
+
+pytestmark = pytest.mark.gpu
+MS = 10**6
+UMAX = 0xFFFFFFFF
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2411_15997_b200 import build, fairserve
+    build.build()
+    return fairserve
+
+
+@pytest.fixture(scope="module")
+def ctx(F):
+    return F.Context(0)
+
+
+def _np(t):
+    import torch
+    a = t.cpu().numpy()
+    if t.dtype == torch.int32:
+        return a.view(np.uint32)
+    if t.dtype == torch.int64:
+        return a
+    return a
+
+
+def gpu_prof_host(F, ctx, p):
+    return F.profile_from_host(ctx, p["A"], p["J"], p["cnt"], p["sum_in"], p["sum_sys"], p["sum_out"],
+                               p["T_req_a"], int(p["T_req_g"][0]), p["T_tok_a"], int(p["T_tok_g"][0]))
+
+
+def cmp_replay(F, ctx, tr, gp, op, cfg, tag=""):
+    T = F.Trace(tr)
+    try:
+        eo, es = O.replay(tr, op, cfg)
+        ecode = 0
+    except O.OracleError as e:
+        ecode, eidx = e.code, e.bad_index
+    if ecode:
+        with pytest.raises(F.FsError) as ei:
+            F.wsc_replay(ctx, T, gp, cfg)
+        assert ei.value.code == ecode and ei.value.bad_index == eidx, tag
+        return None
+    o, s = F.wsc_replay(ctx, T, gp, cfg)
+    for k, ek in (("status", "status"), ("ovl", "ovl"), ("arrive_ns", "arrive_ns"), ("admit_ns", "admit_ns"),
+                  ("first_ns", "first_ns"), ("finish_ns", "finish_ns")):
+        g = _np(o[k])
+        bad = np.nonzero(g != eo[ek])[0]
+        assert len(bad) == 0, (tag, k, bad[:5], g[bad[:5]], eo[ek][bad[:5]])
+    assert (_np(o["order"]) == eo["order"]).all(), tag
+    assert (_np(o["counters"]).view(np.uint64) == eo["counters"]).all(), tag
+    assert (_np(o["admitted_per_app"]).view(np.uint64) == eo["admitted_per_app"]).all(), tag
+    for k in O.SUMMARY_FIELDS:
+        assert s[k] == es[k], (tag, k, s[k], es[k])
+    return o, s
+
+
+# ------------------------------------------------------------------ golden examples
+def test_example_W_gpu(F, ctx):
+    g = golden("example_W")
+    tr = golden_trace(g)
+    p = g["profile"]
+    gp = F.profile_from_host(ctx, 2, p["max_stage"], p["cnt"], p["sum_in"], p["sum_sys"], p["sum_out"])
+    op = O.profile_from_host(2, p["max_stage"], p["cnt"], p["sum_in"], p["sum_sys"], p["sum_out"])
+    o, s = cmp_replay(F, ctx, tr, gp, op, g["cfg"], "W")
+    assert list(_np(o["admit_ns"]) // MS) == g["expect"]["admit_ms"]
+    assert list(_np(o["counters"])) == g["expect"]["counters"]
+
+
+def test_example_WI_gpu(F, ctx):
+    g = golden("example_WI")
+    tr = golden_trace(g)
+    p = g["profile"]
+    gp = F.profile_from_host(ctx, 1, p["max_stage"], p["cnt"], p["sum_in"], p["sum_sys"], p["sum_out"])
+    op = O.profile_from_host(1, p["max_stage"], p["cnt"], p["sum_in"], p["sum_sys"], p["sum_out"])
+    o, s = cmp_replay(F, ctx, tr, gp, op, g["cfg"], "WI")
+    assert list(_np(o["status"])) == g["expect"]["status"]
+    assert list(_np(o["counters"])) == g["expect"]["counters"]
+    # P8: ACT on the replay's arrivals + overload flags reproduces the statuses
+    T = F.Trace(tr)
+    st, _ = F.act_throttle(ctx, T, gp, g["cfg"]["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+    assert list(_np(st)) == g["expect"]["status"]
+
+
+def test_example_A_gpu(F, ctx):
+    import torch
+    g = golden("example_A")
+    tr = golden_trace(g)
+    T = F.Trace(tr)
+    ovl = torch.tensor(g["overloaded"], dtype=torch.uint8, device="cuda")
+    st, _ = F.act_throttle(ctx, T, None, g["cfg"], overloaded=ovl)
+    assert list(_np(st)) == g["expect_all"]
+    st, _ = F.act_throttle(ctx, T, None, dict(g["cfg"], count_mode=1), overloaded=ovl)
+    assert list(_np(st)) == g["expect_heads_only"]
+
+
+def _cmp_profile(gpr, op, nq):
+    for k in ("cnt", "sum_in", "sum_sys", "sum_out", "ohat", "maxstage", "hist", "n_app", "nr_q", "peak_r_u",
+              "peak_t_u", "peak_r_ua", "peak_t_ua", "nr_peak_r_a", "nr_peak_t_a", "nr_peak_r_g", "nr_peak_t_g",
+              "T_req_a", "T_tok_a", "T_req_g", "T_tok_g"):
+        a, b = np.asarray(gpr[k]), np.asarray(op[k])
+        assert a.shape == b.shape and (a == b).all(), (k, np.nonzero(a != b))
+    np.testing.assert_allclose(gpr["interp_q"], op["interp_q"], rtol=1e-6, atol=0)
+
+
+def test_example_P_gpu(F, ctx):
+    g = golden("example_P")
+    tr = golden_trace(g)
+    gpr = F.build_app_profiles(ctx, F.Trace(tr), g["cfg"]).read()
+    _cmp_profile(gpr, O.profile(tr, g["cfg"]), 3)
+    assert list(gpr["peak_r_u"]) == g["expect"]["peak_r_u"]
+
+
+# ------------------------------------------------------------------ profiles
+@pytest.mark.parametrize("case", ["c1", "mid", "c2small_t0", "heads"])
+def test_profile_parity(F, ctx, case):
+    if case == "c1":
+        tr, cfg = G.generate("c1"), dict(tier_max=255)
+    elif case == "mid":
+        tr, cfg = G.generate(dict(G.CONFIGS["c3"], n_users=300, n_calls=150_000, seed=21)), dict(tier_max=255, max_stage=8)
+    elif case == "c2small_t0":
+        tr, cfg = G.generate(dict(G.CONFIGS["c2"], n_users=200, n_calls=60_000, seed=22)), dict(tier_max=0)
+    else:
+        tr, cfg = G.generate(dict(G.CONFIGS["c2"], n_users=100, n_calls=30_000, seed=23)), \
+            dict(tier_max=3, count_mode=1, window_ms=30_000, limit_mult_q8=300)
+    gpr = F.build_app_profiles(ctx, F.Trace(tr), cfg).read()
+    _cmp_profile(gpr, O.profile(tr, cfg), 5)
+
+
+def test_profile_c2_full(F, ctx):
+    tr = G.generate("c2")
+    cfg = dict(tier_max=0)
+    gpr = F.build_app_profiles(ctx, F.Trace(tr), cfg).read()
+    _cmp_profile(gpr, O.profile(tr, cfg), 5)
+
+
+def test_profile_virtual_ranks(F, ctx):
+    """The phased multi-GPU protocol with G virtual ranks on one GPU (SUM of the
+    per-shard round payloads) finalises the unsharded profile bit for bit."""
+    import ctypes as C
+    import torch
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=120, n_calls=40_000, seed=31))
+    cfg = dict(tier_max=0)
+    ref = O.profile(tr, cfg)
+    for Gn in (2, 3):
+        shards = [F.Trace(G.shard_by_user(tr, r, Gn)) for r in range(Gn)]
+        keep = []
+        c = F._profile_cfg(cfg, keep)
+        parts, bufs = [], []
+        for sh in shards:
+            p = C.c_void_p()
+            w = C.c_size_t(0)
+            ctx._check(F.lib().fs_profile_local(ctx.h, F._a(sh.c), F._a(c), C.byref(p), C.byref(w)))
+            parts.append(p)
+            bufs.append(torch.zeros(w.value, dtype=torch.int64, device="cuda"))
+        for _ in range(8):
+            dones, ws = [], []
+            for p, b in zip(parts, bufs):
+                w = C.c_size_t(0)
+                d = C.c_int(0)
+                ctx._check(F.lib().fs_profile_round(p, C.c_void_p(b.data_ptr()), C.byref(w), C.byref(d)))
+                dones.append(d.value)
+                ws.append(w.value)
+            assert len(set(dones)) == 1 and len(set(ws)) == 1
+            if dones[0]:
+                break
+            tot = sum(b[: ws[0]] for b in bufs)
+            for b in bufs:
+                b[: ws[0]] = tot
+        for p in parts:
+            h = C.c_void_p()
+            ctx._check(F.lib().fs_profile_finalize(p, C.byref(h)))
+            _cmp_profile(F.Profile(ctx, h).read(), ref, 5)
+            F.lib().fs_profile_partial_free(p)
+
+
+# ------------------------------------------------------------------ ACT
+@pytest.mark.parametrize("seed", range(60))
+def test_act_tiny(F, ctx, seed):
+    import torch
+    rng = np.random.default_rng(5000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=2, n_apps=A, max_inters=5, max_calls=9)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    n = tr["n_calls"]
+    cfg = dict(window_ms=int(rng.choice((1, 2, 4))), limits_from_profile=0, T_req_g=int(rng.choice((0, 1, 2))),
+               T_req_a=[int(rng.choice((0, 1, 2))) for _ in range(A)], T_tok_g=int(rng.choice((0, 8))),
+               T_tok_a=[int(rng.choice((0, 6))) for _ in range(A)], count_mode=int(rng.integers(0, 2)),
+               tier_max=int(rng.choice((0, 255))))
+    ovl = (rng.random(n) < 0.7).astype(np.uint8) if rng.random() < 0.8 else None
+    tov = None
+    if rng.random() < 0.5:
+        _, _, head_of, _ = O.validate(tr)
+        tov = tr["t_ms"].astype(np.int64) * MS + rng.integers(0, 3, size=n) * MS
+        for i in range(n):
+            if int(head_of[i]) != i:
+                tov[i] = max(tov[i], tov[int(head_of[i])] + 1)
+        tov[rng.random(n) < 0.1] = -1
+    est, esum = O.act(tr, op, cfg, overloaded=ovl, t_ns_override=tov)
+    T = F.Trace(tr)
+    st, s = F.act_throttle(ctx, T, gp, cfg,
+                           overloaded=None if ovl is None else torch.tensor(ovl, device="cuda"),
+                           t_ns_override=None if tov is None else torch.tensor(tov, device="cuda"))
+    assert list(_np(st)) == list(est)
+    for k in ("n_in", "n_admit", "n_block", "n_dropped", "n_filtered", "n_inter_blocked", "n_not_arrived"):
+        assert s[k] == esum[k], k
+
+
+@pytest.mark.parametrize("mode", ["always", "random", "heads_only", "replay"])
+def test_act_c2_shape(F, ctx, mode):
+    import torch
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=300, n_calls=200_000, seed=41))
+    pcfg = dict(tier_max=0)
+    op = O.profile(tr, pcfg)
+    gp = F.build_app_profiles(ctx, F.Trace(tr), pcfg)
+    cfg = dict(window_ms=60000, limits_from_profile=1, count_mode=1 if mode == "heads_only" else 0)
+    n = tr["n_calls"]
+    rng = np.random.default_rng(7)
+    T = F.Trace(tr)
+    ovl, tov = None, None
+    if mode == "random":
+        ovl = (rng.random(n) < 0.5).astype(np.uint8)
+    if mode == "replay":
+        eng = dict(G.CONFIGS["c2"]["engine"], mode=1, tier_max=255, act=cfg)
+        eo, _ = O.replay(tr, op, eng)
+        ovl, tov = eo["ovl"], eo["arrive_ns"]
+    est, esum = O.act(tr, op, cfg, overloaded=ovl, t_ns_override=tov)
+    st, s = F.act_throttle(ctx, T, gp, cfg, overloaded=None if ovl is None else torch.tensor(ovl, device="cuda"),
+                           t_ns_override=None if tov is None else torch.tensor(tov, device="cuda"))
+    g = _np(st)
+    bad = np.nonzero(g != est)[0]
+    assert len(bad) == 0, (bad[:10], g[bad[:10]], est[bad[:10]])
+    assert s["n_block"] == esum["n_block"]
+
+
+# ------------------------------------------------------------------ replay
+@pytest.mark.parametrize("seed", range(150))
+def test_replay_tiny(F, ctx, seed):
+    rng = np.random.default_rng(1000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(1, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    cmp_replay(F, ctx, tr, gp, op, tiny_replay_cfg(rng, A), f"tiny{seed}")
+
+
+@pytest.mark.parametrize("seed", range(1, 6))
+@pytest.mark.parametrize("mode", [0, 1])
+def test_replay_c1(F, ctx, seed, mode):
+    tr = G.generate("c1", seed=seed)
+    c = G.CONFIGS["c1"]
+    op = O.profile(tr, dict(tier_max=255))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=255))
+    cfg = dict(c["engine"], mode=mode, tier_max=255,
+               act=dict(window_ms=60000, limits_from_profile=0, T_req_g=8, T_req_a=[5, 5]))
+    cmp_replay(F, ctx, tr, gp, op, cfg, f"c1-{seed}-{mode}")
+
+
+@pytest.mark.parametrize("variant", ["wi", "w", "t0", "heads", "tok"])
+def test_replay_c2_shape(F, ctx, variant):
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=200, n_calls=100_000, seed=51))
+    pcfg = dict(tier_max=0)
+    op = O.profile(tr, pcfg)
+    gp = F.build_app_profiles(ctx, F.Trace(tr), pcfg)
+    act = dict(window_ms=60000, limits_from_profile=1)
+    cfg = dict(G.CONFIGS["c2"]["engine"], mode=1, tier_max=255, act=act)
+    if variant == "w":
+        cfg["mode"] = 0
+    if variant == "t0":
+        cfg["tier_max"] = 0
+    if variant == "heads":
+        act["count_mode"] = 1
+    if variant == "tok":
+        act["limit_mult_q8"] = 200
+        cfg["prio_abusive_q16"] = 2 * 65536
+        cfg["alpha"], cfg["beta"], cfg["gamma"] = 1, 1, 2
+    cmp_replay(F, ctx, tr, gp, op, cfg, variant)
+
+
+# ------------------------------------------------------------------ step
+@pytest.mark.parametrize("seed", range(40))
+def test_step_vs_oracle(F, ctx, seed):
+    rng = np.random.default_rng(9000 + seed)
+    A = 2
+    tr = tiny_trace(rng, n_users=3, n_apps=A, max_inters=6, max_calls=12, thinks=(0,))
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A)
+    cfg["kv_capacity"] = 100
+    cfg["tier_max"] = 255
+    so_ = O.Step(tr, op, cfg)
+    sg = F.WscState(ctx, F.Trace(tr), gp, cfg)
+    n = tr["n_calls"]
+    pos = 0
+    admitted = []
+    for it in range(12):
+        k = int(rng.integers(0, 4))
+        arr = list(range(pos, min(n, pos + k)))
+        pos += len(arr)
+        t = [it * MS] * len(arr)
+        fin = [admitted.pop(0) for _ in range(min(len(admitted), int(rng.integers(0, 3))))]
+        occ = int(rng.integers(0, 100))
+        nb = int(rng.integers(0, 3))
+        s1, a1 = so_.step(it * MS, occ, nb, fin, arr, t)
+        s2, a2 = sg.step(it * MS, occ, nb, fin, arr, t)
+        assert list(s1) == list(s2)
+        assert list(a1) == list(a2)
+        admitted += list(a1)
+        u1, e1 = so_.read()
+        u2, e2 = sg.read()
+        assert (u1 == u2).all() and e1 == e2
+
+
+# ------------------------------------------------------------------ sweep
+def test_sweep_small(F, ctx):
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=100, n_calls=20_000, seed=61))
+    op = O.profile(tr, dict(tier_max=0))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=0))
+    base = dict(G.CONFIGS["c2"]["engine"], mode=1, act=dict(window_ms=60000, limits_from_profile=1))
+    scen = []
+    for k, w, tm in [(0, (1, 2, 1), 15), (128, (1, 1, 2), 15), (512, (2, 1, 1), 3), (UMAX, (1, 2, 1), 15),
+                     (256, (1, 2, 1), 0), (384, (4, 1, 1), 7), (64, (1, 1, 4), 15), (1024, (1, 0, 1), 15)]:
+        s = dict(base, alpha=w[0], beta=w[1], gamma=w[2], tier_max=tm, prio_abusive_q16=131072 if tm == 7 else 65536)
+        s["act"] = dict(base["act"], limit_mult_q8=k)
+        scen.append(s)
+    scen.append(dict(scen[0], mode=0))
+    es, ecodes = O.sweep(tr, op, scen)
+    gs, gcodes = F.sweep(ctx, F.Trace(tr), gp, scen)
+    assert list(gcodes) == list(ecodes)
+    for a, b in zip(gs, es):
+        assert a == b
+
+
+# ------------------------------------------------------------------ errors
+def test_error_parity(F, ctx):
+    tr = G.generate("c1")
+    T = lambda d: F.Trace(d)
+    bad = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in tr.items()}
+    bad["user"][17] = 99
+    with pytest.raises(F.FsError) as ei:
+        F.build_app_profiles(ctx, T(bad), {})
+    assert ei.value.code == -2 and ei.value.bad_index == 17
+    bad = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in tr.items()}
+    bad["t_ms"][50] = 0
+    code, idx = O.validate(bad)[:2]
+    with pytest.raises(F.FsError) as ei:
+        F.build_app_profiles(ctx, T(bad), {})
+    assert ei.value.code == code and ei.value.bad_index == idx
+    # oversize
+    op = O.profile(tr, {})
+    gp = F.build_app_profiles(ctx, T(tr), {})
+    cfg = dict(G.CONFIGS["c1"]["engine"], mode=0, kv_capacity=3000)
+    with pytest.raises(O.OracleError) as e1:
+        O.replay(tr, op, cfg)
+    with pytest.raises(F.FsError) as e2:
+        F.wsc_replay(ctx, T(tr), gp, cfg)
+    assert (e2.value.code, e2.value.bad_index) == (e1.value.code, e1.value.bad_index)
