@@ -1,0 +1,363 @@
+"""Benchmark of the FairServe trace-scale hot path on B200 (one JSON line on rank 0).
+
+A step = one pass of the whole hot path over one synthetic Copilot-shaped trace:
+  1. fs_build_app_profiles   (benign-only profile, tier_max = 0; Q9)
+  2. fs_wsc_replay            FS(W+I) with profile-derived limits, every user present
+  3. fs_act_throttle          standalone ACT on the replay's arrival times and overload
+                              flags (the throttle evaluation; also the P8 cross-check)
+value = calls in the trace / device time of the step (requests throttled+scheduled/s).
+
+Workloads (BASELINE.json configs): c2 (default; 1k users, 6 apps, 1M calls), c3 (10k
+users, 12 apps, 10M calls), c5 (scenario sweep; scenarios sharded across ranks).
+N > 1: one process per GPU (torchrun); the replay does not shard (DESIGN.md
+"Multi-GPU"), so c2/c3 run one independent replica per rank (weak scaling); c5
+shards its scenarios.  Time = max over ranks of CUDA-event time around the K steps.
+
+--impl reference: the CPU oracle (oracle/, plain single-threaded C++) on this host,
+timed on a bounded sample of the same workload, printed as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"])
+    ap.add_argument("--scenarios", type=int, default=256, help="c5: total scenarios (all ranks)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--timings", action="store_true", help="print per-kernel timings to stderr")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (recipe's clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=2)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_cfg(name):
+    from paper_2411_15997_b200 import tracegen as G
+    c = G.CONFIGS[name]
+    eng = dict(c["engine"], mode=1, tier_max=255, alpha=1, beta=2, gamma=1,
+               act=dict(window_ms=60000, limits_from_profile=1, limit_mult_q8=0, count_mode=0))
+    pcfg = dict(tier_max=c["profile"]["tier_max"], window_ms=60000, max_stage=64)
+    return c, eng, pcfg
+
+
+def sweep_scenarios(eng, total):
+    """C5 grid: throttle k x (alpha,beta,gamma) x E_abusive x tier_max, first `total`."""
+    ks = [128, 192, 256, 320, 384, 512, 640, 768, 1024, 1280, 1536, 2048, 2560, 4096, 8192, 0xFFFFFFFF]
+    ws = [(1, 2, 1), (1, 1, 1), (1, 1, 2), (1, 0, 1), (2, 1, 1), (1, 2, 2), (1, 1, 4), (4, 1, 1)]
+    out = []
+    for k in ks:
+        for (a, b, g) in ws:
+            for E in (65536, 131072):
+                for tm in range(16):
+                    s = dict(eng, alpha=a, beta=b, gamma=g, prio_abusive_q16=E, tier_max=tm)
+                    s["act"] = dict(eng["act"], limit_mult_q8=k)
+                    out.append(s)
+    # spread the first `total` across the grid deterministically
+    idx = np.random.default_rng(5).permutation(len(out))[:total]
+    return [out[i] for i in sorted(idx)]
+
+
+def algo_bytes_profile(n):
+    # ALGORITHMIC bytes per call of fs_build_app_profiles:
+    # read user, t, meta, L_I, L_S, L_O once (24 B) + per order a permutation write+read (8 B)
+    # and the sorted-order gather of (t, tau) (12 B): 24 + 2 * 20 = 64 B
+    return 64 * n
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference(args, rank, world)
+    import torch
+    import torch.distributed as dist
+    from paper_2411_15997_b200 import build as B
+    from paper_2411_15997_b200 import fairserve as F
+    from paper_2411_15997_b200 import tracegen as G
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    ctx = F.Context(local)
+    stream = torch.cuda.current_stream()
+    c, eng, pcfg = workload_cfg("c2" if args.workload == "c5" else args.workload)
+    tr = G.generate(args.workload if args.workload != "c5" else "c5")
+    N = tr["n_calls"]
+    # inputs resident in HBM before timing
+    T = F.Trace(tr)
+    host = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int32)).pin_memory() for k in F.FIELDS}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")   # > 126 MB L2
+
+    scen = None
+    if args.workload == "c5":
+        scen_all = sweep_scenarios(eng, args.scenarios)
+        scen = scen_all[rank::world]
+        prof_fixed = F.build_app_profiles(ctx, T, pcfg)
+
+    outs = F.replay_outputs(ctx, T)
+    status = torch.empty(N, dtype=torch.uint8, device="cuda")
+
+    def step(trace):
+        if scen is not None:
+            return F.sweep(ctx, trace, prof_fixed, scen)
+        prof = F.build_app_profiles(ctx, trace, pcfg)
+        o, s = F.wsc_replay(ctx, trace, prof, eng, out=outs)
+        st, a = F.act_throttle(ctx, trace, prof, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"],
+                               status=status)
+        return s, a
+
+    for _ in range(args.warmup):
+        step(T)
+    torch.cuda.synchronize()
+    ctx.timing_reset()
+    ctx.set_timing(True)
+    evs = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                                  # L2 flush between timed steps (not timed)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            res = step(T)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+    ctx.set_timing(False)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    kt = ctx.timings()
+    launches = sum(v[0] for v in kt.values())
+    # end to end through the public API with host buffers: H2D of the trace, the step, D2H of the statuses
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    d2h = torch.empty(N, dtype=torch.uint8).pin_memory()
+    for _ in range(max(1, min(args.steps, 3))):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        T2 = F.Trace.from_host_tensors(tr, host)
+        step(T2)
+        if scen is None:
+            d2h.copy_(status, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    e2e_steps = max(1, min(args.steps, 3))
+    t = torch.tensor([ms, e2e_ms / e2e_steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, e2e_step_ms = float(t[0]), float(t[1])
+    units_per_rank = N * (len(scen) if scen is not None else 1)
+    total_units = units_per_rank * world if scen is None else N * args.scenarios
+    value = total_units * args.steps / (ms_max / 1e3)
+    e2e_value = total_units / (e2e_step_ms / 1e3)
+    if args.timings and rank == 0:
+        for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1]):
+            sys.stderr.write(f"{k:28s} launches={v[0]:7d} total_ms={v[1]:10.3f} per_step_ms={v[1] / args.steps:9.3f}\n")
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    peaks, peak_src = load_peaks()
+    # dominant kernel and its roofline
+    dom = max(kt.items(), key=lambda kv: kv[1][1])
+    dom_name, (dom_launches, dom_ms) = dom
+    roof = roofline(dom_name, dom_launches, dom_ms, N, peaks, peak_src, args)
+    line = {
+        "metric": "trace requests throttled+scheduled/sec",
+        "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive, profile + FS(W+I) replay + ACT",
+                                "c3": "C3: 10k users, 12 apps, 10M calls, profile + FS(W+I) replay + ACT",
+                                "c5": f"C5: sweep of {args.scenarios} replays of a 1M-call trace"}[args.workload],
+                   "n_calls": N, "n_users": tr["n_users"], "n_apps": tr["n_apps"],
+                   "parallelism": f"replicas x{world}" if scen is None else f"scenarios/{world}",
+                   "l2": "flushed between timed steps (256 MB write, untimed)"},
+        "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
+                "d2h_bytes_per_step": N if scen is None else 0},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "stage_ms": {k: v[1] / args.steps for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])[:8]},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args.workload, tr)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def roofline(name, launches, ms, N, peaks, src, args):
+    per_ms = ms / max(launches, 1)
+    if name in ("wsc_replay", "wsc_sweep"):
+        # serial event chain: bound by one thread's dependent issue latency
+        peak = peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9     # G instr/s for one issuing thread
+        return {"bound": "alu", "kernel": name, "achieved": None, "peak": peak, "unit": "Ginstr/s (1 thread)",
+                "frac": None, "traffic": None, "ms_per_launch": per_ms, "peak_source": src,
+                "note": "serial replay; see profiles/ for instructions/event and ns/event"}
+    return {"bound": "hbm", "kernel": name, "ms_per_launch": per_ms, "achieved": None,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": None, "traffic": None, "peak_source": src}
+
+
+def cpu_baseline(workload, tr):
+    import oracle as O
+    from paper_2411_15997_b200 import tracegen as G
+    c, eng, pcfg = workload_cfg("c2" if workload == "c5" else workload)
+    sample = tr
+    desc = "full trace"
+    if workload == "c3":
+        sample = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
+        desc = "C3-shaped 1M-call / 1k-user sample"
+    t0 = time.perf_counter()
+    if workload == "c5":
+        p = O.profile(sample, pcfg)
+        t0 = time.perf_counter()
+        O.replay(sample, p, eng, outputs=False)
+        n = sample["n_calls"]
+        desc = "one scenario replay of the C5 trace"
+    else:
+        p = O.profile(sample, pcfg)
+        o, _ = O.replay(sample, p, eng)
+        O.act(sample, p, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+        n = sample["n_calls"]
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc,
+            "seconds": dt}
+
+
+def reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_2411_15997_b200 import tracegen as G
+    wl = args.workload
+    c, eng, pcfg = workload_cfg("c2" if wl == "c5" else wl)
+    if wl == "c3":
+        tr = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
+        desc = "C3-shaped 1M-call / 1k-user sample per step"
+    else:
+        tr = G.generate("c2")
+        desc = "full C2 trace per step" if wl == "c2" else "one scenario replay of the C5 trace per step"
+    O.build()
+
+    def step():
+        p = O.profile(tr, pcfg)
+        if wl == "c5":
+            O.replay(tr, p, eng, outputs=False)
+            return
+        o, _ = O.replay(tr, p, eng)
+        O.act(tr, p, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    n = tr["n_calls"]
+    v = n * args.steps / dt
+    line = {"impl": "reference", "metric": "trace requests throttled+scheduled/sec", "value": v,
+            "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": wl, "n_calls": n},
+            "cpu_baseline": {"value": v, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -453,7 +453,9 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
   if (rc) { delete st; return rc; }
   st->ec = eng_cfg(cfg, st->T, 0, tr->n_apps, (u64)tr->n_apps * (P->J + 1), hl);
   st->p_cap = 1;
-  st->L = eng_layout(st->U, st->t.X, st->W.n_heads, cfg->max_batch, st->p_cap, cfg->mode == FS_MODE_WI, 0);
+  // continuation slots per call (the caller may queue several calls of one interaction)
+  st->L = eng_layout(st->U, (u32)std::max<u64>(st->t.n, 1), st->W.n_heads, cfg->max_batch, st->p_cap,
+                     cfg->mode == FS_MODE_WI, 0);
   st->gm = S.alloc<unsigned char>(st->L.bytes_glob + 256);
   st->scal = S.alloc<i64>(4);
   if (S.failed) { delete st; return FS_E_NOMEM; }

@@ -240,7 +240,8 @@ struct Engine {
       if (s.qh_cnt[k] == 0) s.qh_front[k] = (u32)(upos - sh->uh_off[k]);
       s.qh_cnt[k]++;
     } else {
-      u32 x = t.inter[r];
+      // one queued call per interaction in a replay; the online step may queue several
+      u32 x = static_heads ? t.inter[r] : r;
       s.c_call[x] = r; s.c_seq[x] = seq; s.c_t[x] = tr; s.c_next[x] = NONE32;
       if (s.qc_cnt[k] == 0) s.qc_head[k] = x; else s.c_next[s.qc_tail[k]] = x;
       s.qc_tail[k] = x;
