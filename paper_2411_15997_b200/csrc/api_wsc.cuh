@@ -1,7 +1,7 @@
 // api_wsc.cuh -- host orchestration of fs_wsc_replay / fs_wsc_step / fs_sweep:
-// shared trace-derived tables (head lists, static head windows, tiers), per-scenario
-// weights / limits / validity checks, and the engine launches.  Included at the end
-// of fairserve.cu (uses finish(), err_reset(), act_limits()).
+// shared trace-derived tables (packed call records, head lists, static head windows,
+// tiers, ACT ring offsets), per-scenario weights / limits / validity checks, and the
+// engine launches.  Included at the end of fairserve.cu (uses finish(), err_reset()).
 #pragma once
 
 // ------------------------------------------------------------------ shared tables
@@ -44,12 +44,36 @@ __global__ void k_hw_win(u64 n, const u32* list, const u32* key, const u64* seg,
   out_n[dst] = (u32)(p - lb + 1);
   out_t[dst] = ptau[p + 1] - ptau[lb];
 }
-__global__ void k_utier(DTrace t, u32* utier, unsigned long long* tier_calls) {
+// per user: lowest tier of its calls, calls per tier, continuation count (ring capacity)
+__global__ void k_user_stats(DTrace t, u32* utier, unsigned long long* tier_calls, u64* ncont) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= t.n) return;
-  u32 tr = m_tier(t.meta[i]);
-  atomicMin(&utier[t.user[i]], tr);
+  u32 m = t.meta[i], tr = m_tier(m), u = t.user[i];
+  atomicMin(&utier[u], tr);
   atomicAdd(&tier_calls[tr], 1ull);
+  if (m_stage(m) > 1) atomicAdd((unsigned long long*)&ncont[u], 1ull);
+}
+__global__ void k_user_calls(DTrace t, u64* nc) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n) atomicAdd((unsigned long long*)&nc[t.user[i]], 1ull);
+}
+__global__ void k_cap(u64 n, u64* v, u64 cap) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && v[i] > cap) v[i] = cap;
+}
+// packed per-call records
+__global__ void k_pack_records(DTrace t, const u32* next_call, u32 J, const u32* maxstage, const u64* cnt,
+                               const u64* ohat, const u32* posmap, uint4* A, uint4* B, uint4* Cc) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n) return;
+  u32 m = t.meta[i];
+  u64 k = 0;
+  u32 R = 0;
+  if (prof_slot(J, maxstage, cnt, m_app(m), m_stage(m), &k)) R = (u32)ohat[k];
+  u32 Li = t.len_in[i], Ls = t.len_sys[i];
+  A[i] = make_uint4(t.user[i], t.t_ms[i], m, next_call[i]);
+  B[i] = make_uint4(t.think_ms[i], Li + Ls, t.len_out[i], R);
+  Cc[i] = make_uint4((u32)k, m_stage(m) == 1 ? posmap[i] : NONE32, Li, Ls);
 }
 
 struct WscShared {
@@ -57,12 +81,14 @@ struct WscShared {
   u32* heads; u64 n_heads;
   u32* uh_list; u64* uh_off; u32* uh_key;
   u32 *hw_ng, *hw_na; u64 *hw_tg, *hw_ta;
-  u32* utier; u64* tier_calls;
+  u32* utier; u64* tier_calls; u64* r_off; u64 ring_slots;
+  uint4 *recA, *recB, *recC;
   EngShared sh;
 };
 
+// ring_cap: per-user ACT ring capacity cap (0 = exact: the user's continuation count)
 static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profile* P, u32 window_ms, bool windows,
-                       WscShared* W) {
+                       u64 ring_cap, WscShared* W) {
   u64 n = t.n;
   int B = 256;
   build_links(ctx, S, t, &W->L);
@@ -70,15 +96,21 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
   u32* pre = S.alloc<u32>(n + 1);
   W->utier = S.alloc<u32>(t.U + 1);
   W->tier_calls = S.zeros<u64>(256);
+  u64* ncont = S.zeros<u64>(t.U + 1);
+  W->r_off = S.alloc<u64>(t.U + 1);
   if (S.failed) return false;
   cudaMemsetAsync(W->utier, 0xFF, (t.U + 1) * 4, ctx->stream);
   if (n) {
     FS_LAUNCH(ctx, "flag_heads", k_flag_heads, div_up(n, B), B, 0, t, flag);
-    FS_LAUNCH(ctx, "utier", k_utier, div_up(n, B), B, 0, t, W->utier, (unsigned long long*)W->tier_calls);
+    FS_LAUNCH(ctx, "user_stats", k_user_stats, div_up(n, B), B, 0, t, W->utier, (unsigned long long*)W->tier_calls,
+              ncont);
   }
+  if (ring_cap) FS_LAUNCH(ctx, "cap", k_cap, div_up(t.U + 1, B), B, 0, (u64)t.U, ncont, ring_cap);
+  excl_scan<u64>(ctx, S, ncont, W->r_off, t.U, W->r_off + t.U);
   excl_scan<u32>(ctx, S, flag, pre, n, pre + n);
   u32 nh = 0;
   cudaMemcpyAsync(&nh, pre + n, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&W->ring_slots, W->r_off + t.U, 8, cudaMemcpyDeviceToHost, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   W->n_heads = nh;
   W->heads = S.alloc<u32>(nh + 1);
@@ -86,6 +118,8 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
   W->uh_off = S.alloc<u64>(t.U + 1);
   W->hw_ng = S.zeros<u32>(nh + 1); W->hw_na = S.zeros<u32>(nh + 1);
   W->hw_tg = S.zeros<u64>(nh + 1); W->hw_ta = S.zeros<u64>(nh + 1);
+  u32* posmap = S.alloc<u32>(n + 1);
+  W->recA = S.alloc<uint4>(n + 1); W->recB = S.alloc<uint4>(n + 1); W->recC = S.alloc<uint4>(n + 1);
   if (S.failed) return false;
   if (n) FS_LAUNCH(ctx, "scatter_heads", k_scatter_heads, div_up(n, B), B, 0, t, flag, pre, W->heads);
   if (nh) FS_LAUNCH(ctx, "list_keys", k_list_keys, div_up(nh, B), B, 0, (u64)nh, W->heads, t, 0u, keys);
@@ -93,10 +127,12 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
   if (!radix_sort<u32>(ctx, S, keys, W->heads, nh, bits_for(t.U ? t.U - 1 : 0), &skeys, &W->uh_list)) return false;
   W->uh_key = skeys;
   FS_LAUNCH(ctx, "seg_bounds", k_seg_bounds<u32>, div_up(t.U + 1, B), B, 0, skeys, (u64)nh, (u64)t.U, W->uh_off);
+  if (nh) FS_LAUNCH(ctx, "posmap", k_posmap, div_up(nh, B), B, 0, (u64)nh, W->uh_list, posmap);
+  if (n) FS_LAUNCH(ctx, "pack_records", k_pack_records, div_up(n, B), B, 0, t, W->L.next_call, P->J, P->maxstage,
+                   P->cnt, P->ohat, posmap, W->recA, W->recB, W->recC);
   if (windows && nh) {
     const i64 Wms = window_ms;
     u32* ts = S.alloc<u32>(nh); u64* tau = S.alloc<u64>(nh + 1); u64* ptau = S.alloc<u64>(nh + 1);
-    u32* posmap = S.alloc<u32>(n);
     if (S.failed) return false;
     // per user
     FS_LAUNCH(ctx, "hw_gather", k_hw_gather, div_up(nh, B), B, 0, (u64)nh, W->uh_list, t, P->J, P->maxstage, P->cnt,
@@ -105,7 +141,6 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
     FS_LAUNCH(ctx, "hw_win", k_hw_win, div_up(nh, B), B, 0, (u64)nh, W->uh_list, skeys, W->uh_off, ts, ptau, Wms,
               (const u32*)nullptr, W->hw_ng, W->hw_tg);
     // per (user, app), results mapped back to the head's per-user position
-    FS_LAUNCH(ctx, "posmap", k_posmap, div_up(nh, B), B, 0, (u64)nh, W->uh_list, posmap);
     u32* k2 = S.alloc<u32>(nh);
     if (S.failed) return false;
     FS_LAUNCH(ctx, "list_keys", k_list_keys, div_up(nh, B), B, 0, (u64)nh, W->heads, t, 1u, k2);
@@ -122,11 +157,11 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
               W->hw_ta);
   }
   EngShared& sh = W->sh;
-  sh.t = t; sh.next_call = W->L.next_call; sh.heads = W->heads; sh.n_heads = nh;
-  sh.uh_off = W->uh_off; sh.uh_list = W->uh_list;
+  sh.t = t; sh.recA = W->recA; sh.recB = W->recB; sh.recC = W->recC;
+  sh.heads = W->heads; sh.n_heads = nh; sh.uh_off = W->uh_off; sh.uh_list = W->uh_list;
   sh.hw_ng = W->hw_ng; sh.hw_tg = W->hw_tg; sh.hw_na = W->hw_na; sh.hw_ta = W->hw_ta;
-  sh.J = P->J; sh.maxstage = P->maxstage; sh.cnt = P->cnt; sh.ohat = P->ohat;
-  sh.utier = W->utier; sh.tier_calls = W->tier_calls;
+  sh.utier = W->utier; sh.tier_calls = W->tier_calls; sh.r_off = W->r_off;
+  sh.A = t.A; sh.J1 = P->J + 1;
   return true;
 }
 
@@ -134,11 +169,11 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
 struct ScenParam { u32 alpha, beta, gamma, from_profile, kq8, xrg, tier_max, pad; u64 xtg, C; };
 
 // grid.x = scenario: Eq. 2 weights W[a][j] = floor((alpha SI + beta SS + gamma SO) 2^16 / cnt) and limits
-__global__ void k_scen_setup(u32 A, u32 J, const fs_profile* Pd, const u64* cnt, const u64* s_in, const u64* s_sys,
-                             const u64* s_out, const u32* nr_r_a, const u64* nr_t_a, const u32* nr_r_g,
-                             const u64* nr_t_g, const u32* pT_r_a, const u64* pT_t_a, const u32* pT_r_g,
-                             const u64* pT_t_g, const ScenParam* sp, const u32* xra, const u64* xta, u64* W,
-                             DLimits* L, u32* ra, u64* ta) {
+__global__ void k_scen_setup(u32 A, u32 J, const u64* cnt, const u64* s_in, const u64* s_sys, const u64* s_out,
+                             const u32* nr_r_a, const u64* nr_t_a, const u32* nr_r_g, const u64* nr_t_g,
+                             const u32* pT_r_a, const u64* pT_t_a, const u32* pT_r_g, const u64* pT_t_g,
+                             const ScenParam* sp, const u32* xra, const u64* xta, u64* W, DLimits* L, u32* ra,
+                             u64* ta) {
   u32 s = blockIdx.x;
   const ScenParam p = sp[s];
   u64 AJ = (u64)A * (J + 1);
@@ -151,7 +186,6 @@ __global__ void k_scen_setup(u32 A, u32 J, const fs_profile* Pd, const u64* cnt,
     }
     W[(u64)s * AJ + k] = w;
   }
-  (void)Pd;
   if (threadIdx.x == 0) {
     auto lim = [&](u64 nr) -> u64 { if (!nr) return 0; u128 v = ((u128)p.kq8 * nr + 255) >> 8; return v < 1 ? 1 : (u64)v; };
     DLimits l; l.pad = 0;
@@ -225,7 +259,6 @@ static ScenParam scen_param(const fs_replay_cfg* c) {
   return p;
 }
 
-// per-scenario device tables for n configs: W tables, limits, checks.  Returns first error per scenario.
 struct ScenTables { u64* W; DLimits* L; u32* ra; u64* ta; unsigned long long* bad; ScenParam* sp; };
 static bool scen_tables(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profile* P, const fs_replay_cfg* cfgs, u32 ns,
                         ScenTables* T) {
@@ -250,7 +283,7 @@ static bool scen_tables(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profi
   cudaMemcpyAsync(xra, hra.data(), hra.size() * 4, cudaMemcpyHostToDevice, ctx->stream);
   cudaMemcpyAsync(xta, hta.data(), hta.size() * 8, cudaMemcpyHostToDevice, ctx->stream);
   cudaMemsetAsync(T->bad, 0xFF, 2 * (size_t)ns * 8, ctx->stream);
-  FS_LAUNCH(ctx, "scen_setup", k_scen_setup, ns, 256, 0, A, P->J, P, P->cnt, P->sum_in, P->sum_sys, P->sum_out,
+  FS_LAUNCH(ctx, "scen_setup", k_scen_setup, ns, 256, 0, A, P->J, P->cnt, P->sum_in, P->sum_sys, P->sum_out,
             P->nr_peak_r_a, P->nr_peak_t_a, P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g,
             P->T_tok_g, T->sp, xra, xta, T->W, T->L, T->ra, T->ta);
   if (t.n) {
@@ -272,6 +305,8 @@ static EngCfg eng_cfg(const fs_replay_cfg* c, const ScenTables& T, u32 s, u32 A,
   return e;
 }
 
+static const int ERR_TO_FS[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
+
 // ------------------------------------------------------------------ fs_wsc_replay
 extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
                              const fs_replay_out* out, fs_replay_summary* sum) {
@@ -284,8 +319,9 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   fs_replay_out o;
   memset(&o, 0, sizeof(o));
   if (out) o = *out;
+  const bool wi = cfg->mode == FS_MODE_WI;
   WscShared W;
-  if (!wsc_shared(ctx, S, t, P, cfg->act.window_ms, cfg->mode == FS_MODE_WI, &W)) return FS_E_NOMEM;
+  if (!wsc_shared(ctx, S, t, P, cfg->act.window_ms, wi, 0, &W)) return FS_E_NOMEM;
   int rc = finish(ctx, &S);
   if (rc) return rc;
   ScenTables T;
@@ -299,39 +335,44 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   if (hbad[0] != ~0ull) { ctx->bad_index = hbad[0]; snprintf(ctx->msg, sizeof(ctx->msg), "profile slot"); return FS_E_PROFILE; }
   if (hbad[1] != ~0ull) { ctx->bad_index = hbad[1]; snprintf(ctx->msg, sizeof(ctx->msg), "oversize"); return FS_E_OVERSIZE; }
   int B = 256;
-  if (t.n) FS_LAUNCH(ctx, "replay_pre", k_replay_pre, div_up(t.n, B), B, 0, t, cfg->tier_max, o);
-  if (o.admitted_per_app) cudaMemsetAsync(o.admitted_per_app, 0, t.A * 8, ctx->stream);
   u64 AJ = (u64)t.A * (P->J + 1);
   EngCfg ec = eng_cfg(cfg, T, 0, t.A, AJ, hl);
-  u32 p_cap = std::max<u32>(t.X, 1);
-  size_t budget = ctx->smem_optin ? ctx->smem_optin - 512 : 100 * 1024;
-  EngLayout L = eng_layout(t.U, t.X, W.n_heads, cfg->max_batch, p_cap, cfg->mode == FS_MODE_WI, budget);
-  unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
-  fs_replay_summary* dsum = S.alloc<fs_replay_summary>(1);
-  int* dcode = S.zeros<int>(1);
-  u64* didx = S.zeros<u64>(1);
-  if (S.failed) return FS_E_NOMEM;
   EngOut eo;
   eo.status = o.status; eo.ovl = o.overloaded_at_arrival; eo.arrive = o.arrive_ns; eo.admit = o.admit_ns;
   eo.first = o.first_ns; eo.finish = o.finish_ns; eo.order = o.order; eo.counters = o.counters;
   eo.adm_app = o.admitted_per_app;
   if (eo.arrive && !eo.ovl) eo.arrive = nullptr;          // arrive/ovl are written together
   if (eo.admit && !eo.order) eo.admit = nullptr;
-  ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
-  cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
-  FS_LAUNCH(ctx, "wsc_replay", k_replay, 1, 32, L.bytes_smem, a);
-  if (t.n && o.status) FS_LAUNCH(ctx, "replay_post", k_replay_post, div_up(t.n, B), B, 0, t, W.L.head_of, o.status);
+  size_t budget = ctx->smem_optin ? ctx->smem_optin - 512 : 100 * 1024;
+  fs_replay_summary* dsum = S.alloc<fs_replay_summary>(1);
+  int* dcode = S.zeros<int>(1);
+  u64* didx = S.zeros<u64>(1);
+  if (S.failed) return FS_E_NOMEM;
+  // pending-continuation heap: first a shared-memory capacity, on overflow again with every interaction
+  u32 caps[2] = {std::max<u32>(1, std::min<u32>(t.X, 4096)), std::max<u32>(t.X, 1)};
   int hcode = 0; u64 hidx = 0;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    u32 p_cap = caps[attempt];
+    if (attempt == 1 && caps[1] <= caps[0]) break;
+    if (t.n) FS_LAUNCH(ctx, "replay_pre", k_replay_pre, div_up(t.n, B), B, 0, t, cfg->tier_max, o);
+    if (o.admitted_per_app) cudaMemsetAsync(o.admitted_per_app, 0, t.A * 8, ctx->stream);
+    EngLayout L = eng_layout(t.U, t.n, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget);
+    unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
+    if (S.failed) return FS_E_NOMEM;
+    ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
+    cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
+    FS_LAUNCH(ctx, "wsc_replay", k_replay, 1, 64, L.bytes_smem, a);
+    cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    rc = finish(ctx, &S);
+    if (rc) return rc;
+    if (!(hcode && ERR_TO_FS[hcode - 1] == FS_E_NOMEM)) break;     // retry only a capacity overflow
+  }
+  if (t.n && o.status) FS_LAUNCH(ctx, "replay_post", k_replay_post, div_up(t.n, B), B, 0, t, W.L.head_of, o.status);
   cudaMemcpyAsync(sum, dsum, sizeof(*sum), cudaMemcpyDeviceToHost, ctx->stream);
-  cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
-  cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
   rc = finish(ctx, &S);
   if (rc) return rc;
-  if (hcode) {
-    static const int codes[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
-    ctx->bad_index = hidx;
-    return codes[hcode - 1];
-  }
+  if (hcode) { ctx->bad_index = hidx; return ERR_TO_FS[hcode - 1]; }
   return FS_OK;
 }
 
@@ -345,7 +386,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   for (u32 s = 0; s < ns; s++) {
     if (!replay_cfg_ok(&scen[s]) || scen[s].prio_q16) return FS_E_INVAL;
     if (scen[s].mode == FS_MODE_WI) {
-      if (any_wi && scen[s].act.window_ms != scen[0].act.window_ms) return FS_E_INVAL;   // one static window per call
+      for (u32 q = 0; q < s; q++)          // one static head window per call
+        if (scen[q].mode == FS_MODE_WI && scen[q].act.window_ms != scen[s].act.window_ms) return FS_E_INVAL;
       any_wi = true;
     }
     Bmax = std::max(Bmax, scen[s].max_batch);
@@ -357,7 +399,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   u32 win = scen[0].act.window_ms;
   for (u32 s = 0; s < ns; s++) if (scen[s].mode == FS_MODE_WI) { win = scen[s].act.window_ms; break; }
   WscShared W;
-  if (!wsc_shared(ctx, S, t, P, win, any_wi, &W)) return FS_E_NOMEM;
+  if (!wsc_shared(ctx, S, t, P, win, any_wi, SWEEP_RING_CAP, &W)) return FS_E_NOMEM;
   int rc = finish(ctx, &S);
   if (rc) return rc;
   ScenTables T;
@@ -378,7 +420,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   if (S.failed) return FS_E_NOMEM;
   cudaMemcpyAsync(dc, hc.data(), ns * sizeof(EngCfg), cudaMemcpyHostToDevice, ctx->stream);
   u32 p_cap = std::max<u32>(std::min<u32>(t.X, 1u << 16), 1);
-  EngLayout L = eng_layout(t.U, t.X, W.n_heads, Bmax, p_cap, any_wi, 0);
+  EngLayout L = eng_layout(t.U, t.n, W.n_heads, Bmax, p_cap, AJ, any_wi, W.ring_slots, false, 0);
   size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -395,9 +437,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);
   rc = finish(ctx, &S);
   if (rc) return rc;
-  static const int cmap[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
   for (u32 s = 0; s < ns; s++) {
-    codes[s] = hcodes[s] ? cmap[hcodes[s] - 1] : FS_OK;
+    codes[s] = hcodes[s] ? ERR_TO_FS[hcodes[s] - 1] : FS_OK;
     if (hbad[2 * s] != ~0ull) codes[s] = FS_E_PROFILE;
     else if (hbad[2 * s + 1] != ~0ull) codes[s] = FS_E_OVERSIZE;
     if (codes[s] != FS_OK) memset(&out[s], 0, sizeof(out[s]));
@@ -420,10 +461,11 @@ struct fs_wsc_state {
   ~fs_wsc_state() { delete S; }
 };
 
-__global__ void k_step_init(EngLayout L, unsigned char* gm, u32 p_cap, u32 U, u64 n_heads, i64* scal) {
+__global__ void k_step_init(EngLayout L, unsigned char* gm, u32 p_cap, EngShared sh, const u64* W, u32 U, i64* scal) {
   EngState st;
-  eng_bind(L, nullptr, gm, p_cap, &st);
-  eng_clear(st, U, n_heads, threadIdx.x, blockDim.x);
+  eng_bind(L, nullptr, gm, p_cap, &st, nullptr);
+  st.W = (u64*)W;
+  eng_clear(st, sh, W, 0, U, threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) { scal[0] = -1; scal[1] = 0; scal[2] = 0; scal[3] = 0; }
 }
 
@@ -439,7 +481,8 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
   err_reset(ctx);
   st->t = dtrace(tr);
   st->U = tr->n_users;
-  if (!wsc_shared(ctx, S, st->t, P, cfg->act.window_ms, false, &st->W)) { delete st; return FS_E_NOMEM; }
+  // ring capacity per user = all its calls (heads and continuations are logged)
+  if (!wsc_shared(ctx, S, st->t, P, cfg->act.window_ms, false, 0, &st->W)) { delete st; return FS_E_NOMEM; }
   int rc = finish(ctx, &S);
   if (rc) { delete st; return rc; }
   if (!scen_tables(ctx, S, st->t, P, cfg, 1, &st->T)) { delete st; return FS_E_NOMEM; }
@@ -451,15 +494,26 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
   if (!rc && hbad[0] != ~0ull) { ctx->bad_index = hbad[0]; rc = FS_E_PROFILE; }
   if (!rc && hbad[1] != ~0ull) { ctx->bad_index = hbad[1]; rc = FS_E_OVERSIZE; }
   if (rc) { delete st; return rc; }
-  st->ec = eng_cfg(cfg, st->T, 0, tr->n_apps, (u64)tr->n_apps * (P->J + 1), hl);
+  u64 AJ = (u64)tr->n_apps * (P->J + 1);
+  st->ec = eng_cfg(cfg, st->T, 0, tr->n_apps, AJ, hl);
   st->p_cap = 1;
-  // continuation slots per call (the caller may queue several calls of one interaction)
-  st->L = eng_layout(st->U, (u32)std::max<u64>(st->t.n, 1), st->W.n_heads, cfg->max_batch, st->p_cap,
-                     cfg->mode == FS_MODE_WI, 0);
+  // the online ring logs heads too: capacity per user = all of its calls (CSR over users)
+  u64* nc = S.zeros<u64>(st->U + 1);
+  u64* roff = S.alloc<u64>(st->U + 1);
+  if (S.failed) { delete st; return FS_E_NOMEM; }
+  if (st->t.n) FS_LAUNCH(ctx, "user_calls", k_user_calls, div_up(st->t.n, 256), 256, 0, st->t, nc);
+  excl_scan<u64>(ctx, S, nc, roff, st->U, roff + st->U);
+  u64 ring_slots = 0;
+  cudaMemcpyAsync(&ring_slots, roff + st->U, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) { delete st; return rc; }
+  st->W.sh.r_off = roff;
+  st->L = eng_layout(st->U, std::max<u64>(st->t.n, 1), st->W.n_heads, cfg->max_batch, st->p_cap, AJ,
+                     cfg->mode == FS_MODE_WI, ring_slots, false, 0);
   st->gm = S.alloc<unsigned char>(st->L.bytes_glob + 256);
   st->scal = S.alloc<i64>(4);
   if (S.failed) { delete st; return FS_E_NOMEM; }
-  FS_LAUNCH(ctx, "step_init", k_step_init, 1, 256, 0, st->L, st->gm, st->p_cap, st->U, st->W.n_heads, st->scal);
+  FS_LAUNCH(ctx, "step_init", k_step_init, 1, 256, 0, st->L, st->gm, st->p_cap, st->W.sh, st->ec.W, st->U, st->scal);
   rc = finish(ctx, &S);
   if (rc) { delete st; return rc; }
   *out = st;
@@ -487,11 +541,7 @@ extern "C" int fs_wsc_step(fs_ctx* ctx, fs_wsc_state* st, int64_t now_ns, int64_
   cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
   int rc = finish(ctx, &S);
   if (rc) return rc;
-  if (hcode) {
-    static const int codes[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
-    ctx->bad_index = hidx;
-    return codes[hcode - 1];
-  }
+  if (hcode) { ctx->bad_index = hidx; return ERR_TO_FS[hcode - 1]; }
   return FS_OK;
 }
 
@@ -500,11 +550,8 @@ extern "C" int fs_wsc_state_read(fs_ctx* ctx, const fs_wsc_state* st, uint64_t* 
   Scratch S(ctx);
   u64* d = S.alloc<u64>(st->U + 1);
   if (S.failed) return FS_E_NOMEM;
-  EngState es;
-  // the counters array is the first global array of the step layout
-  const u64* u = (const u64*)(st->gm + st->L.off[L_U]);
+  const u64* u = (const u64*)(st->gm + st->L.off[L_U]);     // the step layout keeps everything in global memory
   FS_LAUNCH(ctx, "step_read", k_step_read, div_up(st->U + 1, 256), 256, 0, st->U, u, d);
-  (void)es;
   i64 e = -1;
   cudaMemcpyAsync(counters, d, st->U * 8, cudaMemcpyDeviceToHost, ctx->stream);
   cudaMemcpyAsync(&e, st->scal, 8, cudaMemcpyDeviceToHost, ctx->stream);

@@ -1,32 +1,42 @@
 // replay.cuh -- WSC replay engine: Alg. 1 with the integer
-// engine model, run by ONE thread per replay over
-// pointer-addressed state (shared memory when it fits, else global / L2).
+// engine model, run by ONE thread per replay.
 //
 // Serial event loop with event skipping: between
 // arrivals, finishes and admissions the batch B is constant, so the m iterations
 // to the next event are applied in closed form (clock += m d, occ += m |B|).
-// Data structures (per replay):
-//   counters u[U] (Q32.32); per-user FIFOs: heads as a cursor range over the
-//   user's (t, id)-ordered head list (+ a blocked bitset), continuations as a
-//   linked list through per-interaction slots; an indexed binary heap of queued
-//   users keyed (class, u, tie) for the pick (l.31-38) and one keyed u for the
-//   lift (l.16-18); a min-heap of B keyed (finish iteration, id); a min-heap of
-//   pending continuations keyed (t, id); ACT: static head-window counts shared by
-//   all replays + a per-user ring of recent continuation arrivals.
+//
+// Latency design (the loop is a dependent chain, so every global round trip counts):
+//   * per-call packed records (3 x 16 B, built once per trace+profile) replace the
+//     8 SoA fields + profile lookups: one round trip fetches all a call needs;
+//   * counters, heaps, FIFO cursors, the batch heap (finish info carried in the
+//     entry) and the pending-continuation heap live in shared memory when they fit;
+//   * single replay: a producer warp streams the (t, id)-ordered head arrivals with
+//     their records and static ACT windows into a shared-memory ring ahead of the
+//     engine thread, so head deliveries never wait on global memory.
+// Data structures: counters u[U] (Q32.32, bit 63 = "front is a head" class bit);
+// per-user FIFOs: heads as a cursor over the user's (t, id)-ordered head list (+ a
+// blocked bitset), continuations as a linked list through per-call slots; indexed
+// binary heaps of queued users keyed (class, u, tie) for the pick (l.31-38) and
+// keyed u for the lift (l.16-18); ACT: static head windows shared by all replays +
+// a per-user ring of recent continuation arrivals.
 #pragma once
 #include "act.cuh"
 
-static const u32 RING_CAP = 256;      // continuation arrivals per user kept per window (FS_E_NOMEM beyond)
+static const u32 SWEEP_RING_CAP = 512;  // sweep: continuation arrivals kept per user window (FS_E_NOMEM beyond)
+static const u32 HRING = 128;         // head prefetch ring entries
 
 struct EngShared {                      // read-only, shared by every replay of a trace
   DTrace t;
-  const u32* next_call;
+  const uint4* recA;                    // {user, t_ms, meta, next_call}
+  const uint4* recB;                    // {think_ms, prompt = L_I + L_S, L_O, reserve R = O-hat(a, j')}
+  const uint4* recC;                    // {profile slot, head position in uh_list, L_I, L_S}
   const u32* heads; u64 n_heads;        // head call ids in trace order
   const u64* uh_off; const u32* uh_list;   // per-user (t, id)-ordered head lists
   const u32* hw_ng; const u64* hw_tg; const u32* hw_na; const u64* hw_ta;   // static head windows (uh position)
-  u32 J; const u32* maxstage; const u64* cnt; const u64* ohat;          // profile
   const u32* utier;                     // tier per user (0xFFFFFFFF = no calls)
   const u64* tier_calls;                // [256] calls per tier
+  const u64* r_off;                     // [U+1] ACT continuation-ring offsets (CSR by user)
+  u32 A, J1;
 };
 
 struct EngCfg {                         // one scenario
@@ -40,17 +50,21 @@ struct EngCfg {                         // one scenario
   const u64* W;                         // [A][J1] Q16 stage weights for (alpha, beta, gamma)
 };
 
+struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
+struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
+struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
+
 struct EngState {                       // per replay; any array may live in smem or global
-  u64* u; u32* tie;                     // [U] counter with class in bit 63; tie of the queue front
+  u64* u; u32* tie; u32* hf;            // [U] counter (+class bit); tie of the front; front head id
   u32 *hk, *hk_pos, *hm, *hm_pos;       // heaps of queued users + positions [U]
-  u32 *qh_front, *qh_next, *qh_cnt;     // [U]
-  u32 *qc_head, *qc_tail, *qc_cnt;      // [U]
-  u32 *c_call, *c_next, *c_seq; i64* c_t;   // [X] per interaction: queued continuation
+  u32 *qh_front, *qh_next, *qh_cnt;     // [U] absolute uh_list positions
+  u32 *qc_head, *qc_tail, *qc_cnt;      // [U] call ids
+  u32 *c_next, *c_nseq; i64* c_t;       // [slots] queued continuation links, next's seq, arrival
   u32* blocked;                         // [n_heads/32 + 1] bitset over uh positions
-  u64* b_fi; u32* b_id;                 // B heap [Bmax]
-  u32* nl_id; i64* nl_arr;              // calls admitted this round [Bmax]
-  i64* p_t; u32* p_id; u32 p_cap;       // pending continuation heap
-  i64* r_t; u32* r_tau; uint8_t* r_app; u32* r_head; u32* r_len;   // [U][RING_CAP] + [U]
+  BEnt* b; u32* nl_id; i64* nl_arr;     // B heap [Bmax]; calls admitted this round [Bmax]
+  PEnt* p; u32 p_cap;                   // pending continuation heap
+  i64* r_t; u32* r_tau; uint8_t* r_app; u32* r_head; u32* r_len;   // [ring slots] (CSR by user) + [U]
+  u64* W;                               // stage weights (smem copy or the scenario's table)
 };
 
 struct EngOut {                         // optional per-call outputs (single replay only)
@@ -58,7 +72,14 @@ struct EngOut {                         // optional per-call outputs (single rep
   u64* counters; u64* adm_app;
 };
 
+struct HeadRing {                       // producer warp -> engine thread (shared memory)
+  HEnt* e;
+  volatile u32* prod; volatile u32* cons; volatile u32* eof; volatile u32* abort;
+};
+
 #define CLS_BIT (1ull << 63)
+
+__device__ __forceinline__ uint4 ldg4(const uint4* p) { return __ldg(p); }
 
 struct Engine {
   const EngShared* sh;
@@ -66,30 +87,30 @@ struct Engine {
   EngState s;
   EngOut o;
   u32 U;
-  // scalar state
   u32 hk_n, hm_n, b_n, p_n, nl_n;
   i64 clock, occ;
   u64 iter;
   i64 e;                                 // last user to exit Q (Alg. 1 l.14), -1 = NONE
   u32 seq;
-  u64 hp;                                // next head (trace order)
+  u64 hp;                                // next head (trace order) when reading heads directly
+  bool use_ring, static_heads, slot_by_call;
+  HeadRing ring;
+  HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
   u64 digest, n_adm;
-  bool static_heads;                     // heads' window part precomputed (replay / sweep); false: step
   fs_replay_summary sum;
   int err_code; u64 err_idx;
 
-  // ---------------------------------------------------------------- keys
+  // ---------------------------------------------------------------- keys and heaps
   __device__ __forceinline__ u64 uval(u32 k) const { return s.u[k] & ~CLS_BIT; }
-  __device__ __forceinline__ bool kless(u32 a, u32 b) const {   // (class, u, tie) lexicographic
+  __device__ __forceinline__ bool kless(u32 a, u32 b) const {   // (class, u, tie)
     u64 ka = s.u[a], kb = s.u[b];
     if (ka != kb) return ka < kb;
     return s.tie[a] < s.tie[b];
   }
-  __device__ __forceinline__ bool mless(u32 a, u32 b) const {   // u, then user id (any order works)
+  __device__ __forceinline__ bool mless(u32 a, u32 b) const {
     u64 ka = uval(a), kb = uval(b);
     return ka != kb ? ka < kb : a < b;
   }
-  // indexed binary heaps (hk: kless, hm: mless)
   template <bool K> __device__ void h_up(u32* h, u32* pos, u32 i) {
     u32 x = h[i];
     while (i > 0) {
@@ -121,246 +142,281 @@ struct Engine {
     h_up<K>(h, pos, i);
     h_down<K>(h, pos, n, pos[last]);
   }
-
-  // ---------------------------------------------------------------- per-call model quantities
-  __device__ __forceinline__ u64 slot_of(u32 r) const {
-    u32 m = sh->t.meta[r], a = m_app(m);
-    u32 j = min(min(m_stage(m), sh->J), sh->maxstage[a]);
-    return (u64)a * (sh->J + 1) + j;
-  }
-  __device__ __forceinline__ u64 prompt(u32 r) const { return (u64)sh->t.len_in[r] + sh->t.len_sys[r]; }
-  __device__ __forceinline__ u64 reserve(u32 r) const { return sh->ohat[slot_of(r)]; }
   __device__ __forceinline__ bool queued(u32 k) const { return s.qh_cnt[k] + s.qc_cnt[k] != 0; }
-  __device__ __forceinline__ u32 head_front(u32 k) const { return sh->uh_list[sh->uh_off[k] + s.qh_front[k]]; }
-  __device__ __forceinline__ bool is_blocked(u64 pos) const { return (s.blocked[pos >> 5] >> (pos & 31)) & 1u; }
-  // recompute class bit + tie of a queued user's front (continuations first, l.31-35)
-  __device__ __forceinline__ void set_front_key(u32 k) {
-    if (s.qc_cnt[k]) { s.u[k] &= ~CLS_BIT; s.tie[k] = s.c_seq[s.qc_head[k]]; }
-    else { s.u[k] |= CLS_BIT; s.tie[k] = head_front(k); }
+  __device__ __forceinline__ void set_front_key(u32 k, u32 cont_seq) {
+    if (s.qc_cnt[k]) { s.u[k] &= ~CLS_BIT; s.tie[k] = cont_seq; }
+    else { s.u[k] |= CLS_BIT; s.tie[k] = s.hf[k]; }
   }
 
   __device__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
     sh = shr; c = cfg; s = st; o = out; U = nusers;
     hk_n = hm_n = b_n = p_n = nl_n = 0;
-    clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0; static_heads = true;
+    clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
+    use_ring = false; static_heads = true; slot_by_call = true; cur_ok = false;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
 
   // ---------------------------------------------------------------- Eq. 3 at finish (l.44-48)
-  __device__ bool charge(u32 r) {
-    const DTrace& t = sh->t;
-    u32 k = t.user[r];
-    u64 E = c->prio_q16 ? c->prio_q16[k] : (m_tier(t.meta[r]) == 0 ? c->prio_b : c->prio_a);
-    u64 N = (u64)c->alpha * t.len_in[r] + (u64)c->beta * t.len_sys[r] + (u64)c->gamma * t.len_out[r];
-    u128 inc = (((u128)E * N) << 32) / c->W[slot_of(r)];
+  __device__ __forceinline__ u64 increment(u32 user, u32 meta, const uint4& B, const uint4& Cc) const {
+    u64 E = c->prio_q16 ? c->prio_q16[user] : (m_tier(meta) == 0 ? c->prio_b : c->prio_a);
+    u64 N = (u64)c->alpha * Cc.z + (u64)c->beta * Cc.w + (u64)c->gamma * B.z;
+    u128 inc = (((u128)E * N) << 32) / s.W[Cc.x];
+    return inc >= ((u128)1 << 63) ? ~0ull : (u64)inc;
+  }
+  __device__ bool charge(u32 k, u64 inc, u32 r) {
     u64 cur = uval(k);
-    if (inc >= ((u128)1 << 63) || (u128)cur + inc >= ((u128)1 << 63)) { err_code = ERR_OVERFLOW; err_idx = r; return false; }
-    s.u[k] += (u64)inc;                                   // class bit untouched (no carry: u < 2^63)
+    if (inc == ~0ull || cur + inc >= (1ull << 63)) { err_code = ERR_OVERFLOW; err_idx = r; return false; }
+    s.u[k] += inc;                                        // class bit untouched (no carry: u < 2^63)
     if (s.hk_pos[k] != NONE32) {                          // queued: keys increased
       h_down<true>(s.hk, s.hk_pos, hk_n, s.hk_pos[k]);
       h_down<false>(s.hm, s.hm_pos, hm_n, s.hm_pos[k]);
     }
     return true;
   }
+  __device__ bool charge_call(u32 r) {                    // online step: records from global
+    uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
+    return charge(A.x, increment(A.x, A.z, B, Cc), r);
+  }
 
-  // ---------------------------------------------------------------- ACT check for a head (l.19-24)
-  __device__ int act_check(u32 r, u32 k, u64 upos, i64 tr) {
-    u64 n_g = 0, t_g = 0, n_a = 0, t_a = 0;
-    if (static_heads) { n_g = sh->hw_ng[upos]; t_g = sh->hw_tg[upos]; n_a = sh->hw_na[upos]; t_a = sh->hw_ta[upos]; }
-    u32 a = m_app(sh->t.meta[r]);
+  // ---------------------------------------------------------------- ACT window check (l.19-24)
+  __device__ int act_check(u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
     if (!c->heads_only || !static_heads) {
       u32 h = s.r_head[k], len = s.r_len[k];
-      u64 base = (u64)k * RING_CAP;
-      while (len && s.r_t[base + h] <= tr - c->Wns) { h = (h + 1) % RING_CAP; len--; }   // leave the window (Q4)
+      u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
+      while (len && s.r_t[base + h] <= tr - c->Wns) { h = (h + 1) % cap; len--; }   // leave the window (Q4)
       s.r_head[k] = h; s.r_len[k] = len;
       for (u32 q = 0; q < len; q++) {
-        u32 idx = (h + q) % RING_CAP;
+        u32 idx = (h + q) % cap;
         u64 tau = s.r_tau[base + idx];
         n_g++; t_g += tau;
-        if (s.r_app[base + idx] == a) { n_a++; t_a += tau; }
+        if (s.r_app[base + idx] == app) { n_a++; t_a += tau; }
       }
     }
     const DLimits& L = c->L;
     if (L.rg && n_g > L.rg) return FS_ST_BLOCK_USER_REQ;
     if (L.tg && t_g > L.tg) return FS_ST_BLOCK_USER_TOK;
-    if (c->ra[a] && n_a > c->ra[a]) return FS_ST_BLOCK_APP_REQ;
-    if (c->ta[a] && t_a > c->ta[a]) return FS_ST_BLOCK_APP_TOK;
+    if (c->ra[app] && n_a > c->ra[app]) return FS_ST_BLOCK_APP_REQ;
+    if (c->ta[app] && t_a > c->ta[app]) return FS_ST_BLOCK_APP_TOK;
     return FS_ST_ADMIT;
   }
+  __device__ bool ring_push(u32 k, i64 tr, u32 tau, u32 app, u32 r) {
+    u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
+    u32 h = s.r_head[k], len = s.r_len[k];
+    while (len && s.r_t[base + h] <= tr - c->Wns) { h = (h + 1) % cap; len--; }
+    if (len == cap) { err_code = ERR_NOMEM; err_idx = r; return false; }
+    u32 idx = (h + len) % cap;
+    s.r_t[base + idx] = tr; s.r_tau[base + idx] = tau; s.r_app[base + idx] = (uint8_t)app;
+    s.r_head[k] = h; s.r_len[k] = len + 1;
+    return true;
+  }
 
-  // ---------------------------------------------------------------- delivery of one arrival (l.11-25)
-  // returns the arrival status (FS_ST_ADMIT or a BLOCK code), -1 on error
-  __device__ int deliver(u32 r, i64 tr, bool ovl) {
-    const DTrace& t = sh->t;
-    u32 k = t.user[r], m = t.meta[r];
-    bool head = m_stage(m) == 1;
-    if (head && sh->uh_list[sh->uh_off[k] + s.qh_next[k]] != r) {   // heads of a user arrive in (t, id) order
-      err_code = ERR_ORDER; err_idx = r; return -1;
-    }
+  // lift (l.12-18) for a user about to deliver; returns whether it was queued
+  __device__ __forceinline__ bool lift(u32 k) {
+    if (queued(k)) return true;
+    u64 uk = uval(k), l;
+    if (hm_n == 0) l = e >= 0 ? uval((u32)e) : 0;           // l.13-15
+    else l = uval(s.hm[0]);                                 // l.16-18
+    if (l > uk) s.u[k] = (s.u[k] & CLS_BIT) | l;
+    return false;
+  }
+  __device__ __forceinline__ void arrived(u32 r, i64 tr, bool ovl) {
     sum.n_arrived++;
     if (ovl) sum.n_ovl_arrivals++;
     if (o.arrive) { o.arrive[r] = tr; o.ovl[r] = ovl; }
-    bool was = queued(k);
-    if (!was) {                                                   // l.12
-      u64 uk = uval(k), lift;
-      if (hm_n == 0) lift = e >= 0 ? uval((u32)e) : 0;            // l.13-15
-      else lift = uval(s.hm[0]);                                  // l.16-18
-      if (lift > uk) s.u[k] = (s.u[k] & CLS_BIT) | lift;
-    }
+  }
+  __device__ __forceinline__ void newly_queued(u32 k) {
+    s.hk[hk_n] = k; h_up<true>(s.hk, s.hk_pos, hk_n++);
+    s.hm[hm_n] = k; h_up<false>(s.hm, s.hm_pos, hm_n++);
+  }
+
+  // ---------------------------------------------------------------- deliveries (l.11-25)
+  // returns the arrival status (FS_ST_ADMIT or a BLOCK code), -1 on error
+  __device__ int deliver_head(const HEnt& h, i64 tr, bool ovl) {
+    u32 r = h.r, k = h.A.x, m = h.A.z;
+    u32 upos = h.C.y;
+    if (upos != s.qh_next[k]) { err_code = ERR_ORDER; err_idx = r; return -1; }   // (t, id) order per user
+    arrived(r, tr, ovl);
+    bool was = lift(k);
     int st = FS_ST_ADMIT;
-    u64 upos = 0;
-    if (head) upos = sh->uh_off[k] + s.qh_next[k];
     if (c->mode == FS_MODE_WI) {
-      // l.19: log the arrival (the heads' part is the static window when static_heads)
-      if (static_heads ? (!head && !c->heads_only) : (head || !c->heads_only)) {
-        u64 base = (u64)k * RING_CAP;
-        u32 h = s.r_head[k], len = s.r_len[k];
-        while (len && s.r_t[base + h] <= tr - c->Wns) { h = (h + 1) % RING_CAP; len--; }
-        if (len == RING_CAP) { err_code = ERR_NOMEM; err_idx = r; return -1; }
-        u32 idx = (h + len) % RING_CAP;
-        s.r_t[base + idx] = tr;
-        s.r_tau[base + idx] = (u32)(prompt(r) + reserve(r));
-        s.r_app[base + idx] = (uint8_t)m_app(m);
-        s.r_head[k] = h; s.r_len[k] = len + 1;
-      }
-      if (ovl && head) st = act_check(r, k, upos, tr);            // l.20-24
+      if (!static_heads && !ring_push(k, tr, h.B.y + h.B.w, m_app(m), r)) return -1;   // l.19
+      if (ovl) st = act_check(k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);                  // l.20-24
     }
     digest = sm64(digest ^ ((u64)r * 16 + (u64)st));
-    if (head) {
-      s.qh_next[k]++;
-      if (st != FS_ST_ADMIT) {
-        s.blocked[upos >> 5] |= 1u << (upos & 31);
-        if (s.qh_cnt[k] == 0) s.qh_front[k] = s.qh_next[k];
-        sum.n_block[st - 1]++;
-        sum.n_dropped += m_ncalls(m) - 1;
-        if (o.status) o.status[r] = (uint8_t)st;
-        return st;
-      }
-      if (s.qh_cnt[k] == 0) s.qh_front[k] = (u32)(upos - sh->uh_off[k]);
-      s.qh_cnt[k]++;
-    } else {
-      // one queued call per interaction in a replay; the online step may queue several
-      u32 x = static_heads ? t.inter[r] : r;
-      s.c_call[x] = r; s.c_seq[x] = seq; s.c_t[x] = tr; s.c_next[x] = NONE32;
-      if (s.qc_cnt[k] == 0) s.qc_head[k] = x; else s.c_next[s.qc_tail[k]] = x;
-      s.qc_tail[k] = x;
-      s.qc_cnt[k]++;
+    s.qh_next[k] = upos + 1;
+    if (st != FS_ST_ADMIT) {
+      s.blocked[upos >> 5] |= 1u << (upos & 31);
+      if (s.qh_cnt[k] == 0) s.qh_front[k] = upos + 1;
+      sum.n_block[st - 1]++;
+      sum.n_dropped += m_ncalls(m) - 1;
+      if (o.status) o.status[r] = (uint8_t)st;
+      return st;
     }
+    if (s.qh_cnt[k] == 0) { s.qh_front[k] = upos; s.hf[k] = r; }
+    s.qh_cnt[k]++;
     seq++;
-    if (!was) {                                                   // newly queued user
-      set_front_key(k);
-      s.hk[hk_n] = k; h_up<true>(s.hk, s.hk_pos, hk_n++);
-      s.hm[hm_n] = k; h_up<false>(s.hm, s.hm_pos, hm_n++);
-    } else if (!head && s.qc_cnt[k] == 1) {                       // class 1 -> 0: key decreased
-      set_front_key(k);
-      h_up<true>(s.hk, s.hk_pos, s.hk_pos[k]);
+    if (!was) { set_front_key(k, 0); newly_queued(k); }
+    return FS_ST_ADMIT;
+  }
+  __device__ int deliver_cont(u32 r, u32 k, u32 m, i64 tr, bool ovl) {
+    arrived(r, tr, ovl);
+    bool was = lift(k);
+    if (c->mode == FS_MODE_WI && !c->heads_only) {          // l.19 (continuations are never throttled)
+      uint4 B = ldg4(&sh->recB[r]);
+      if (!ring_push(k, tr, B.y + B.w, m_app(m), r)) return -1;
     }
+    digest = sm64(digest ^ ((u64)r * 16));
+    u32 x = r;
+    s.c_next[x] = NONE32; s.c_t[x] = tr;
+    if (s.qc_cnt[k] == 0) s.qc_head[k] = x; else { s.c_next[s.qc_tail[k]] = x; s.c_nseq[s.qc_tail[k]] = seq; }
+    s.qc_tail[k] = x;
+    s.qc_cnt[k]++;
+    u32 myseq = seq++;
+    if (!was) { set_front_key(k, myseq); newly_queued(k); }
+    else if (s.qc_cnt[k] == 1) { set_front_key(k, myseq); h_up<true>(s.hk, s.hk_pos, s.hk_pos[k]); }   // class 1 -> 0
     return FS_ST_ADMIT;
   }
 
   // ---------------------------------------------------------------- one pick (l.28-39)
-  // Returns the admitted call or NONE32 if Q is empty or the candidate does not fit (Q16, Q17).
-  __device__ u32 pick(i64 occ_now, u32 nb, i64* arr_t) {
-    if (hk_n == 0) return NONE32;
+  struct Adm { u32 r; u64 need, prompt; BEnt b; i64 arr; };
+  __device__ bool pick(i64 occ_now, u32 nb, Adm* a) {
+    if (hk_n == 0) return false;
     u32 k = s.hk[0];
     bool cont = s.qc_cnt[k] != 0;
-    u32 x = cont ? s.qc_head[k] : 0;
-    u32 r = cont ? s.c_call[x] : head_front(k);
-    if ((u128)(u64)occ_now + prompt(r) + reserve(r) > c->C || nb >= c->Bmax) return NONE32;
+    u32 r = cont ? s.qc_head[k] : s.hf[k];
+    uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
+    u32 nx = 0, nseq = 0; i64 ct = 0;
+    if (cont) { nx = s.c_next[r]; nseq = s.c_nseq[r]; ct = s.c_t[r]; }
+    u64 need = (u64)B.y + B.w;
+    if ((u128)(u64)occ_now + need > c->C || nb >= c->Bmax) return false;      // can_add_new_request (Q16, Q17)
     if (cont) {
-      *arr_t = s.c_t[x];
-      s.qc_head[k] = s.c_next[x];
+      a->arr = ct;
+      s.qc_head[k] = nx;
       s.qc_cnt[k]--;
     } else {
-      *arr_t = (i64)sh->t.t_ms[r] * 1000000;
+      a->arr = (i64)A.y * 1000000;
       s.qh_cnt[k]--;
-      if (s.qh_cnt[k]) {                                          // next non-blocked queued head
-        u64 base = sh->uh_off[k];
+      if (s.qh_cnt[k]) {                                     // next non-blocked queued head
         u32 f = s.qh_front[k] + 1;
-        while (is_blocked(base + f)) f++;
+        for (;;) {
+          u32 w = s.blocked[f >> 5], id = sh->uh_list[f];
+          if (!((w >> (f & 31)) & 1u)) { s.hf[k] = id; break; }
+          f++;
+        }
         s.qh_front[k] = f;
       } else s.qh_front[k] = s.qh_next[k];
     }
-    if (!queued(k)) {                                             // user leaves Q: e <- k
+    if (!queued(k)) {                                        // user leaves Q: e <- k
       h_remove<true>(s.hk, s.hk_pos, hk_n, k);
       h_remove<false>(s.hm, s.hm_pos, hm_n, k);
       s.u[k] &= ~CLS_BIT;
       e = k;
     } else {
-      set_front_key(k);                                           // key increased
+      set_front_key(k, nseq);                                // key increased
       h_down<true>(s.hk, s.hk_pos, hk_n, 0);
     }
-    return r;
+    a->r = r;
+    a->need = need;
+    a->prompt = B.y;
+    a->b.r = r; a->b.user = A.x; a->b.meta = A.z; a->b.link = A.w; a->b.think = B.x;
+    a->b.rel = B.y + B.z;
+    a->b.fi = iter + B.z - 1;
+    a->b.inc = increment(A.x, A.z, B, Cc);
+    return true;
   }
 
-  // ---------------------------------------------------------------- pending arrivals
-  __device__ __forceinline__ void skip_filtered_heads() {
-    while (hp < sh->n_heads && m_tier(sh->t.meta[sh->heads[hp]]) > c->tier_max) hp++;
-  }
-  __device__ __forceinline__ bool next_pending(i64* tn, u32* id) {
-    bool any = false;
-    if (hp < sh->n_heads) { u32 h = sh->heads[hp]; *tn = (i64)sh->t.t_ms[h] * 1000000; *id = h; any = true; }
-    if (p_n) {
-      i64 pt = s.p_t[0]; u32 pid = s.p_id[0];
-      if (!any || pt < *tn || (pt == *tn && pid < *id)) { *tn = pt; *id = pid; any = true; }
+  // ---------------------------------------------------------------- heads source
+  __device__ __forceinline__ bool head_peek(HEnt* h) {
+    if (use_ring) {
+      u32 cs = *ring.cons;
+      for (;;) {
+        if (*ring.prod != cs) break;
+        if (*ring.eof && *ring.prod == cs) return false;
+        __nanosleep(32);
+      }
+      __threadfence_block();
+      *h = ring.e[cs % HRING];
+      return true;
     }
-    return any;
+    if (!cur_ok) {
+      while (hp < sh->n_heads) {
+        u32 r = sh->heads[hp];
+        uint4 A = ldg4(&sh->recA[r]);
+        if (m_tier(A.z) <= c->tier_max) {
+          cur.A = A; cur.B = ldg4(&sh->recB[r]); cur.C = ldg4(&sh->recC[r]); cur.r = r;
+          if (c->mode == FS_MODE_WI && static_heads) {
+            u32 up = cur.C.y;
+            cur.ng = sh->hw_ng[up]; cur.na = sh->hw_na[up]; cur.tg = sh->hw_tg[up]; cur.ta = sh->hw_ta[up];
+          } else { cur.ng = cur.na = 0; cur.tg = cur.ta = 0; }
+          cur_ok = true;
+          break;
+        }
+        hp++;
+      }
+      if (!cur_ok) return false;
+    }
+    *h = cur;
+    return true;
   }
-  __device__ __forceinline__ bool p_less(u32 a, u32 b) const {
-    return s.p_t[a] < s.p_t[b] || (s.p_t[a] == s.p_t[b] && s.p_id[a] < s.p_id[b]);
+  __device__ __forceinline__ void head_pop() {
+    if (use_ring) { *ring.cons = *ring.cons + 1; return; }
+    cur_ok = false; hp++;
   }
-  __device__ bool p_push(i64 tn, u32 id) {
-    if (p_n == s.p_cap) { err_code = ERR_NOMEM; err_idx = id; return false; }
+
+  // ---------------------------------------------------------------- pending heap (t, id)
+  __device__ __forceinline__ bool pless(const PEnt& a, const PEnt& b) const { return a.t < b.t || (a.t == b.t && a.r < b.r); }
+  __device__ bool p_push(const PEnt& x) {
+    if (p_n == s.p_cap) { err_code = ERR_NOMEM; err_idx = x.r; return false; }
     u32 i = p_n++;
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
-      if (!(tn < s.p_t[pi] || (tn == s.p_t[pi] && id < s.p_id[pi]))) break;
-      s.p_t[i] = s.p_t[pi]; s.p_id[i] = s.p_id[pi]; i = pi;
+      if (!pless(x, s.p[pi])) break;
+      s.p[i] = s.p[pi]; i = pi;
     }
-    s.p_t[i] = tn; s.p_id[i] = id;
+    s.p[i] = x;
     return true;
   }
   __device__ void p_pop() {
     p_n--;
     if (!p_n) return;
-    i64 tn = s.p_t[p_n]; u32 id = s.p_id[p_n];
+    PEnt x = s.p[p_n];
     u32 i = 0;
     for (;;) {
       u32 l = 2 * i + 1;
       if (l >= p_n) break;
       u32 m = l;
-      if (l + 1 < p_n && p_less(l + 1, l)) m = l + 1;
-      if (!(s.p_t[m] < tn || (s.p_t[m] == tn && s.p_id[m] < id))) break;
-      s.p_t[i] = s.p_t[m]; s.p_id[i] = s.p_id[m]; i = m;
+      if (l + 1 < p_n && pless(s.p[l + 1], s.p[l])) m = l + 1;
+      if (!pless(s.p[m], x)) break;
+      s.p[i] = s.p[m]; i = m;
     }
-    s.p_t[i] = tn; s.p_id[i] = id;
+    s.p[i] = x;
   }
   // B heap keyed (finish iteration, id)
-  __device__ __forceinline__ bool b_less(u64 fa, u32 ia, u64 fb, u32 ib) const { return fa < fb || (fa == fb && ia < ib); }
-  __device__ void b_push(u64 fi, u32 id) {
+  __device__ __forceinline__ bool bless(const BEnt& a, const BEnt& b) const { return a.fi < b.fi || (a.fi == b.fi && a.r < b.r); }
+  __device__ void b_push(const BEnt& x) {
     u32 i = b_n++;
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
-      if (!b_less(fi, id, s.b_fi[pi], s.b_id[pi])) break;
-      s.b_fi[i] = s.b_fi[pi]; s.b_id[i] = s.b_id[pi]; i = pi;
+      if (!bless(x, s.b[pi])) break;
+      s.b[i] = s.b[pi]; i = pi;
     }
-    s.b_fi[i] = fi; s.b_id[i] = id;
+    s.b[i] = x;
   }
   __device__ void b_pop() {
     b_n--;
     if (!b_n) return;
-    u64 fi = s.b_fi[b_n]; u32 id = s.b_id[b_n];
+    BEnt x = s.b[b_n];
     u32 i = 0;
     for (;;) {
       u32 l = 2 * i + 1;
       if (l >= b_n) break;
       u32 m = l;
-      if (l + 1 < b_n && b_less(s.b_fi[l + 1], s.b_id[l + 1], s.b_fi[l], s.b_id[l])) m = l + 1;
-      if (!b_less(s.b_fi[m], s.b_id[m], fi, id)) break;
-      s.b_fi[i] = s.b_fi[m]; s.b_id[i] = s.b_id[m]; i = m;
+      if (l + 1 < b_n && bless(s.b[l + 1], s.b[l])) m = l + 1;
+      if (!bless(s.b[m], x)) break;
+      s.b[i] = s.b[m]; i = m;
     }
-    s.b_fi[i] = fi; s.b_id[i] = id;
+    s.b[i] = x;
   }
 
   __device__ __forceinline__ bool overloaded() const {   // Q5
@@ -370,47 +426,62 @@ struct Engine {
 
   // ---------------------------------------------------------------- the replay (O4 with event skipping)
   __device__ void run() {
-    const DTrace& t = sh->t;
-    skip_filtered_heads();
+    HEnt hh;
     for (;;) {
-      i64 tn = 0; u32 idn = 0;
-      bool pend = next_pending(&tn, &idn);
+      bool hok = head_peek(&hh);
+      i64 th = hok ? (i64)hh.A.y * 1000000 : 0;
+      bool pok = p_n != 0;
+      // next pending arrival in (t, id) order
+      bool pend = hok || pok;
+      i64 tn = 0;
+      if (hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hh.r < s.p[0].r))) tn = th;
+      else if (pok) tn = s.p[0].t;
       if (b_n == 0 && hk_n == 0) {                                // 1: idle engine restarts at the arrival
         if (!pend) break;
         if (tn > clock) clock = tn;
       }
       bool ovl = overloaded();                                    // 2: occupancy at iteration start
       while (pend && tn <= clock) {
-        if (p_n && s.p_id[0] == idn && s.p_t[0] == tn) p_pop();
-        else { hp++; skip_filtered_heads(); }
-        if (deliver(idn, tn, ovl) < 0) return;
-        pend = next_pending(&tn, &idn);
+        int st;
+        if (hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hh.r < s.p[0].r))) {
+          head_pop();
+          st = deliver_head(hh, th, ovl);
+        } else {
+          PEnt pe = s.p[0];
+          p_pop();
+          st = deliver_cont(pe.r, pe.user, pe.meta, pe.t, ovl);
+        }
+        if (st < 0) return;
+        hok = head_peek(&hh);
+        th = hok ? (i64)hh.A.y * 1000000 : 0;
+        pok = p_n != 0;
+        pend = hok || pok;
+        if (hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hh.r < s.p[0].r))) tn = th;
+        else if (pok) tn = s.p[0].t;
       }
       u64 P_new = 0;                                              // 3: admission round
       nl_n = 0;
-      for (;;) {
-        i64 arr;
-        u32 r = pick(occ, b_n, &arr);
-        if (r == NONE32) break;
-        u64 P = prompt(r);
-        b_push(iter + t.len_out[r] - 1, r);
-        occ += (i64)P; P_new += P;
-        s.nl_id[nl_n] = r; s.nl_arr[nl_n] = arr; nl_n++;
+      Adm ad;
+      while (pick(occ, b_n, &ad)) {
+        u32 r = ad.r;
+        b_push(ad.b);
+        occ += (i64)ad.prompt; P_new += ad.prompt;
+        s.nl_id[nl_n] = r; s.nl_arr[nl_n] = ad.arr; nl_n++;
         sum.n_admitted++;
-        u64 wt = (u64)(clock - arr);
+        u64 wt = (u64)(clock - ad.arr);
         sum.sum_wait_ns += wt;
         if (wt > sum.max_wait_ns) sum.max_wait_ns = wt;
         digest = sm64(digest ^ r);
         digest = sm64(digest ^ (u64)clock);
         if (o.admit) { o.admit[r] = clock; o.order[r] = (u32)n_adm; if (o.status) o.status[r] = FS_ST_ADMIT; }
-        if (o.adm_app) o.adm_app[m_app(t.meta[r])]++;
+        if (o.adm_app) o.adm_app[m_app(ad.b.meta)]++;
         n_adm++;
       }
       if (b_n == 0) continue;
       u64 d = c->base + c->dec * b_n + c->pre * P_new;            // 4: iteration(s)
       u64 m = 1;
       if (nl_n == 0) {                                            // event skipping: B constant until
-        m = s.b_fi[0] - iter + 1;                                 //   the next finish ...
+        m = s.b[0].fi - iter + 1;                                 //   the next finish ...
         if (pend && d > 0) {                                      //   ... or the next arrival
           u64 ma = ((u64)(tn - clock) + d - 1) / d;
           if (ma < m) m = ma;
@@ -425,16 +496,18 @@ struct Engine {
         if (o.first) o.first[r] = clock;
         sum.sum_ttft_ns += (u64)(clock - s.nl_arr[q]);
       }
-      while (b_n && s.b_fi[0] == iter - 1) {                      // finishes (l.43-48)
-        u32 r = s.b_id[0];
+      while (b_n && s.b[0].fi == iter - 1) {                      // finishes (l.43-48)
+        BEnt f = s.b[0];
         b_pop();
-        if (o.finish) o.finish[r] = clock;
+        if (o.finish) o.finish[f.r] = clock;
         sum.n_finished++;
-        occ -= (i64)(prompt(r) + t.len_out[r]);
-        if (!charge(r)) return;
-        u32 mm = t.meta[r];
-        if (m_stage(mm) < m_ncalls(mm))
-          if (!p_push(clock + (i64)t.think_ms[r] * 1000000, sh->next_call[r])) return;
+        occ -= (i64)f.rel;
+        if (!charge(f.user, f.inc, f.r)) return;
+        if (m_stage(f.meta) < m_ncalls(f.meta)) {
+          PEnt pe; pe.t = clock + (i64)f.think * 1000000; pe.r = f.link; pe.user = f.user;
+          pe.meta = f.meta + (1u << 8); pe.pad = 0;
+          if (!p_push(pe)) return;
+        }
       }
     }
     // STOP: final digest, counters, summary
@@ -443,43 +516,79 @@ struct Engine {
     sum.makespan_ns = clock;
     bool any = false;
     for (u32 k = 0; k < U; k++) {
-      if (sh->utier[k] > c->tier_max) continue;
       u64 v = uval(k);
+      if (o.counters) o.counters[k] = v;
+      if (sh->utier[k] > c->tier_max) continue;
       if (!any) { sum.u_min = sum.u_max = v; any = true; }
       if (v < sum.u_min) sum.u_min = v;
       if (v > sum.u_max) sum.u_max = v;
-      if (o.counters) o.counters[k] = v;
     }
-    if (o.counters) for (u32 k = 0; k < U; k++) if (sh->utier[k] > c->tier_max) o.counters[k] = uval(k);
     for (u32 tt = c->tier_max + 1; tt < 256; tt++) sum.n_filtered += sh->tier_calls[tt];
     sum.digest = digest;
   }
 };
 
+// ------------------------------------------------------------------ producer warp: head arrivals -> ring
+__device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing ring, bool windows) {
+  int lane = threadIdx.x & 31;
+  u32 prod = 0;
+  for (u64 base = 0; base < sh->n_heads; base += 32) {
+    u64 j = base + lane;
+    bool ok = j < sh->n_heads;
+    HEnt h;
+    memset(&h, 0, sizeof(h));
+    if (ok) {
+      h.r = sh->heads[j];
+      h.A = ldg4(&sh->recA[h.r]);
+      ok = m_tier(h.A.z) <= c->tier_max;
+    }
+    if (ok) {
+      h.B = ldg4(&sh->recB[h.r]);
+      h.C = ldg4(&sh->recC[h.r]);
+      if (windows) { u32 up = h.C.y; h.ng = sh->hw_ng[up]; h.na = sh->hw_na[up]; h.tg = sh->hw_tg[up]; h.ta = sh->hw_ta[up]; }
+    }
+    u32 mask = __ballot_sync(FULL_MASK, ok);
+    u32 cnt = __popc(mask);
+    if (!cnt) continue;
+    u32 ab = 0;
+    if (lane == 0) while (prod + cnt - *ring.cons > HRING && !(ab = *ring.abort)) __nanosleep(64);
+    if (__shfl_sync(FULL_MASK, ab, 0)) return;     // the engine stopped on an error
+    __syncwarp();
+    if (ok) ring.e[(prod + __popc(mask & lanemask_lt())) % HRING] = h;
+    __threadfence_block();
+    __syncwarp();
+    prod += cnt;
+    if (lane == 0) *ring.prod = prod;
+  }
+  __threadfence_block();
+  if (lane == 0) *ring.eof = 1;
+}
+
 // ------------------------------------------------------------------ state layout
-// Offsets of a replay's arrays inside one memory region; `in_smem` selects which
-// arrays go to the (first) shared-memory region when a budget is given.
 struct EngLayout {
   size_t bytes_smem = 0, bytes_glob = 0;
   size_t off[32];
   bool smem[32];
 };
-enum { L_U, L_TIE, L_HK, L_HKP, L_HM, L_HMP, L_BFI, L_BID, L_NLID, L_NLARR, L_QHF, L_QHN, L_QHC, L_QCH, L_QCT, L_QCC,
-       L_CCALL, L_CNEXT, L_CSEQ, L_CT, L_BLK, L_PT, L_PID, L_RT, L_RTAU, L_RAPP, L_RHEAD, L_RLEN, L_N };
+enum { L_U, L_TIE, L_HF, L_HK, L_HKP, L_HM, L_HMP, L_B, L_NLID, L_NLARR, L_P, L_W, L_QHF, L_QHN, L_QHC, L_QCH, L_QCT,
+       L_QCC, L_CNEXT, L_CNSEQ, L_CT, L_BLK, L_RT, L_RTAU, L_RAPP, L_RHEAD, L_RLEN, L_HR, L_N };
 
-static EngLayout eng_layout(u32 U, u32 X, u64 n_heads, u32 Bmax, u32 p_cap, bool act_ring, size_t smem_budget) {
+static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
+                            bool hring, size_t smem_budget) {
   size_t sz[L_N];
-  sz[L_U] = (size_t)U * 8; sz[L_TIE] = (size_t)U * 4; sz[L_HK] = sz[L_HKP] = sz[L_HM] = sz[L_HMP] = (size_t)U * 4;
-  sz[L_BFI] = (size_t)Bmax * 8; sz[L_BID] = (size_t)Bmax * 4; sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
+  sz[L_U] = (size_t)U * 8; sz[L_TIE] = sz[L_HF] = (size_t)U * 4;
+  sz[L_HK] = sz[L_HKP] = sz[L_HM] = sz[L_HMP] = (size_t)U * 4;
+  sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
+  sz[L_P] = (size_t)p_cap * sizeof(PEnt); sz[L_W] = (size_t)AJ * 8;
   sz[L_QHF] = sz[L_QHN] = sz[L_QHC] = sz[L_QCH] = sz[L_QCT] = sz[L_QCC] = (size_t)U * 4;
-  sz[L_CCALL] = sz[L_CNEXT] = sz[L_CSEQ] = (size_t)X * 4; sz[L_CT] = (size_t)X * 8;
-  sz[L_BLK] = (size_t)(n_heads / 32 + 1) * 4;
-  sz[L_PT] = (size_t)p_cap * 8; sz[L_PID] = (size_t)p_cap * 4;
-  size_t ring = act_ring ? (size_t)U * RING_CAP : 0;
+  sz[L_CNEXT] = sz[L_CNSEQ] = (size_t)slots * 4; sz[L_CT] = (size_t)slots * 8;
+  sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
+  size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
   sz[L_RT] = ring * 8; sz[L_RTAU] = ring * 4; sz[L_RAPP] = ring; sz[L_RHEAD] = sz[L_RLEN] = (size_t)U * 4;
-  // shared-memory priority: hottest first
-  static const int prio[] = {L_U, L_TIE, L_HK, L_HKP, L_BFI, L_BID, L_NLID, L_NLARR, L_PT, L_PID, L_HM, L_HMP,
-                             L_QHF, L_QHN, L_QHC, L_QCC, L_QCH, L_QCT};
+  sz[L_HR] = hring ? (size_t)HRING * sizeof(HEnt) + 64 : 0;
+  // shared-memory priority: hottest first (the head ring must be shared)
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_U, L_TIE, L_HF, L_HK, L_HKP, L_QCC, L_QHC,
+                             L_QCH, L_QCT, L_QHF, L_QHN, L_HM, L_HMP, L_RHEAD, L_RLEN};
   EngLayout L;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
@@ -491,27 +600,37 @@ static EngLayout eng_layout(u32 U, u32 X, u64 n_heads, u32 Bmax, u32 p_cap, bool
   return L;
 }
 
-__device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned char* gl, u32 p_cap, EngState* s) {
+__device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned char* gl, u32 p_cap, EngState* s,
+                                HeadRing* hr) {
   auto P = [&](int k) -> void* { return (L.smem[k] ? sm : gl) + L.off[k]; };
-  s->u = (u64*)P(L_U); s->tie = (u32*)P(L_TIE);
+  s->u = (u64*)P(L_U); s->tie = (u32*)P(L_TIE); s->hf = (u32*)P(L_HF);
   s->hk = (u32*)P(L_HK); s->hk_pos = (u32*)P(L_HKP); s->hm = (u32*)P(L_HM); s->hm_pos = (u32*)P(L_HMP);
-  s->b_fi = (u64*)P(L_BFI); s->b_id = (u32*)P(L_BID); s->nl_id = (u32*)P(L_NLID); s->nl_arr = (i64*)P(L_NLARR);
+  s->b = (BEnt*)P(L_B); s->nl_id = (u32*)P(L_NLID); s->nl_arr = (i64*)P(L_NLARR);
+  s->p = (PEnt*)P(L_P); s->p_cap = p_cap; s->W = (u64*)P(L_W);
   s->qh_front = (u32*)P(L_QHF); s->qh_next = (u32*)P(L_QHN); s->qh_cnt = (u32*)P(L_QHC);
   s->qc_head = (u32*)P(L_QCH); s->qc_tail = (u32*)P(L_QCT); s->qc_cnt = (u32*)P(L_QCC);
-  s->c_call = (u32*)P(L_CCALL); s->c_next = (u32*)P(L_CNEXT); s->c_seq = (u32*)P(L_CSEQ); s->c_t = (i64*)P(L_CT);
-  s->blocked = (u32*)P(L_BLK); s->p_t = (i64*)P(L_PT); s->p_id = (u32*)P(L_PID); s->p_cap = p_cap;
+  s->c_next = (u32*)P(L_CNEXT); s->c_nseq = (u32*)P(L_CNSEQ); s->c_t = (i64*)P(L_CT);
+  s->blocked = (u32*)P(L_BLK);
   s->r_t = (i64*)P(L_RT); s->r_tau = (u32*)P(L_RTAU); s->r_app = (uint8_t*)P(L_RAPP);
   s->r_head = (u32*)P(L_RHEAD); s->r_len = (u32*)P(L_RLEN);
+  if (hr) {
+    unsigned char* base = (unsigned char*)P(L_HR);
+    hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
+    hr->abort = (volatile u32*)(base + 12);
+    hr->e = (HEnt*)(base + 64);
+  }
 }
 
-// zero / NONE-initialise a replay's state (whole warp cooperates)
-__device__ inline void eng_clear(const EngState& s, u32 U, u64 n_heads, int lane, int nl) {
+// zero / NONE-initialise a replay's state (whole warp cooperates); W copied in
+__device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u64* W, u64 AJ, u32 U, int lane, int nl) {
   for (u32 k = lane; k < U; k += nl) {
-    s.u[k] = 0; s.tie[k] = 0; s.hk_pos[k] = NONE32; s.hm_pos[k] = NONE32;
-    s.qh_front[k] = 0; s.qh_next[k] = 0; s.qh_cnt[k] = 0; s.qc_head[k] = NONE32; s.qc_tail[k] = NONE32; s.qc_cnt[k] = 0;
+    s.u[k] = 0; s.tie[k] = 0; s.hf[k] = 0; s.hk_pos[k] = NONE32; s.hm_pos[k] = NONE32;
+    u32 o = (u32)sh.uh_off[k];
+    s.qh_front[k] = o; s.qh_next[k] = o; s.qh_cnt[k] = 0; s.qc_head[k] = NONE32; s.qc_tail[k] = NONE32; s.qc_cnt[k] = 0;
     s.r_head[k] = 0; s.r_len[k] = 0;
   }
-  for (u64 w = lane; w < n_heads / 32 + 1; w += nl) s.blocked[w] = 0;
+  for (u64 w = lane; w < sh.n_heads / 32 + 2; w += nl) s.blocked[w] = 0;
+  if (s.W != W) for (u64 k = lane; k < AJ; k += nl) s.W[k] = W[k];
 }
 
 struct ReplayKArgs {
@@ -519,21 +638,32 @@ struct ReplayKArgs {
   fs_replay_summary* sum; int* err_code; u64* err_idx; u32 p_cap;
 };
 
-// single replay: one CTA, one warp; lane 0 runs the serial engine
-__global__ void __launch_bounds__(32) k_replay(ReplayKArgs a) {
+// single replay: one CTA of two warps -- warp 0 lane 0 runs the serial engine,
+// warp 1 streams head arrivals into the shared ring
+__global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   EngState st;
-  eng_bind(a.L, sm, a.gmem, a.p_cap, &st);
-  eng_clear(st, a.U, a.sh.n_heads, threadIdx.x, 32);
-  __syncwarp();
-  __threadfence_block();
+  HeadRing hr;
+  eng_bind(a.L, sm, a.gmem, a.p_cap, &st, &hr);
+  u64 AJ = (u64)a.sh.A * a.sh.J1;
+  if (threadIdx.x == 0) { *hr.prod = 0; *hr.cons = 0; *hr.eof = 0; *hr.abort = 0; }
+  st.W = a.L.smem[L_W] ? st.W : (u64*)a.cfg.W;
+  eng_clear(st, a.sh, a.cfg.W, AJ, a.U, threadIdx.x, 64);
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    head_producer(&a.sh, &a.cfg, hr, a.cfg.mode == FS_MODE_WI);
+    return;
+  }
   if (threadIdx.x != 0) return;
   Engine E;
   E.init(&a.sh, &a.cfg, st, a.out, a.U);
+  E.use_ring = true;
+  E.ring = hr;
   E.run();
   *a.sum = E.sum;
   *a.err_code = E.err_code ? E.err_code + 1 : 0;
   *a.err_idx = E.err_idx;
+  *hr.abort = 1;                          // unblock the producer (error exit leaves heads unconsumed)
 }
 
 // sweep: one warp per scenario slot, scenarios taken from an atomic queue
@@ -545,16 +675,19 @@ __global__ void __launch_bounds__(128) k_sweep(SweepKArgs a) {
   int lane = threadIdx.x & 31;
   u32 slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   unsigned char* g = a.gmem + (size_t)slot * a.slot_bytes;
-  EngState st;
-  eng_bind(a.L, nullptr, g, a.p_cap, &st);
+  EngState st0;
+  eng_bind(a.L, nullptr, g, a.p_cap, &st0, nullptr);
   EngOut none;
   memset(&none, 0, sizeof(none));
+  u64 AJ = (u64)a.sh.A * a.sh.J1;
   for (;;) {
     u32 sc = 0;
     if (lane == 0) sc = atomicAdd(a.next, 1u);
     sc = __shfl_sync(FULL_MASK, sc, 0);
     if (sc >= a.n_scen) return;
-    eng_clear(st, a.U, a.sh.n_heads, lane, 32);
+    EngState st = st0;
+    st.W = (u64*)a.cfgs[sc].W;
+    eng_clear(st, a.sh, a.cfgs[sc].W, AJ, a.U, lane, 32);
     __syncwarp();
     __threadfence_block();
     if (lane == 0) {
@@ -571,7 +704,7 @@ __global__ void __launch_bounds__(128) k_sweep(SweepKArgs a) {
 // ------------------------------------------------------------------ online step (fs_wsc_step)
 struct StepKArgs {
   EngShared sh; EngCfg cfg; EngLayout L; u32 U; unsigned char* gmem; u32 p_cap;
-  i64* scal;             // persistent scalars: [0] e, [1] seq (+ hk_n, hm_n packed in [2], [3])
+  i64* scal;             // persistent scalars: [0] e, [1] seq, [2] hk_n, [3] hm_n
   i64 occ; u32 batch;
   const u32* fin; u32 nfin; const u32* arr; const i64* arr_t; u32 narr;
   uint8_t* arr_status; u32* admitted; u32* n_admitted; int* err_code; u64* err_idx;
@@ -579,7 +712,8 @@ struct StepKArgs {
 __global__ void k_step(StepKArgs a) {
   if (threadIdx.x != 0) return;
   EngState st;
-  eng_bind(a.L, nullptr, a.gmem, a.p_cap, &st);
+  eng_bind(a.L, nullptr, a.gmem, a.p_cap, &st, nullptr);
+  st.W = (u64*)a.cfg.W;
   EngOut none;
   memset(&none, 0, sizeof(none));
   Engine E;
@@ -589,24 +723,31 @@ __global__ void k_step(StepKArgs a) {
   E.occ = a.occ;
   *a.err_code = 0;
   for (u32 q = 0; q < a.nfin; q++) {                              // l.44-48
-    if (!E.charge(a.fin[q])) { *a.err_code = E.err_code + 1; *a.err_idx = a.fin[q]; return; }
+    if (!E.charge_call(a.fin[q])) { *a.err_code = E.err_code + 1; *a.err_idx = a.fin[q]; return; }
   }
   bool ovl = E.overloaded();
   for (u32 q = 0; q < a.narr; q++) {                              // l.11-25
     u32 r = a.arr[q];
-    if (m_tier(a.sh.t.meta[r]) > a.cfg.tier_max) { a.arr_status[q] = FS_ST_FILTERED; continue; }
-    int s = E.deliver(r, a.arr_t[q], ovl);
+    uint4 A = ldg4(&a.sh.recA[r]);
+    if (m_tier(A.z) > a.cfg.tier_max) { a.arr_status[q] = FS_ST_FILTERED; continue; }
+    int s;
+    if (m_stage(A.z) == 1) {
+      HEnt h;
+      memset(&h, 0, sizeof(h));
+      h.r = r; h.A = A; h.B = ldg4(&a.sh.recB[r]); h.C = ldg4(&a.sh.recC[r]);
+      s = E.deliver_head(h, a.arr_t[q], ovl);
+    } else {
+      s = E.deliver_cont(r, A.x, A.z, a.arr_t[q], ovl);
+    }
     if (s < 0) { *a.err_code = E.err_code + 1; *a.err_idx = r; return; }
     a.arr_status[q] = (uint8_t)s;
   }
   u32 na = 0;                                                      // l.28-39
   i64 occ = a.occ; u32 nb = a.batch;
-  for (;;) {
-    i64 arr;
-    u32 r = E.pick(occ, nb, &arr);
-    if (r == NONE32) break;
-    a.admitted[na++] = r;
-    occ += (i64)E.prompt(r);
+  Engine::Adm ad;
+  while (E.pick(occ, nb, &ad)) {
+    a.admitted[na++] = ad.r;
+    occ += (i64)ad.prompt;
     nb++;
   }
   *a.n_admitted = na;
