@@ -56,6 +56,7 @@ struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head
 
 struct EngState {                       // per replay; any array may live in smem or global
   u64* u; u32* tie; u32* hf;            // [U] counter (+class bit); tie of the front; front head id
+  u32* nf;                              // [U] KV need (prompt + reserve) of the front, NONE32 = unknown
   u32 *hk, *hk_pos, *hm, *hm_pos;       // heaps of queued users + positions [U]
   u32 *qh_front, *qh_next, *qh_cnt;     // [U] absolute uh_list positions
   u32 *qc_head, *qc_tail, *qc_cnt;      // [U] call ids
@@ -73,7 +74,7 @@ struct EngOut {                         // optional per-call outputs (single rep
 };
 
 struct HeadRing {                       // producer warp -> engine thread (shared memory)
-  HEnt* e;
+  HEnt* e; uint2* key;                  // entries and their (t_ms, id) keys
   volatile u32* prod; volatile u32* cons; volatile u32* eof; volatile u32* abort;
 };
 
@@ -95,6 +96,7 @@ struct Engine {
   u64 hp;                                // next head (trace order) when reading heads directly
   bool use_ring, static_heads, slot_by_call;
   HeadRing ring;
+  u32 rc_cons, rc_prod;                  // ring consumer index, last producer index seen
   HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
   u64 digest, n_adm;
   fs_replay_summary sum;
@@ -146,13 +148,14 @@ struct Engine {
   __device__ __forceinline__ void set_front_key(u32 k, u32 cont_seq) {
     if (s.qc_cnt[k]) { s.u[k] &= ~CLS_BIT; s.tie[k] = cont_seq; }
     else { s.u[k] |= CLS_BIT; s.tie[k] = s.hf[k]; }
+    s.nf[k] = NONE32;                                      // front changed: its KV need is unknown
   }
 
   __device__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
     sh = shr; c = cfg; s = st; o = out; U = nusers;
     hk_n = hm_n = b_n = p_n = nl_n = 0;
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
-    use_ring = false; static_heads = true; slot_by_call = true; cur_ok = false;
+    use_ring = false; static_heads = true; slot_by_call = true; cur_ok = false; rc_cons = rc_prod = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
@@ -161,8 +164,25 @@ struct Engine {
   __device__ __forceinline__ u64 increment(u32 user, u32 meta, const uint4& B, const uint4& Cc) const {
     u64 E = c->prio_q16 ? c->prio_q16[user] : (m_tier(meta) == 0 ? c->prio_b : c->prio_a);
     u64 N = (u64)c->alpha * Cc.z + (u64)c->beta * Cc.w + (u64)c->gamma * B.z;
-    u128 inc = (((u128)E * N) << 32) / s.W[Cc.x];
-    return inc >= ((u128)1 << 63) ? ~0ull : (u64)inc;
+    return q32_div(E * N, s.W[Cc.x]);
+  }
+  // floor(n * 2^32 / W) exactly (n < 2^60, W >= 1), ~0 if >= 2^63: a double-precision
+  // estimate corrected with the exact 128-bit remainder (cheaper than a u128 division).
+  __device__ __forceinline__ static double u128_to_d(u128 x) {
+    return (double)(u64)(x >> 64) * 18446744073709551616.0 + (double)(u64)x;
+  }
+  __device__ __forceinline__ static u64 q32_div(u64 n, u64 W) {
+    u128 num = (u128)n << 32;
+    double qd = __dmul_rn(__ddiv_rn((double)n, (double)W), 4294967296.0);
+    if (qd > 9.0e18) { u128 q = num / W; return q >= ((u128)1 << 63) ? ~0ull : (u64)q; }   // near overflow: exact
+    u64 q = (u64)qd;
+    u128 p = (u128)q * W;
+    if (p > num) { u64 cq = (u64)ceil(u128_to_d(p - num) / (double)W); q -= cq; }
+    else { u64 cq = (u64)(u128_to_d(num - p) / (double)W); q += cq; }
+    p = (u128)q * W;
+    while (p > num) { q--; p -= W; }
+    while (num - p >= W) { q++; p += W; }
+    return q >= (1ull << 63) ? ~0ull : q;
   }
   __device__ bool charge(u32 k, u64 inc, u32 r) {
     u64 cur = uval(k);
@@ -282,14 +302,18 @@ struct Engine {
   struct Adm { u32 r; u64 need, prompt; BEnt b; i64 arr; };
   __device__ bool pick(i64 occ_now, u32 nb, Adm* a) {
     if (hk_n == 0) return false;
+    if (nb >= c->Bmax) return false;                         // can_add_new_request (Q17): batch slots
     u32 k = s.hk[0];
+    u32 nfk = s.nf[k];                                       // cached need of the front: a failing
+    if (nfk != NONE32 && (u64)occ_now + nfk > c->C) return false;   // candidate costs no global load
     bool cont = s.qc_cnt[k] != 0;
     u32 r = cont ? s.qc_head[k] : s.hf[k];
     uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
     u32 nx = 0, nseq = 0; i64 ct = 0;
     if (cont) { nx = s.c_next[r]; nseq = s.c_nseq[r]; ct = s.c_t[r]; }
     u64 need = (u64)B.y + B.w;
-    if ((u128)(u64)occ_now + need > c->C || nb >= c->Bmax) return false;      // can_add_new_request (Q16, Q17)
+    s.nf[k] = (u32)need;
+    if ((u128)(u64)occ_now + need > c->C) return false;      // can_add_new_request (Q16, Q17): KV
     if (cont) {
       a->arr = ct;
       s.qc_head[k] = nx;
@@ -327,18 +351,38 @@ struct Engine {
   }
 
   // ---------------------------------------------------------------- heads source
-  __device__ __forceinline__ bool head_peek(HEnt* h) {
+  // next head arrival: (t_ms, call id) only; head_take() copies the whole entry
+  __device__ __forceinline__ bool head_peek(u32* tms, u32* rid) {
     if (use_ring) {
-      u32 cs = *ring.cons;
-      for (;;) {
-        if (*ring.prod != cs) break;
-        if (*ring.eof && *ring.prod == cs) return false;
-        __nanosleep(32);
+      if (rc_cons == rc_prod) {
+        for (;;) {
+          rc_prod = *ring.prod;
+          if (rc_prod != rc_cons) break;
+          if (*ring.eof) { rc_prod = *ring.prod; if (rc_prod == rc_cons) return false; break; }
+          __nanosleep(32);
+        }
+        __threadfence_block();
       }
-      __threadfence_block();
-      *h = ring.e[cs % HRING];
+      uint2 k = ring.key[rc_cons % HRING];
+      *tms = k.x; *rid = k.y;
       return true;
     }
+    HEnt h;
+    if (!head_peek_direct(&h)) return false;
+    *tms = h.A.y; *rid = h.r;
+    return true;
+  }
+  __device__ __forceinline__ void head_take(HEnt* h) {
+    if (use_ring) {
+      *h = ring.e[rc_cons % HRING];
+      rc_cons++;
+      *ring.cons = rc_cons;
+      return;
+    }
+    *h = cur;
+    cur_ok = false; hp++;
+  }
+  __device__ __forceinline__ bool head_peek_direct(HEnt* h) {
     if (!cur_ok) {
       while (hp < sh->n_heads) {
         u32 r = sh->heads[hp];
@@ -358,10 +402,6 @@ struct Engine {
     }
     *h = cur;
     return true;
-  }
-  __device__ __forceinline__ void head_pop() {
-    if (use_ring) { *ring.cons = *ring.cons + 1; return; }
-    cur_ok = false; hp++;
   }
 
   // ---------------------------------------------------------------- pending heap (t, id)
@@ -428,14 +468,14 @@ struct Engine {
   __device__ void run() {
     HEnt hh;
     for (;;) {
-      bool hok = head_peek(&hh);
-      i64 th = hok ? (i64)hh.A.y * 1000000 : 0;
+      u32 hms = 0, hid = 0;
+      bool hok = head_peek(&hms, &hid);
+      i64 th = (i64)hms * 1000000;
       bool pok = p_n != 0;
       // next pending arrival in (t, id) order
       bool pend = hok || pok;
-      i64 tn = 0;
-      if (hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hh.r < s.p[0].r))) tn = th;
-      else if (pok) tn = s.p[0].t;
+      bool is_head = hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hid < s.p[0].r));
+      i64 tn = is_head ? th : (pok ? s.p[0].t : 0);
       if (b_n == 0 && hk_n == 0) {                                // 1: idle engine restarts at the arrival
         if (!pend) break;
         if (tn > clock) clock = tn;
@@ -443,8 +483,8 @@ struct Engine {
       bool ovl = overloaded();                                    // 2: occupancy at iteration start
       while (pend && tn <= clock) {
         int st;
-        if (hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hh.r < s.p[0].r))) {
-          head_pop();
+        if (is_head) {
+          head_take(&hh);
           st = deliver_head(hh, th, ovl);
         } else {
           PEnt pe = s.p[0];
@@ -452,12 +492,12 @@ struct Engine {
           st = deliver_cont(pe.r, pe.user, pe.meta, pe.t, ovl);
         }
         if (st < 0) return;
-        hok = head_peek(&hh);
-        th = hok ? (i64)hh.A.y * 1000000 : 0;
+        hok = head_peek(&hms, &hid);
+        th = (i64)hms * 1000000;
         pok = p_n != 0;
         pend = hok || pok;
-        if (hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hh.r < s.p[0].r))) tn = th;
-        else if (pok) tn = s.p[0].t;
+        is_head = hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hid < s.p[0].r));
+        tn = is_head ? th : (pok ? s.p[0].t : 0);
       }
       u64 P_new = 0;                                              // 3: admission round
       nl_n = 0;
@@ -551,10 +591,15 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
     u32 cnt = __popc(mask);
     if (!cnt) continue;
     u32 ab = 0;
-    if (lane == 0) while (prod + cnt - *ring.cons > HRING && !(ab = *ring.abort)) __nanosleep(64);
+    // ring full: sleep long (the engine consumes ~1 head per microsecond at best)
+    if (lane == 0) while (prod + cnt - *ring.cons > HRING && !(ab = *ring.abort)) __nanosleep(2000);
     if (__shfl_sync(FULL_MASK, ab, 0)) return;     // the engine stopped on an error
     __syncwarp();
-    if (ok) ring.e[(prod + __popc(mask & lanemask_lt())) % HRING] = h;
+    if (ok) {
+      u32 slot = (prod + __popc(mask & lanemask_lt())) % HRING;
+      ring.e[slot] = h;
+      ring.key[slot] = make_uint2(h.A.y, h.r);
+    }
     __threadfence_block();
     __syncwarp();
     prod += cnt;
@@ -570,13 +615,13 @@ struct EngLayout {
   size_t off[32];
   bool smem[32];
 };
-enum { L_U, L_TIE, L_HF, L_HK, L_HKP, L_HM, L_HMP, L_B, L_NLID, L_NLARR, L_P, L_W, L_QHF, L_QHN, L_QHC, L_QCH, L_QCT,
+enum { L_U, L_TIE, L_HF, L_NF, L_HK, L_HKP, L_HM, L_HMP, L_B, L_NLID, L_NLARR, L_P, L_W, L_QHF, L_QHN, L_QHC, L_QCH, L_QCT,
        L_QCC, L_CNEXT, L_CNSEQ, L_CT, L_BLK, L_RT, L_RTAU, L_RAPP, L_RHEAD, L_RLEN, L_HR, L_N };
 
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
                             bool hring, size_t smem_budget) {
   size_t sz[L_N];
-  sz[L_U] = (size_t)U * 8; sz[L_TIE] = sz[L_HF] = (size_t)U * 4;
+  sz[L_U] = (size_t)U * 8; sz[L_TIE] = sz[L_HF] = sz[L_NF] = (size_t)U * 4;
   sz[L_HK] = sz[L_HKP] = sz[L_HM] = sz[L_HMP] = (size_t)U * 4;
   sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
   sz[L_P] = (size_t)p_cap * sizeof(PEnt); sz[L_W] = (size_t)AJ * 8;
@@ -585,9 +630,9 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
   size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
   sz[L_RT] = ring * 8; sz[L_RTAU] = ring * 4; sz[L_RAPP] = ring; sz[L_RHEAD] = sz[L_RLEN] = (size_t)U * 4;
-  sz[L_HR] = hring ? (size_t)HRING * sizeof(HEnt) + 64 : 0;
+  sz[L_HR] = hring ? (size_t)HRING * (sizeof(HEnt) + 8) + 64 : 0;
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_U, L_TIE, L_HF, L_HK, L_HKP, L_QCC, L_QHC,
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_U, L_TIE, L_HF, L_NF, L_HK, L_HKP, L_QCC, L_QHC,
                              L_QCH, L_QCT, L_QHF, L_QHN, L_HM, L_HMP, L_RHEAD, L_RLEN};
   EngLayout L;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
@@ -603,7 +648,7 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
 __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned char* gl, u32 p_cap, EngState* s,
                                 HeadRing* hr) {
   auto P = [&](int k) -> void* { return (L.smem[k] ? sm : gl) + L.off[k]; };
-  s->u = (u64*)P(L_U); s->tie = (u32*)P(L_TIE); s->hf = (u32*)P(L_HF);
+  s->u = (u64*)P(L_U); s->tie = (u32*)P(L_TIE); s->hf = (u32*)P(L_HF); s->nf = (u32*)P(L_NF);
   s->hk = (u32*)P(L_HK); s->hk_pos = (u32*)P(L_HKP); s->hm = (u32*)P(L_HM); s->hm_pos = (u32*)P(L_HMP);
   s->b = (BEnt*)P(L_B); s->nl_id = (u32*)P(L_NLID); s->nl_arr = (i64*)P(L_NLARR);
   s->p = (PEnt*)P(L_P); s->p_cap = p_cap; s->W = (u64*)P(L_W);
@@ -617,14 +662,14 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
     unsigned char* base = (unsigned char*)P(L_HR);
     hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
     hr->abort = (volatile u32*)(base + 12);
-    hr->e = (HEnt*)(base + 64);
+    hr->e = (HEnt*)(base + 64); hr->key = (uint2*)(base + 64 + HRING * sizeof(HEnt));
   }
 }
 
 // zero / NONE-initialise a replay's state (whole warp cooperates); W copied in
 __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u64* W, u64 AJ, u32 U, int lane, int nl) {
   for (u32 k = lane; k < U; k += nl) {
-    s.u[k] = 0; s.tie[k] = 0; s.hf[k] = 0; s.hk_pos[k] = NONE32; s.hm_pos[k] = NONE32;
+    s.u[k] = 0; s.tie[k] = 0; s.hf[k] = 0; s.nf[k] = NONE32; s.hk_pos[k] = NONE32; s.hm_pos[k] = NONE32;
     u32 o = (u32)sh.uh_off[k];
     s.qh_front[k] = o; s.qh_next[k] = o; s.qh_cnt[k] = 0; s.qc_head[k] = NONE32; s.qc_tail[k] = NONE32; s.qc_cnt[k] = 0;
     s.r_head[k] = 0; s.r_len[k] = 0;
