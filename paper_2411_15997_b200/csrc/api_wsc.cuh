@@ -76,6 +76,18 @@ __global__ void k_pack_records(DTrace t, const u32* next_call, u32 J, const u32*
   Cc[i] = make_uint4((u32)k, m_stage(m) == 1 ? posmap[i] : NONE32, Li, Ls);
 }
 
+// Eq. 3 / Alg. 1 l.48 increment of every call for one config: floor(E N 2^32 / W_aj), ~0 if >= 2^63
+__global__ void k_pack_inc(u64 n, const uint4* recA, const uint4* recB, const uint4* recC, EngCfg c, u64* inc) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint4 A = recA[i], Bv = recB[i], Cv = recC[i];
+  u64 E = c.prio_q16 ? c.prio_q16[A.x] : (m_tier(A.z) == 0 ? c.prio_b : c.prio_a);
+  u64 N = (u64)c.alpha * Cv.z + (u64)c.beta * Cv.w + (u64)c.gamma * Bv.z;
+  u64 w = c.W[Cv.x];
+  u128 q = w ? (((u128)E * N) << 32) / w : 0;
+  inc[i] = q >= ((u128)1 << 63) ? ~0ull : (u64)q;
+}
+
 struct WscShared {
   Links L;
   u32* heads; u64 n_heads;
@@ -302,6 +314,9 @@ static EngCfg eng_cfg(const fs_replay_cfg* c, const ScenTables& T, u32 s, u32 A,
   e.tier_max = c->tier_max; e.heads_only = c->act.count_mode == FS_COUNT_HEADS_ONLY;
   e.Wns = (i64)c->act.window_ms * 1000000;
   e.L = hl; e.ra = T.ra + (u64)s * A; e.ta = T.ta + (u64)s * A; e.W = T.W + (u64)s * AJ;
+  e.inc = nullptr;
+  if (c->overload_permille == 0xFFFFFFFFu) e.occ_thr = ~0ull;      // never overloaded
+  else e.occ_thr = (u64)(((u128)c->overload_permille * c->kv_capacity + 999) / 1000);
   return e;
 }
 
@@ -337,6 +352,10 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   int B = 256;
   u64 AJ = (u64)t.A * (P->J + 1);
   EngCfg ec = eng_cfg(cfg, T, 0, t.A, AJ, hl);
+  u64* incs = S.alloc<u64>(t.n + 1);                      // Eq. 3 increments: parallel, off the serial path
+  if (S.failed) return FS_E_NOMEM;
+  if (t.n) FS_LAUNCH(ctx, "pack_inc", k_pack_inc, div_up(t.n, B), B, 0, t.n, W.recA, W.recB, W.recC, ec, incs);
+  ec.inc = incs;
   EngOut eo;
   eo.status = o.status; eo.ovl = o.overloaded_at_arrival; eo.arrive = o.arrive_ns; eo.admit = o.admit_ns;
   eo.first = o.first_ns; eo.finish = o.finish_ns; eo.order = o.order; eo.counters = o.counters;

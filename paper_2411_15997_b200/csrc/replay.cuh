@@ -48,6 +48,8 @@ struct EngCfg {                         // one scenario
   i64 Wns;
   DLimits L; const u32* ra; const u64* ta;
   const u64* W;                         // [A][J1] Q16 stage weights for (alpha, beta, gamma)
+  const u64* inc;                       // per-call Eq. 3 increments precomputed in parallel (or null)
+  u64 occ_thr;                          // overloaded <=> occ >= occ_thr = ceil(theta C / 1000) (Q5)
 };
 
 struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
@@ -204,10 +206,10 @@ struct Engine {
     if (!c->heads_only || !static_heads) {
       u32 h = s.r_head[k], len = s.r_len[k];
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
-      while (len && s.r_t[base + h] <= tr - c->Wns) { h = (h + 1) % cap; len--; }   // leave the window (Q4)
+      while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // leave the window (Q4)
       s.r_head[k] = h; s.r_len[k] = len;
       for (u32 q = 0; q < len; q++) {
-        u32 idx = (h + q) % cap;
+        u32 idx = h + q; if (idx >= cap) idx -= cap;
         u64 tau = s.r_tau[base + idx];
         n_g++; t_g += tau;
         if (s.r_app[base + idx] == app) { n_a++; t_a += tau; }
@@ -223,9 +225,9 @@ struct Engine {
   __device__ bool ring_push(u32 k, i64 tr, u32 tau, u32 app, u32 r) {
     u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
     u32 h = s.r_head[k], len = s.r_len[k];
-    while (len && s.r_t[base + h] <= tr - c->Wns) { h = (h + 1) % cap; len--; }
+    while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }
     if (len == cap) { err_code = ERR_NOMEM; err_idx = r; return false; }
-    u32 idx = (h + len) % cap;
+    u32 idx = h + len; if (idx >= cap) idx -= cap;
     s.r_t[base + idx] = tr; s.r_tau[base + idx] = tau; s.r_app[base + idx] = (uint8_t)app;
     s.r_head[k] = h; s.r_len[k] = len + 1;
     return true;
@@ -313,7 +315,7 @@ struct Engine {
     if (cont) { nx = s.c_next[r]; nseq = s.c_nseq[r]; ct = s.c_t[r]; }
     u64 need = (u64)B.y + B.w;
     s.nf[k] = (u32)need;
-    if ((u128)(u64)occ_now + need > c->C) return false;      // can_add_new_request (Q16, Q17): KV
+    if ((u64)occ_now + need > c->C) return false;            // can_add_new_request (Q16, Q17): KV
     if (cont) {
       a->arr = ct;
       s.qc_head[k] = nx;
@@ -346,7 +348,7 @@ struct Engine {
     a->b.r = r; a->b.user = A.x; a->b.meta = A.z; a->b.link = A.w; a->b.think = B.x;
     a->b.rel = B.y + B.z;
     a->b.fi = iter + B.z - 1;
-    a->b.inc = increment(A.x, A.z, B, Cc);
+    a->b.inc = c->inc ? c->inc[r] : increment(A.x, A.z, B, Cc);
     return true;
   }
 
@@ -460,8 +462,7 @@ struct Engine {
   }
 
   __device__ __forceinline__ bool overloaded() const {   // Q5
-    if (c->theta == 0xFFFFFFFFu) return false;
-    return (u128)(u64)occ * 1000 >= (u128)c->theta * c->C;
+    return (u64)occ >= c->occ_thr;                        // occ * 1000 >= theta * C, exactly
   }
 
   // ---------------------------------------------------------------- the replay (O4 with event skipping)
@@ -523,8 +524,8 @@ struct Engine {
       if (nl_n == 0) {                                            // event skipping: B constant until
         m = s.b[0].fi - iter + 1;                                 //   the next finish ...
         if (pend && d > 0) {                                      //   ... or the next arrival
-          u64 ma = ((u64)(tn - clock) + d - 1) / d;
-          if (ma < m) m = ma;
+          u64 gap = (u64)(tn - clock);
+          if (gap <= m * d) m = (gap + d - 1) / d;                // first boundary at or after tn
         }
       }
       iter += m;
@@ -592,7 +593,9 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
     if (!cnt) continue;
     u32 ab = 0;
     // ring full: sleep long (the engine consumes ~1 head per microsecond at best)
-    if (lane == 0) while (prod + cnt - *ring.cons > HRING && !(ab = *ring.abort)) __nanosleep(2000);
+    // wait for half a ring of room, sleeping long: the engine needs microseconds per head
+    if (lane == 0 && prod + cnt - *ring.cons > HRING)
+      while (prod + HRING / 2 - *ring.cons > HRING && !(ab = *ring.abort)) __nanosleep(20000);
     if (__shfl_sync(FULL_MASK, ab, 0)) return;     // the engine stopped on an error
     __syncwarp();
     if (ok) {
