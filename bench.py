@@ -253,7 +253,7 @@ def main():
     # dominant kernel and its roofline
     dom = max(kt.items(), key=lambda kv: kv[1][1])
     dom_name, (dom_launches, dom_ms) = dom
-    roof = roofline(dom_name, dom_launches, dom_ms, N, peaks, peak_src, args)
+    roof = roofline(dom_name, dom_launches, dom_ms, N, peaks, peak_src, args, kt)
     line = {
         "metric": "trace requests throttled+scheduled/sec",
         "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -280,16 +280,58 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(name, launches, ms, N, peaks, src, args):
-    per_ms = ms / max(launches, 1)
+# ALGORITHMIC bytes per call of the kernels that touch every call once per launch
+ALGO_BYTES = {"prof_stream": 16, "win_gather": 36, "act_flags": 42, "pack_records": 84}
+
+
+def ncu_csv(path):
+    """{metric name: value} of the first kernel row of an ncu --csv --metrics log."""
+    import csv
+    try:
+        rows = [r for r in csv.reader(open(path)) if r and not r[0].startswith("==")]
+    except OSError:
+        return {}
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+    out = {}
+    for r in rows[1:]:
+        try:
+            out[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
+        except (KeyError, ValueError, IndexError):
+            pass
+    return out
+
+
+def roofline(name, launches, ms, N, peaks, src, args, kt):
+    per_s = ms / max(launches, 1) / 1e3
+    stages = []
+    for k, b in ALGO_BYTES.items():
+        if k in kt and kt[k][1] > 0:
+            gbs = b * N * kt[k][0] / (kt[k][1] / 1e3) / 1e9
+            stages.append({"kernel": k, "bound": "hbm", "bytes_per_call": b, "achieved": gbs,
+                           "peak": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"]})
     if name in ("wsc_replay", "wsc_sweep"):
-        # serial event chain: bound by one thread's dependent issue latency
-        peak = peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9     # G instr/s for one issuing thread
-        return {"bound": "alu", "kernel": name, "achieved": None, "peak": peak, "unit": "Ginstr/s (1 thread)",
-                "frac": None, "traffic": None, "ms_per_launch": per_ms, "peak_source": src,
-                "note": "serial replay; see profiles/ for instructions/event and ns/event"}
-    return {"bound": "hbm", "kernel": name, "ms_per_launch": per_ms, "achieved": None,
-            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": None, "traffic": None, "peak_source": src}
+        # dependent instruction chain: one engine warp (+ the head-prefetch warp) issuing at
+        # most one warp-instruction per cycle each at the measured max SM clock (DESIGN.md §6).
+        prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_replay.csv")) if args.workload == "c2" else {}
+        ghz = peaks.get("sm_max_mhz", 1965.0) / 1e3
+        peak = 2 * ghz
+        inst = prof.get("smsp__inst_executed.sum")
+        ncalls = 1_000_000
+        achieved = inst / ncalls * N / per_s / 1e9 if inst else None
+        traffic = None
+        if prof.get("dram__bytes_read.sum") is not None:
+            traffic = prof["dram__bytes_read.sum"] + prof.get("dram__bytes_write.sum", 0.0)
+        return {"bound": "alu", "kernel": name, "achieved": achieved, "peak": peak, "unit": "Ginst/s",
+                "frac": achieved / peak if achieved else None, "traffic": traffic, "ms_per_launch": per_s * 1e3,
+                "peak_source": src + " (2 issuing warps x 1 inst/cycle x sm_max_mhz)",
+                "instructions_per_call": inst / ncalls if inst else None,
+                "ns_per_call": per_s / N * 1e9, "hbm_stages": stages}
+    b = ALGO_BYTES.get(name, 0) * N
+    gbs = b / per_s / 1e9 if b else None
+    return {"bound": "hbm", "kernel": name, "ms_per_launch": per_s * 1e3, "achieved": gbs,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"] if gbs else None,
+            "traffic": None, "peak_source": src, "hbm_stages": stages}
 
 
 def cpu_baseline(workload, tr):

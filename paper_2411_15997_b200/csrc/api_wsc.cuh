@@ -46,12 +46,19 @@ __global__ void k_hw_win(u64 n, const u32* list, const u32* key, const u64* seg,
 }
 // per user: lowest tier of its calls, calls per tier, continuation count (ring capacity)
 __global__ void k_user_stats(DTrace t, u32* utier, unsigned long long* tier_calls, u64* ncont) {
+  __shared__ u32 th[256];                       // block-private tier histogram (16 hot bins)
+  th[threadIdx.x] = 0;
+  __syncthreads();
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= t.n) return;
-  u32 m = t.meta[i], tr = m_tier(m), u = t.user[i];
-  atomicMin(&utier[u], tr);
-  atomicAdd(&tier_calls[tr], 1ull);
-  if (m_stage(m) > 1) atomicAdd((unsigned long long*)&ncont[u], 1ull);
+  if (i < t.n) {
+    u32 m = t.meta[i], tr = m_tier(m), u = t.user[i];
+    if (utier[u] > tr) atomicMin(&utier[u], tr);
+    u32 peers = __match_any_sync(__activemask(), tr);
+    if ((threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) atomicAdd(&th[tr], (u32)__popc(peers));
+    if (m_stage(m) > 1) atomicAdd((unsigned long long*)&ncont[u], 1ull);
+  }
+  __syncthreads();
+  if (th[threadIdx.x]) atomicAdd(&tier_calls[threadIdx.x], (unsigned long long)th[threadIdx.x]);
 }
 __global__ void k_user_calls(DTrace t, u64* nc) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;

@@ -1,0 +1,56 @@
+"""GPU parity at BASELINE.json's full sizes, in bench.py's launch configuration,
+against oracle goldens written by tools/make_goldens.py (oracle/ only):
+profile tables, every per-call replay output (sha256), the replay digest/summary,
+and the ACT statuses on the replay's arrivals (P8 cross-check)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2411_15997_b200 import tracegen as G
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def h(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_full_size(name):
+    path = os.path.join(GOLD, f"full_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = json.load(open(path))
+    import torch
+    from paper_2411_15997_b200 import build, fairserve as F
+    build.build()
+    ctx = F.Context(0)
+    tr = G.generate(name)
+    assert tr["n_calls"] == g["n_calls"]
+    T = F.Trace(tr)
+    prof = F.build_app_profiles(ctx, T, g["profile_cfg"])
+    p = prof.read()
+    for k, v in g["profile"].items():
+        assert p[k].tolist() == v, k
+    for k, v in g["profile_sha"].items():
+        assert h(p[k]) == v, k
+    np.testing.assert_allclose(p["interp_q"], np.array(g["interp_q"]), rtol=1e-6)
+    o, s = F.wsc_replay(ctx, T, prof, g["engine"])
+    for k in ("n_arrived", "n_block", "n_dropped", "n_admitted", "n_finished", "n_iterations", "n_ovl_arrivals",
+              "makespan_ns", "sum_wait_ns", "max_wait_ns", "sum_ttft_ns", "u_min", "u_max", "digest"):
+        assert s[k] == g["replay_wi"][k], (k, s[k], g["replay_wi"][k])
+    conv = {"status": np.uint8, "ovl": np.uint8, "arrive_ns": np.int64, "admit_ns": np.int64, "first_ns": np.int64,
+            "finish_ns": np.int64, "order": np.uint32, "counters": np.uint64, "admitted_per_app": np.uint64}
+    for k, v in g["replay_sha"].items():
+        a = o[k].cpu().numpy().view(conv[k]) if o[k].dtype != torch.uint8 else o[k].cpu().numpy()
+        assert h(a) == v, k
+    st, sa = F.act_throttle(ctx, T, prof, g["engine"]["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+    assert h(st.cpu().numpy()) == g["act_sha"]
+    for k, v in g["act"].items():
+        assert sa[k] == v, k
+    _, sw = F.wsc_replay(ctx, T, prof, dict(g["engine"], mode=0), outputs=False)
+    assert sw["digest"] == g["replay_w"]["digest"]

@@ -1,0 +1,70 @@
+"""Write full-size oracle goldens (tests/golden/full_<cfg>.json) for the GPU parity
+tests at BASELINE sizes.  Calls only oracle/ and the seeded input generator.
+
+    python tools/make_goldens.py c2 [c3 ...]
+
+Each golden stores, for the bench's launch configuration (profile tier_max=0,
+FS(W+I) replay with profile-derived limits over every user, ACT on the replay's
+arrival times and overload flags) and for FS(W): the replay summary (incl. the
+digest over every delivery, admission, final counter and the makespan), sha256
+digests of the per-call output arrays, and the profile's small tables.
+"""
+import hashlib
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import oracle as O  # noqa: E402
+from paper_2411_15997_b200 import tracegen as G  # noqa: E402
+
+
+def h(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def run(name):
+    c = G.CONFIGS[name]
+    t0 = time.time()
+    tr = G.generate(name)
+    pcfg = dict(tier_max=c["profile"]["tier_max"], window_ms=60000, max_stage=64)
+    p = O.profile(tr, pcfg)
+    t1 = time.time()
+    act = dict(window_ms=60000, limits_from_profile=1, limit_mult_q8=0, count_mode=0)
+    eng = dict(c["engine"], mode=1, tier_max=255, alpha=1, beta=2, gamma=1, act=act)
+    o, s = O.replay(tr, p, eng)
+    t2 = time.time()
+    st, sa = O.act(tr, p, act, overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+    t3 = time.time()
+    ow, sw = O.replay(tr, p, dict(eng, mode=0), outputs=False)
+    out = {
+        "citation": "written by tools/make_goldens.py from oracle/ only (SURVEY.md §8(c) O2-O5); "
+                    "inputs: paper_2411_15997_b200/tracegen.py config " + name,
+        "config": name, "n_calls": tr["n_calls"], "profile_cfg": pcfg, "engine": eng,
+        "profile": {k: p[k].tolist() for k in ("T_req_a", "T_tok_a", "T_req_g", "T_tok_g", "nr_peak_r_a",
+                                                "nr_peak_t_a", "maxstage")},
+        "profile_sha": {k: h(p[k]) for k in ("cnt", "sum_in", "sum_sys", "sum_out", "hist", "nr_q", "peak_r_u",
+                                             "peak_t_u", "peak_r_ua", "peak_t_ua")},
+        "interp_q": p["interp_q"].tolist(),
+        "replay_wi": s, "replay_w": sw,
+        "replay_sha": {k: h(o[k]) for k in ("status", "ovl", "arrive_ns", "admit_ns", "first_ns", "finish_ns",
+                                            "order", "counters", "admitted_per_app")},
+        "act": {k: sa[k] for k in ("n_in", "n_admit", "n_block", "n_dropped", "n_filtered")},
+        "act_sha": h(st),
+        "act_equals_replay_status": bool((st == o["status"]).all()),
+        "oracle_seconds": {"profile": t1 - t0, "replay_wi": t2 - t1, "act": t3 - t2},
+    }
+    path = os.path.join(ROOT, "tests", "golden", f"full_{name}.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(name, "written", path, out["oracle_seconds"], flush=True)
+
+
+if __name__ == "__main__":
+    for nm in sys.argv[1:] or ["c2"]:
+        run(nm)
