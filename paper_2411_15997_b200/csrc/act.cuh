@@ -143,7 +143,7 @@ __global__ void k_act_flags(ActFlagArgs a, u32* flag, u64* tau) {
 
 struct ActDecideArgs {
   u64 n; const u32* meta; const uint8_t* ovl; const DLimits* L; const u32* ra; const u64* ta;
-  ActOrder u, ua; uint8_t* status; u32* changed;
+  ActOrder u, ua; uint8_t* status; u32* changed; const u32* user; u32* user_changed;
 };
 __global__ void k_act_decide(ActDecideArgs a) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -164,28 +164,137 @@ __global__ void k_act_decide(ActDecideArgs a) {
   else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
   else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
   else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
-  if (st != a.status[i]) { a.status[i] = st; *a.changed = 1; }
+  if (st != a.status[i]) { a.status[i] = st; *a.changed = 1; a.user_changed[a.user[i]] = 1; }
+}
+
+// ------------------------------------------------------------------ sequential fix-up (exact)
+// One warp per user whose decisions still changed in the last Jacobi pass: the warp
+// walks the user's calls in (t, id) order in lock-step (every lane computes the same
+// thing from values broadcast with shuffles), recomputing counted flags, window counts
+// and decisions from scratch -- the sequential definition itself.  Prefix values of
+// the recent positions live in a per-warp shared ring; older ones in the pass's global
+// prefix arrays, which the walk overwrites for its user.
+static const int WALK_R = 256;
+struct WalkRing { u32 cu, ca; u64 tu, ta; u32 st, pad; };
+struct ActWalkArgs {
+  const u32* users; u32 n_users_walk; const u64* seg_u;
+  const u32* perm_u; const u32* perm_ua; const u32* pos_ua; const u32* pos_u;
+  const u64* lb_u; const u64* lb_ua; const i64* ts_u;
+  u32* pc_u; u64* ptau_u; u32* pc_ua; u64* ptau_ua;
+  const u32* meta; const u32* head_of; const u64* tau_call; const uint8_t* ovl;
+  const DLimits* L; const u32* ra; const u64* ta; u32 heads_only, A;
+  uint8_t* status;
+};
+__global__ void __launch_bounds__(128) k_act_walk(ActWalkArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  WalkRing* ring = (WalkRing*)sm + wib * WALK_R;
+  u32* Ca = (u32*)((WalkRing*)sm + 4 * WALK_R) + wib * a.A;
+  u64* Ta = (u64*)((u32*)((WalkRing*)sm + 4 * WALK_R) + 4 * a.A) + wib * a.A;
+  u32 w = blockIdx.x * 4 + wib;
+  if (w >= a.n_users_walk) return;
+  const u32 u = a.users[w];
+  const u64 s = a.seg_u[u], e = a.seg_u[u + 1];
+  const DLimits L = *a.L;
+  for (u32 k = lane; k < a.A; k += 32) { Ca[k] = 0; Ta[k] = 0; }
+  __syncwarp();
+  u32 cu = s < e ? a.pc_u[s] : 0;          // running counts (any base: only differences matter)
+  u64 tu = s < e ? a.ptau_u[s] : 0;
+  for (u64 p0 = s; p0 < e; p0 += 32) {
+    u64 p = p0 + lane;
+    bool ok = p < e;
+    u32 id = 0, m = 0, q = 0, hp = 0; u64 tau = 0, lbu = 0, lbq = 0, lbx = 0; bool arr = false, ov = true;
+    if (ok) {
+      id = a.perm_u[p]; m = a.meta[id]; tau = a.tau_call[id]; q = a.pos_ua[id];
+      arr = a.ts_u[p] != INT64_MAX;
+      ov = a.ovl ? a.ovl[id] != 0 : true;
+      if (m_stage(m) == 1) { lbu = a.lb_u[p]; lbq = a.lb_ua[q]; lbx = a.pos_u[a.perm_ua[lbq]]; }
+      else hp = a.pos_u[a.head_of[id]];
+    }
+    u32 n = e - p0 < 32 ? (u32)(e - p0) : 32u;
+    for (u32 j = 0; j < n; j++) {
+      u64 pj = p0 + j;
+      u32 idj = __shfl_sync(FULL_MASK, id, j), mj = __shfl_sync(FULL_MASK, m, j), qj = __shfl_sync(FULL_MASK, q, j);
+      u64 tj = __shfl_sync(FULL_MASK, tau, j);
+      bool aj = __shfl_sync(FULL_MASK, arr, j), oj = __shfl_sync(FULL_MASK, ov, j);
+      u32 app = m_app(mj);
+      bool head = m_stage(mj) == 1;
+      u32 st = a.status[idj];                              // FILTERED / NOT_ARRIVED are final
+      bool live = st != FS_ST_FILTERED && aj;
+      bool counted = false;
+      if (live) {
+        if (head) counted = true;
+        else if (!a.heads_only) {
+          u64 hpj = __shfl_sync(FULL_MASK, (u64)hp, j);
+          u32 hs = pj - hpj < WALK_R ? ring[hpj % WALK_R].st : a.status[a.head_of[idj]];
+          counted = hs == FS_ST_ADMIT;
+        }
+      }
+      u32 ca = Ca[app]; u64 ta_ = Ta[app];
+      // before-values of this position (exclusive prefixes)
+      WalkRing rv; rv.cu = cu; rv.ca = ca; rv.tu = tu; rv.ta = ta_; rv.st = st; rv.pad = 0;
+      if (counted) { cu++; tu += tj; ca++; ta_ += tj; }
+      if (head && live && oj) {                            // Alg. 1 l.20-24 on the window (Q4)
+        u64 lbuj = __shfl_sync(FULL_MASK, lbu, j), lbxj = __shfl_sync(FULL_MASK, lbx, j);
+        u64 lbqj = __shfl_sync(FULL_MASK, lbq, j);
+        u32 bcu; u64 btu; u32 bca; u64 bta;
+        if (pj - lbuj < WALK_R && lbuj < pj) { bcu = ring[lbuj % WALK_R].cu; btu = ring[lbuj % WALK_R].tu; }
+        else if (lbuj == pj) { bcu = rv.cu; btu = rv.tu; }
+        else { bcu = a.pc_u[lbuj]; btu = a.ptau_u[lbuj]; }
+        if (pj - lbxj < WALK_R && lbxj < pj) { bca = ring[lbxj % WALK_R].ca; bta = ring[lbxj % WALK_R].ta; }
+        else if (lbxj == pj) { bca = rv.ca; bta = rv.ta; }
+        else { bca = a.pc_ua[lbqj]; bta = a.ptau_ua[lbqj]; }
+        u64 n_g = cu - bcu, t_g = tu - btu, n_a = ca - bca, t_a = ta_ - bta;
+        st = FS_ST_ADMIT;
+        if (L.rg && n_g > L.rg) st = FS_ST_BLOCK_USER_REQ;
+        else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
+        else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
+        else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
+      } else if (head && live) st = FS_ST_ADMIT;
+      rv.st = st;
+      __syncwarp();
+      if (lane == 0) {
+        ring[pj % WALK_R] = rv;
+        Ca[app] = ca; Ta[app] = ta_;
+        a.pc_u[pj] = rv.cu; a.ptau_u[pj] = rv.tu; a.pc_ua[qj] = rv.ca; a.ptau_ua[qj] = rv.ta;
+        if (head && live) a.status[idj] = (uint8_t)st;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void k_act_list(u32 U, const u32* uchg, u32* list, u32* n) {
+  u32 u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < U && uchg[u]) list[atomicAdd(n, 1u)] = u;
 }
 
 // final statuses of continuations / never-arrived calls, and the summary
+// (n_in, n_admit, n_block[4], n_dropped, n_filtered, n_inter_blocked, n_not_arrived;
+// block-reduced in shared memory, one global atomic per counter per block)
 __global__ void k_act_final(u64 n, const u32* meta, const u32* head_of, const u32* pos_u, const i64* ts_u,
                             uint8_t* status, unsigned long long* summ) {
+  __shared__ u32 c[10];
+  if (threadIdx.x < 10) c[threadIdx.x] = 0;
+  __syncthreads();
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  u32 m = meta[i];
-  uint8_t st = status[i];
-  bool arrived = ts_u[pos_u[i]] != INT64_MAX;
-  if (st != FS_ST_FILTERED) {
-    if (m_stage(m) > 1)     // DROPPED iff the head's final status is not ADMIT
-      st = status[head_of[i]] != FS_ST_ADMIT ? FS_ST_DROPPED : (arrived ? FS_ST_ADMIT : FS_ST_NOT_ARRIVED);
+  if (i < n) {
+    u32 m = meta[i];
+    uint8_t st = status[i];
+    bool arrived = ts_u[pos_u[i]] != INT64_MAX;
+    if (st != FS_ST_FILTERED) {
+      if (m_stage(m) > 1)     // DROPPED iff the head's final status is not ADMIT
+        st = status[head_of[i]] != FS_ST_ADMIT ? FS_ST_DROPPED : (arrived ? FS_ST_ADMIT : FS_ST_NOT_ARRIVED);
+    }
+    if (st == FS_ST_ADMIT) { atomicAdd(&c[0], 1u); atomicAdd(&c[1], 1u); }
+    else if (st >= 1 && st <= 4) {
+      atomicAdd(&c[0], 1u); atomicAdd(&c[1 + st], 1u);
+      if (m_ncalls(m) > 1) atomicAdd(&c[8], 1u);
+    } else if (st == FS_ST_DROPPED) atomicAdd(&c[6], 1u);
+    else if (st == FS_ST_FILTERED) atomicAdd(&c[7], 1u);
+    else if (st == FS_ST_NOT_ARRIVED) atomicAdd(&c[9], 1u);
+    status[i] = st;
   }
-  // summary: n_in, n_admit, n_block[4], n_dropped, n_filtered, n_inter_blocked, n_not_arrived
-  if (st == FS_ST_ADMIT) { atomicAdd(&summ[0], 1ull); atomicAdd(&summ[1], 1ull); }
-  else if (st >= 1 && st <= 4) {
-    atomicAdd(&summ[0], 1ull); atomicAdd(&summ[1 + st], 1ull);
-    if (m_ncalls(m) > 1) atomicAdd(&summ[8], 1ull);
-  } else if (st == FS_ST_DROPPED) atomicAdd(&summ[6], 1ull);
-  else if (st == FS_ST_FILTERED) atomicAdd(&summ[7], 1ull);
-  else if (st == FS_ST_NOT_ARRIVED) atomicAdd(&summ[9], 1ull);
-  status[i] = st;
+  __syncthreads();
+  if (threadIdx.x < 10 && c[threadIdx.x]) atomicAdd(&summ[threadIdx.x], (unsigned long long)c[threadIdx.x]);
 }

@@ -2,6 +2,7 @@
 // host orchestration of the kernels in *.cuh.  Every step of the path runs in those
 // kernels; host code here only sizes buffers, launches and reads back status words.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "act.cuh"
@@ -502,25 +503,47 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   ActOrder ou, oua;
   if (!act_order(ctx, S, t, tov, false, W, &ou) || !act_order(ctx, S, t, tov, true, W, &oua)) return FS_E_NOMEM;
   u32* changed = S.alloc<u32>(1);
+  u32* uchg = S.alloc<u32>(t.U + 1);
+  u32* ulist = S.alloc<u32>(t.U + 1);
+  u32* nlist = S.alloc<u32>(1);
   if (S.failed) return FS_E_NOMEM;
-  u64 passes = 0;
+  u64 passes = 0, fixup = 0;
   const u32 heads_only = cfg->count_mode == FS_COUNT_HEADS_ONLY;
+  // Jacobi passes before the exact per-user sequential walk of the users still changing
+  // (FS_ACT_JACOBI_MAX overrides the default 2, for tests of both paths)
+  const char* jenv = getenv("FS_ACT_JACOBI_MAX");
+  const u64 JACOBI_MAX = jenv ? (u64)std::max(1L, atol(jenv)) : 2;
   for (;;) {
     cudaMemsetAsync(changed, 0, 4, ctx->stream);
+    cudaMemsetAsync(uchg, 0, (t.U + 1) * 4, ctx->stream);
     for (ActOrder* ao : {&ou, &oua}) {
       ActFlagArgs fa{n, ao->o.perm, t.meta, L.head_of, status, tau_call, ao->ts, heads_only};
       FS_LAUNCH(ctx, "act_flags", k_act_flags, div_up(n, B), B, 0, fa, ao->flag, ao->tau);
       excl_scan<u32>(ctx, S, ao->flag, ao->pc, n, ao->pc + n);
       excl_scan<u64>(ctx, S, ao->tau, ao->ptau, n, ao->ptau + n);
     }
-    ActDecideArgs da{n, t.meta, overloaded, LD.L, LD.ra, LD.ta, ou, oua, status, changed};
+    ActDecideArgs da{n, t.meta, overloaded, LD.L, LD.ra, LD.ta, ou, oua, status, changed, t.user, uchg};
     FS_LAUNCH(ctx, "act_decide", k_act_decide, div_up(n, B), B, 0, da);
     passes++;
     u32 hc = 0;
     cudaMemcpyAsync(&hc, changed, 4, cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     if (!hc || heads_only) break;
-    if (passes > 100000) return FS_E_CUDA;    // unreachable: converges within #heads passes
+    if (passes >= JACOBI_MAX) {
+      cudaMemsetAsync(nlist, 0, 4, ctx->stream);
+      FS_LAUNCH(ctx, "act_list", k_act_list, div_up(t.U, B), B, 0, t.U, uchg, ulist, nlist);
+      u32 nw = 0;
+      cudaMemcpyAsync(&nw, nlist, 4, cudaMemcpyDeviceToHost, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      fixup = nw;
+      ActWalkArgs wa{ulist, nw, ou.o.seg, ou.o.perm, oua.o.perm, oua.pos, ou.pos, ou.lb, oua.lb, ou.ts,
+                     ou.pc, ou.ptau, oua.pc, oua.ptau, t.meta, L.head_of, tau_call, overloaded, LD.L, LD.ra,
+                     LD.ta, heads_only, t.A, status};
+      size_t smem = (size_t)4 * WALK_R * sizeof(WalkRing) + (size_t)4 * t.A * 12;
+      cudaFuncSetAttribute(k_act_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (nw) FS_LAUNCH(ctx, "act_walk", k_act_walk, div_up(nw, 4), 128, smem, wa);
+      break;
+    }
   }
   unsigned long long* summ = S.zeros<unsigned long long>(10);
   if (S.failed) return FS_E_NOMEM;
@@ -533,7 +556,7 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   for (int k = 0; k < 4; k++) sum->n_block[k] = hs[2 + k];
   sum->n_dropped = hs[6]; sum->n_filtered = hs[7]; sum->n_inter_blocked = hs[8]; sum->n_not_arrived = hs[9];
   sum->jacobi_passes = passes;
-  sum->n_fixup_users = 0;
+  sum->n_fixup_users = fixup;
   return FS_OK;
 }
 

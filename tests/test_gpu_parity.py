@@ -189,8 +189,15 @@ def test_profile_virtual_ranks(F, ctx):
 
 
 # ------------------------------------------------------------------ ACT
+@pytest.fixture(params=["1", "2", "1000"])
+def jacobi(request, monkeypatch):
+    """Jacobi passes before the sequential walk: walk-only, default, Jacobi-only."""
+    monkeypatch.setenv("FS_ACT_JACOBI_MAX", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("seed", range(60))
-def test_act_tiny(F, ctx, seed):
+def test_act_tiny(F, ctx, seed, jacobi):
     import torch
     rng = np.random.default_rng(5000 + seed)
     A = int(rng.integers(1, 3))
@@ -223,7 +230,7 @@ def test_act_tiny(F, ctx, seed):
 
 
 @pytest.mark.parametrize("mode", ["always", "random", "heads_only", "replay"])
-def test_act_c2_shape(F, ctx, mode):
+def test_act_c2_shape(F, ctx, mode, jacobi):
     import torch
     tr = G.generate(dict(G.CONFIGS["c2"], n_users=300, n_calls=200_000, seed=41))
     pcfg = dict(tier_max=0)
