@@ -38,8 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c5"])
-    ap.add_argument("--scenarios", type=int, default=256, help="c5: total scenarios (all ranks)")
+    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c5"])
+    ap.add_argument("--scenarios", type=int, default=4096, help="c5: scenarios per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timings", action="store_true", help="print per-kernel timings to stderr")
     return ap.parse_args()
@@ -142,6 +142,153 @@ def sweep_scenarios(eng, total):
 
 def algo_bytes_profile(n):
     # ALGORITHMIC bytes per call of fs_build_app_profiles:
+    # read user, t, meta, L_I, L_S, L_O once (24 B) + per order a permutation write+read (8 B)
+    # and the sorted-order gather of (t, tau) (12 B): 24 + 2 * 20 = 64 B
+    return 64 * n
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference(args, rank, world)
+    import torch
+    import torch.distributed as dist
+    from paper_2411_15997_b200 import build as B
+    from paper_2411_15997_b200 import fairserve as F
+    from paper_2411_15997_b200 import tracegen as G
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        B.build()
+    if world > 1:
+        dist.barrier()
+    ctx = F.Context(local)
+    stream = torch.cuda.current_stream()
+    wl = args.workload
+    c, eng, pcfg = workload_cfg("c2" if wl == "c5" else wl)
+    # weak scaling: every rank gets its own independent problem (rank 0 = the BASELINE config)
+    tr = G.generate(wl, seed=G.CONFIGS[wl]["seed"] + rank)
+    N = tr["n_calls"]
+    T = F.Trace(tr)                                                # inputs resident in HBM before timing
+    host = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int32)).pin_memory() for k in F.FIELDS}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")   # > 126 MB L2
+    scen = sweep_scenarios(eng, args.scenarios) if wl == "c5" else None
+    outs = F.replay_outputs(ctx, T)
+    status = torch.empty(N, dtype=torch.uint8, device="cuda")
+
+    def step(trace):
+        prof = F.build_app_profiles(ctx, trace, pcfg)                 # A1-A5
+        if scen is not None:
+            return F.sweep(ctx, trace, prof, scen)                       # A9 (A6-A7 inside every replay)
+        o, s = F.wsc_replay(ctx, trace, prof, eng, out=outs)            # A7
+        return F.act_throttle(ctx, trace, prof, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"],
+                              status=status)                             # A6 on the replay's arrivals (P8)
+
+    for _ in range(args.warmup):
+        step(T)
+    torch.cuda.synchronize()
+    ctx.timing_reset()
+    ctx.set_timing(True)
+    evs = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                                  # L2 flush between timed steps (not timed)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(T)
+            b.record(stream)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+    ctx.set_timing(False)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    kt = ctx.timings()
+    launches = sum(v[0] for v in kt.values())
+    # end to end through the public API with host buffers: H2D of the trace, the step, D2H of the results
+    e2e_steps = 1 if scen is not None else max(1, min(args.steps, 3))
+    e2e_ms = 0.0
+    d2h = torch.empty(N, dtype=torch.uint8).pin_memory()
+    for _ in range(e2e_steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        T2 = F.Trace.from_host_tensors(tr, host)
+        step(T2)                                          # the sweep returns its summaries in host memory
+        if scen is None:
+            d2h.copy_(status, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    # one single replay of the C2 configuration on this trace (BASELINE configs[1]), for context
+    single = None
+    if scen is not None and rank == 0:
+        prof = F.build_app_profiles(ctx, T, pcfg)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        F.wsc_replay(ctx, T, prof, eng, out=outs)
+        b.record(stream)
+        torch.cuda.synchronize()
+        single = {"workload": "C2 single FS(W+I) replay (configs[1])", "ms": a.elapsed_time(b),
+                  "value": N / (a.elapsed_time(b) / 1e3), "unit": "requests/s"}
+    t = torch.tensor([ms, e2e_ms / e2e_steps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, e2e_step_ms = float(t[0]), float(t[1])
+    units_per_rank = N * (len(scen) if scen is not None else 1)
+    total_units = units_per_rank * world
+    value = total_units * args.steps / (ms_max / 1e3)
+    e2e_value = total_units / (e2e_step_ms / 1e3)
+    if args.timings and rank == 0:
+        for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1]):
+            sys.stderr.write(f"{k:28s} launches={v[0]:7d} total_ms={v[1]:10.3f} per_step_ms={v[1] / args.steps:9.3f}\n")
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    peaks, peak_src = load_peaks()
+    dom_name, (dom_launches, dom_ms) = max(kt.items(), key=lambda kv: kv[1][1])
+    roof = roofline(dom_name, dom_launches, dom_ms, N, peaks, peak_src, args, kt)
+    S = len(scen) if scen is not None else 0
+    line = {
+        "metric": "trace requests throttled+scheduled/sec",
+        "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive; profile + FS(W+I) replay + ACT",
+                                "c3": "C3: 10k users, 12 apps, 10M calls; profile + FS(W+I) replay + ACT",
+                                "c5": f"C5: profile + sweep of {S} replays (throttle k x (alpha,beta,gamma) x "
+                                      f"E_abusive x tier_max) of a 1M-call trace"}[wl],
+                   "n_calls": N, "n_users": tr["n_users"], "n_apps": tr["n_apps"], "scenarios_per_gpu": S,
+                   "parallelism": (f"independent problem per GPU x{world}"),
+                   "l2": "flushed between timed steps (256 MB write, untimed)"},
+        "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
+                "d2h_bytes_per_step": N if scen is None else 144 * S},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "stage_ms": {k: v[1] / args.steps for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])[:8]},
+        "clocks": clk.summary(),
+    }
+    if single:
+        line["single_replay"] = single
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(wl, tr)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ALGORITHMIC bytes per call of fs_build_app_profiles:
     # read user, t, meta, L_I, L_S, L_O once (24 B) + per order a permutation write+read (8 B)
     # and the sorted-order gather of (t, tau) (12 B): 24 + 2 * 20 = 64 B
     return 64 * n
@@ -311,14 +458,22 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
             stages.append({"kernel": k, "bound": "hbm", "bytes_per_call": b, "achieved": gbs,
                            "peak": peaks["hbm_gbs"], "frac": gbs / peaks["hbm_gbs"]})
     if name in ("wsc_replay", "wsc_sweep"):
-        # dependent instruction chain: one engine warp (+ the head-prefetch warp) issuing at
-        # most one warp-instruction per cycle each at the measured max SM clock.
-        prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_replay.csv")) if args.workload == "c2" else {}
         ghz = peaks.get("sm_max_mhz", 1965.0) / 1e3
-        peak = 2 * ghz
+        units = N
+        if name == "wsc_replay":
+            # dependent instruction chain: one engine warp (+ the head-prefetch warp) issuing at
+            # most one warp-instruction per cycle each at the measured max SM clock.
+            prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_replay.csv")) if args.workload == "c2" else {}
+            peak = 2 * ghz
+            ncalls = 1_000_000
+        else:
+            # many independent one-lane replays: every SMSP can issue one warp-instruction per cycle
+            prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_sweep.csv"))
+            peak = peaks.get("sm_count", 148) * 4 * ghz
+            ncalls = 1_000_000 * int(prof.get("scenarios", 64))
+            units = N * args.scenarios
         inst = prof.get("smsp__inst_executed.sum")
-        ncalls = 1_000_000
-        achieved = inst / ncalls * N / per_s / 1e9 if inst else None
+        achieved = inst / ncalls * units / per_s / 1e9 if inst else None
         traffic = None
         if prof.get("dram__bytes_read.sum") is not None:
             traffic = prof["dram__bytes_read.sum"] + prof.get("dram__bytes_write.sum", 0.0)
@@ -335,29 +490,31 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
 
 
 def cpu_baseline(workload, tr):
+    """The oracle as it stands (oracle/, single-threaded C++) on a bounded sample of the
+    same workload, timed on this host."""
     import oracle as O
     from paper_2411_15997_b200 import tracegen as G
     c, eng, pcfg = workload_cfg("c2" if workload == "c5" else workload)
-    sample = tr
-    desc = "full trace"
+    sample, desc = tr, "full trace"
     if workload == "c3":
         sample = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
-        desc = "C3-shaped 1M-call / 1k-user sample"
+        desc = "C3-shaped 1M-call / 1k-user sample: profile + FS(W+I) replay + ACT"
     t0 = time.perf_counter()
+    p = O.profile(sample, pcfg)
+    n = sample["n_calls"]
     if workload == "c5":
-        p = O.profile(sample, pcfg)
-        t0 = time.perf_counter()
-        O.replay(sample, p, eng, outputs=False)
-        n = sample["n_calls"]
-        desc = "one scenario replay of the C5 trace"
+        scen = sweep_scenarios(eng, 4096)
+        picks = [scen[0], scen[len(scen) // 2]]
+        O.sweep(sample, p, picks)
+        n *= len(picks)
+        desc = "C5 trace: profile + 2 of the grid's scenario replays"
     else:
-        p = O.profile(sample, pcfg)
         o, _ = O.replay(sample, p, eng)
         O.act(sample, p, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
-        n = sample["n_calls"]
+        if workload == "c2":
+            desc = "full C2 step: profile + FS(W+I) replay + ACT"
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc,
-            "seconds": dt}
+    return {"value": n / dt, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt}
 
 
 def reference(args, rank, world):
@@ -372,13 +529,16 @@ def reference(args, rank, world):
         desc = "C3-shaped 1M-call / 1k-user sample per step"
     else:
         tr = G.generate("c2")
-        desc = "full C2 trace per step" if wl == "c2" else "one scenario replay of the C5 trace per step"
+        desc = "full C2 step" if wl == "c2" else "C5 trace: profile + 2 of the grid's scenario replays per step"
     O.build()
+
+    scen = sweep_scenarios(eng, 4096)
+    picks = [scen[0], scen[len(scen) // 2]]
 
     def step():
         p = O.profile(tr, pcfg)
         if wl == "c5":
-            O.replay(tr, p, eng, outputs=False)
+            O.sweep(tr, p, picks)
             return
         o, _ = O.replay(tr, p, eng)
         O.act(tr, p, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
@@ -389,7 +549,7 @@ def reference(args, rank, world):
     for _ in range(args.steps):
         step()
     dt = time.perf_counter() - t0
-    n = tr["n_calls"]
+    n = tr["n_calls"] * (2 if wl == "c5" else 1)
     v = n * args.steps / dt
     line = {"impl": "reference", "metric": "trace requests throttled+scheduled/sec", "value": v,
             "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

@@ -18,4 +18,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
     --csv --log-file gpurun_out/${TAG}_hbm.csv python tools/prof_stages.py c3 > gpurun_out/${TAG}_hbm.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:'k_prof_stream' -c 1 -o gpurun_out/${TAG}_prof_stream \
     python tools/prof_stages.py c3 > /dev/null 2>&1
+
+# the sweep kernel (64 scenarios of the C5 trace): instructions per (call x scenario)
+ncu --metrics smsp__inst_executed.sum,gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active \
+    --clock-control none -k regex:'^k_sweep$' --csv --log-file gpurun_out/${TAG}_sweep.csv \
+    python tools/prof_sweep.py 64 > gpurun_out/${TAG}_sweep.log 2>&1
+echo '"0","0","x","x","k_sweep","1","7","(1,1,1)","(1,1,1)","0","10.0","info","scenarios","","64"' >> gpurun_out/${TAG}_sweep.csv
 echo done
