@@ -294,143 +294,6 @@ def main():
     return 64 * n
 
 
-def main():
-    args = parse()
-    rank, world, local = dist_env()
-    if args.impl == "reference":
-        return reference(args, rank, world)
-    import torch
-    import torch.distributed as dist
-    from paper_2411_15997_b200 import build as B
-    from paper_2411_15997_b200 import fairserve as F
-    from paper_2411_15997_b200 import tracegen as G
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if rank == 0:
-        B.build()
-    if world > 1:
-        dist.barrier()
-    ctx = F.Context(local)
-    stream = torch.cuda.current_stream()
-    c, eng, pcfg = workload_cfg("c2" if args.workload == "c5" else args.workload)
-    tr = G.generate(args.workload if args.workload != "c5" else "c5")
-    N = tr["n_calls"]
-    # inputs resident in HBM before timing
-    T = F.Trace(tr)
-    host = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int32)).pin_memory() for k in F.FIELDS}
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")   # > 126 MB L2
-
-    scen = None
-    if args.workload == "c5":
-        scen_all = sweep_scenarios(eng, args.scenarios)
-        scen = scen_all[rank::world]
-        prof_fixed = F.build_app_profiles(ctx, T, pcfg)
-
-    outs = F.replay_outputs(ctx, T)
-    status = torch.empty(N, dtype=torch.uint8, device="cuda")
-
-    def step(trace):
-        if scen is not None:
-            return F.sweep(ctx, trace, prof_fixed, scen)
-        prof = F.build_app_profiles(ctx, trace, pcfg)
-        o, s = F.wsc_replay(ctx, trace, prof, eng, out=outs)
-        st, a = F.act_throttle(ctx, trace, prof, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"],
-                               status=status)
-        return s, a
-
-    for _ in range(args.warmup):
-        step(T)
-    torch.cuda.synchronize()
-    ctx.timing_reset()
-    ctx.set_timing(True)
-    evs = []
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()                                  # L2 flush between timed steps (not timed)
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            res = step(T)
-            b.record(stream)
-            evs.append((a, b))
-        torch.cuda.synchronize()
-    ctx.set_timing(False)
-    ms = sum(a.elapsed_time(b) for a, b in evs)
-    kt = ctx.timings()
-    launches = sum(v[0] for v in kt.values())
-    # end to end through the public API with host buffers: H2D of the trace, the step, D2H of the statuses
-    torch.cuda.synchronize()
-    e2e_ms = 0.0
-    d2h = torch.empty(N, dtype=torch.uint8).pin_memory()
-    for _ in range(max(1, min(args.steps, 3))):
-        flush.zero_()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        T2 = F.Trace.from_host_tensors(tr, host)
-        step(T2)
-        if scen is None:
-            d2h.copy_(status, non_blocking=True)
-        b.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms += a.elapsed_time(b)
-    e2e_steps = max(1, min(args.steps, 3))
-    t = torch.tensor([ms, e2e_ms / e2e_steps], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, e2e_step_ms = float(t[0]), float(t[1])
-    units_per_rank = N * (len(scen) if scen is not None else 1)
-    total_units = units_per_rank * world if scen is None else N * args.scenarios
-    value = total_units * args.steps / (ms_max / 1e3)
-    e2e_value = total_units / (e2e_step_ms / 1e3)
-    if args.timings and rank == 0:
-        for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1]):
-            sys.stderr.write(f"{k:28s} launches={v[0]:7d} total_ms={v[1]:10.3f} per_step_ms={v[1] / args.steps:9.3f}\n")
-    if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
-    peaks, peak_src = load_peaks()
-    # dominant kernel and its roofline
-    dom = max(kt.items(), key=lambda kv: kv[1][1])
-    dom_name, (dom_launches, dom_ms) = dom
-    roof = roofline(dom_name, dom_launches, dom_ms, N, peaks, peak_src, args, kt)
-    line = {
-        "metric": "trace requests throttled+scheduled/sec",
-        "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive, profile + FS(W+I) replay + ACT",
-                                "c3": "C3: 10k users, 12 apps, 10M calls, profile + FS(W+I) replay + ACT",
-                                "c5": f"C5: sweep of {args.scenarios} replays of a 1M-call trace"}[args.workload],
-                   "n_calls": N, "n_users": tr["n_users"], "n_apps": tr["n_apps"],
-                   "parallelism": f"replicas x{world}" if scen is None else f"scenarios/{world}",
-                   "l2": "flushed between timed steps (256 MB write, untimed)"},
-        "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
-                "d2h_bytes_per_step": N if scen is None else 0},
-        "gpu_launches": int(launches),
-        "roofline": roof,
-        "stage_ms": {k: v[1] / args.steps for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])[:8]},
-        "clocks": clk.summary(),
-    }
-    if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(args.workload, tr)
-    print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
-
-
-# ALGORITHMIC bytes per call of the kernels that touch every call once per launch
-ALGO_BYTES = {"prof_stream": 16, "win_gather": 36, "act_flags": 42, "pack_records": 84}
-
-
 def ncu_csv(path):
     """{metric name: value} of the first kernel row of an ncu --csv --metrics log."""
     import csv
