@@ -576,7 +576,7 @@ extern "C" int fs_wsc_state_read(fs_ctx* ctx, const fs_wsc_state* st, uint64_t* 
   Scratch S(ctx);
   u64* d = S.alloc<u64>(st->U + 1);
   if (S.failed) return FS_E_NOMEM;
-  const u64* u = (const u64*)(st->gm + st->L.off[L_U]);     // the step layout keeps everything in global memory
+  const UState* u = (const UState*)(st->gm + st->L.off[L_US]);   // the step layout keeps everything in global memory
   FS_LAUNCH(ctx, "step_read", k_step_read, div_up(st->U + 1, 256), 256, 0, st->U, u, d);
   i64 e = -1;
   cudaMemcpyAsync(counters, d, st->U * 8, cudaMemcpyDeviceToHost, ctx->stream);

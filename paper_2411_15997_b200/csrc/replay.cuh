@@ -5,25 +5,28 @@
 // arrivals, finishes and admissions the batch B is constant, so the m iterations
 // to the next event are applied in closed form (clock += m d, occ += m |B|).
 //
-// Latency design (the loop is a dependent chain, so every global round trip counts):
+// The loop is a dependent chain, so its cost is (instructions x latency) per call:
 //   * per-call packed records (3 x 16 B, built once per trace+profile) replace the
 //     8 SoA fields + profile lookups: one round trip fetches all a call needs;
-//   * counters, heaps, FIFO cursors, the batch heap (finish info carried in the
-//     entry) and the pending-continuation heap live in shared memory when they fit;
+//     a single replay also precomputes every Eq. 3 increment in parallel;
+//   * per-user state is one 64-B struct (one line per touch); the two heaps hold
+//     their keys inline (no indirection during sifts);
+//   * shared memory first (head ring, batch heap, weights, pending heap, user
+//     structs, heaps), global / L2 for the rest;
 //   * single replay: a producer warp streams the (t, id)-ordered head arrivals with
 //     their records and static ACT windows into a shared-memory ring ahead of the
 //     engine thread, so head deliveries never wait on global memory.
-// Data structures: counters u[U] (Q32.32, bit 63 = "front is a head" class bit);
+// Data structures: counters u (Q32.32, bit 63 = "front is a head" class bit);
 // per-user FIFOs: heads as a cursor over the user's (t, id)-ordered head list (+ a
 // blocked bitset), continuations as a linked list through per-call slots; indexed
-// binary heaps of queued users keyed (class, u, tie) for the pick (l.31-38) and
-// keyed u for the lift (l.16-18); ACT: static head windows shared by all replays +
-// a per-user ring of recent continuation arrivals.
+// binary heaps of queued users keyed (class|u, tie) for the pick (l.31-38) and keyed
+// u for the lift (l.16-18); ACT: static head windows shared by all replays + a
+// per-user ring of recent continuation arrivals.
 #pragma once
 #include "act.cuh"
 
 static const u32 SWEEP_RING_CAP = 512;  // sweep: continuation arrivals kept per user window (FS_E_NOMEM beyond)
-static const u32 HRING = 128;         // head prefetch ring entries
+static const u32 HRING = 128;           // head prefetch ring entries
 
 struct EngShared {                      // read-only, shared by every replay of a trace
   DTrace t;
@@ -52,21 +55,29 @@ struct EngCfg {                         // one scenario
   u64 occ_thr;                          // overloaded <=> occ >= occ_thr = ceil(theta C / 1000) (Q5)
 };
 
+struct alignas(16) UState {             // per user, 64 B
+  u64 u;                                // counter, Q32.32; bit 63 = class of the queue front (1 = head)
+  u32 tie, hf, nf;                      // tie of the front; front head id; KV need of the front (NONE = ?)
+  u32 hk_pos, hm_pos;                   // heap positions (NONE = not queued)
+  u32 qh_front, qh_next, qh_cnt;        // head FIFO: absolute uh_list positions, queued count
+  u32 qc_head, qc_tail, qc_cnt;         // continuation FIFO (call ids)
+  u32 r_head, r_len;                    // ACT continuation ring
+  u32 pad;
+};
+struct HK { u64 key; u32 tie, user; };  // pick heap entry: (class | u, tie)
+struct HM { u64 u; u32 user, pad; };    // lift heap entry: u
+struct CSlot { u32 next, nseq; i64 t; };   // queued continuation: next in FIFO, its seq, own arrival
 struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
 struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
 
-struct EngState {                       // per replay; any array may live in smem or global
-  u64* u; u32* tie; u32* hf;            // [U] counter (+class bit); tie of the front; front head id
-  u32* nf;                              // [U] KV need (prompt + reserve) of the front, NONE32 = unknown
-  u32 *hk, *hk_pos, *hm, *hm_pos;       // heaps of queued users + positions [U]
-  u32 *qh_front, *qh_next, *qh_cnt;     // [U] absolute uh_list positions
-  u32 *qc_head, *qc_tail, *qc_cnt;      // [U] call ids
-  u32 *c_next, *c_nseq; i64* c_t;       // [slots] queued continuation links, next's seq, arrival
-  u32* blocked;                         // [n_heads/32 + 1] bitset over uh positions
+struct EngState {
+  UState* us; HK* hk; HM* hm;
+  CSlot* cs;                            // [slots] per call
+  u32* blocked;                         // [n_heads/32 + 2] bitset over uh positions
   BEnt* b; u32* nl_id; i64* nl_arr;     // B heap [Bmax]; calls admitted this round [Bmax]
   PEnt* p; u32 p_cap;                   // pending continuation heap
-  i64* r_t; u32* r_tau; uint8_t* r_app; u32* r_head; u32* r_len;   // [ring slots] (CSR by user) + [U]
+  i64* r_t; u32* r_tau; uint8_t* r_app; // ACT rings [ring slots] (CSR by user)
   u64* W;                               // stage weights (smem copy or the scenario's table)
 };
 
@@ -96,7 +107,7 @@ struct Engine {
   i64 e;                                 // last user to exit Q (Alg. 1 l.14), -1 = NONE
   u32 seq;
   u64 hp;                                // next head (trace order) when reading heads directly
-  bool use_ring, static_heads, slot_by_call;
+  bool use_ring, static_heads;
   HeadRing ring;
   u32 rc_cons, rc_prod;                  // ring consumer index, last producer index seen
   HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
@@ -104,65 +115,67 @@ struct Engine {
   fs_replay_summary sum;
   int err_code; u64 err_idx;
 
-  // ---------------------------------------------------------------- keys and heaps
-  __device__ __forceinline__ u64 uval(u32 k) const { return s.u[k] & ~CLS_BIT; }
-  __device__ __forceinline__ bool kless(u32 a, u32 b) const {   // (class, u, tie)
-    u64 ka = s.u[a], kb = s.u[b];
-    if (ka != kb) return ka < kb;
-    return s.tie[a] < s.tie[b];
-  }
-  __device__ __forceinline__ bool mless(u32 a, u32 b) const {
-    u64 ka = uval(a), kb = uval(b);
-    return ka != kb ? ka < kb : a < b;
-  }
-  template <bool K> __device__ void h_up(u32* h, u32* pos, u32 i) {
-    u32 x = h[i];
+  // ---------------------------------------------------------------- heaps with inline keys
+  __device__ __forceinline__ static bool kl(const HK& a, const HK& b) { return a.key < b.key || (a.key == b.key && a.tie < b.tie); }
+  __device__ __forceinline__ static bool ml(const HM& a, const HM& b) { return a.u < b.u || (a.u == b.u && a.user < b.user); }
+  __device__ void hk_up(u32 i, HK x) {
     while (i > 0) {
-      u32 pi = (i - 1) >> 1, p = h[pi];
-      if (!(K ? kless(x, p) : mless(x, p))) break;
-      h[i] = p; pos[p] = i; i = pi;
+      u32 pi = (i - 1) >> 1;
+      HK p = s.hk[pi];
+      if (!kl(x, p)) break;
+      s.hk[i] = p; s.us[p.user].hk_pos = i; i = pi;
     }
-    h[i] = x; pos[x] = i;
+    s.hk[i] = x; s.us[x.user].hk_pos = i;
   }
-  template <bool K> __device__ void h_down(u32* h, u32* pos, u32 n, u32 i) {
-    u32 x = h[i];
+  __device__ void hk_down(u32 i, HK x) {
     for (;;) {
       u32 l = 2 * i + 1;
-      if (l >= n) break;
-      u32 r = l + 1, m = l;
-      if (r < n && (K ? kless(h[r], h[l]) : mless(h[r], h[l]))) m = r;
-      if (!(K ? kless(h[m], x) : mless(h[m], x))) break;
-      h[i] = h[m]; pos[h[m]] = i; i = m;
+      if (l >= hk_n) break;
+      HK cl = s.hk[l];
+      if (l + 1 < hk_n) { HK cr = s.hk[l + 1]; if (kl(cr, cl)) { cl = cr; l++; } }
+      if (!kl(cl, x)) break;
+      s.hk[i] = cl; s.us[cl.user].hk_pos = i; i = l;
     }
-    h[i] = x; pos[x] = i;
+    s.hk[i] = x; s.us[x.user].hk_pos = i;
   }
-  template <bool K> __device__ void h_remove(u32* h, u32* pos, u32& n, u32 k) {
-    u32 i = pos[k];
-    pos[k] = NONE32;
-    n--;
-    if (i == n) return;
-    u32 last = h[n];
-    h[i] = last; pos[last] = i;
-    h_up<K>(h, pos, i);
-    h_down<K>(h, pos, n, pos[last]);
+  __device__ void hm_up(u32 i, HM x) {
+    while (i > 0) {
+      u32 pi = (i - 1) >> 1;
+      HM p = s.hm[pi];
+      if (!ml(x, p)) break;
+      s.hm[i] = p; s.us[p.user].hm_pos = i; i = pi;
+    }
+    s.hm[i] = x; s.us[x.user].hm_pos = i;
   }
-  __device__ __forceinline__ bool queued(u32 k) const { return s.qh_cnt[k] + s.qc_cnt[k] != 0; }
-  __device__ __forceinline__ void set_front_key(u32 k, u32 cont_seq) {
-    if (s.qc_cnt[k]) { s.u[k] &= ~CLS_BIT; s.tie[k] = cont_seq; }
-    else { s.u[k] |= CLS_BIT; s.tie[k] = s.hf[k]; }
-    s.nf[k] = NONE32;                                      // front changed: its KV need is unknown
+  __device__ void hm_down(u32 i, HM x) {
+    for (;;) {
+      u32 l = 2 * i + 1;
+      if (l >= hm_n) break;
+      HM cl = s.hm[l];
+      if (l + 1 < hm_n) { HM cr = s.hm[l + 1]; if (ml(cr, cl)) { cl = cr; l++; } }
+      if (!ml(cl, x)) break;
+      s.hm[i] = cl; s.us[cl.user].hm_pos = i; i = l;
+    }
+    s.hm[i] = x; s.us[x.user].hm_pos = i;
+  }
+  __device__ void heaps_remove(u32 k, u32 pk, u32 pm) {   // user k leaves Q
+    hk_n--;
+    if (pk != hk_n) { HK last = s.hk[hk_n]; if (pk > 0 && kl(last, s.hk[(pk - 1) >> 1])) hk_up(pk, last); else hk_down(pk, last); }
+    hm_n--;
+    if (pm != hm_n) { HM last = s.hm[hm_n]; if (pm > 0 && ml(last, s.hm[(pm - 1) >> 1])) hm_up(pm, last); else hm_down(pm, last); }
+    s.us[k].hk_pos = NONE32; s.us[k].hm_pos = NONE32;
   }
 
   __device__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
     sh = shr; c = cfg; s = st; o = out; U = nusers;
     hk_n = hm_n = b_n = p_n = nl_n = 0;
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
-    use_ring = false; static_heads = true; slot_by_call = true; cur_ok = false; rc_cons = rc_prod = 0;
+    use_ring = false; static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
 
-  // ---------------------------------------------------------------- Eq. 3 at finish (l.44-48)
+  // ---------------------------------------------------------------- Eq. 3 (l.44-48)
   __device__ __forceinline__ u64 increment(u32 user, u32 meta, const uint4& B, const uint4& Cc) const {
     u64 E = c->prio_q16 ? c->prio_q16[user] : (m_tier(meta) == 0 ? c->prio_b : c->prio_a);
     u64 N = (u64)c->alpha * Cc.z + (u64)c->beta * Cc.w + (u64)c->gamma * B.z;
@@ -187,12 +200,17 @@ struct Engine {
     return q >= (1ull << 63) ? ~0ull : q;
   }
   __device__ bool charge(u32 k, u64 inc, u32 r) {
-    u64 cur = uval(k);
+    UState& us = s.us[k];
+    u64 cur = us.u & ~CLS_BIT;
     if (inc == ~0ull || cur + inc >= (1ull << 63)) { err_code = ERR_OVERFLOW; err_idx = r; return false; }
-    s.u[k] += inc;                                        // class bit untouched (no carry: u < 2^63)
-    if (s.hk_pos[k] != NONE32) {                          // queued: keys increased
-      h_down<true>(s.hk, s.hk_pos, hk_n, s.hk_pos[k]);
-      h_down<false>(s.hm, s.hm_pos, hm_n, s.hm_pos[k]);
+    u64 nu = us.u + inc;                                 // class bit untouched (no carry: u < 2^63)
+    us.u = nu;
+    u32 pk = us.hk_pos;
+    if (pk != NONE32) {                                  // queued: both keys increased
+      HK x; x.key = nu; x.tie = us.tie; x.user = k;
+      hk_down(pk, x);
+      HM y; y.u = nu & ~CLS_BIT; y.user = k; y.pad = 0;
+      hm_down(us.hm_pos, y);
     }
     return true;
   }
@@ -202,12 +220,12 @@ struct Engine {
   }
 
   // ---------------------------------------------------------------- ACT window check (l.19-24)
-  __device__ int act_check(u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
+  __device__ int act_check(UState& us, u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
     if (!c->heads_only || !static_heads) {
-      u32 h = s.r_head[k], len = s.r_len[k];
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
-      while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // leave the window (Q4)
-      s.r_head[k] = h; s.r_len[k] = len;
+      u32 h = us.r_head, len = us.r_len;
+      while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // (Q4)
+      us.r_head = h; us.r_len = len;
       for (u32 q = 0; q < len; q++) {
         u32 idx = h + q; if (idx >= cap) idx -= cap;
         u64 tau = s.r_tau[base + idx];
@@ -222,24 +240,24 @@ struct Engine {
     if (c->ta[app] && t_a > c->ta[app]) return FS_ST_BLOCK_APP_TOK;
     return FS_ST_ADMIT;
   }
-  __device__ bool ring_push(u32 k, i64 tr, u32 tau, u32 app, u32 r) {
+  __device__ bool ring_push(UState& us, u32 k, i64 tr, u32 tau, u32 app, u32 r) {
     u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
-    u32 h = s.r_head[k], len = s.r_len[k];
+    u32 h = us.r_head, len = us.r_len;
     while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }
     if (len == cap) { err_code = ERR_NOMEM; err_idx = r; return false; }
     u32 idx = h + len; if (idx >= cap) idx -= cap;
     s.r_t[base + idx] = tr; s.r_tau[base + idx] = tau; s.r_app[base + idx] = (uint8_t)app;
-    s.r_head[k] = h; s.r_len[k] = len + 1;
+    us.r_head = h; us.r_len = len + 1;
     return true;
   }
 
-  // lift (l.12-18) for a user about to deliver; returns whether it was queued
-  __device__ __forceinline__ bool lift(u32 k) {
-    if (queued(k)) return true;
-    u64 uk = uval(k), l;
-    if (hm_n == 0) l = e >= 0 ? uval((u32)e) : 0;           // l.13-15
-    else l = uval(s.hm[0]);                                 // l.16-18
-    if (l > uk) s.u[k] = (s.u[k] & CLS_BIT) | l;
+  // lift (l.12-18); returns whether the user was queued
+  __device__ __forceinline__ bool lift(UState& us) {
+    if (us.qh_cnt + us.qc_cnt != 0) return true;
+    u64 l;
+    if (hm_n == 0) l = e >= 0 ? (s.us[(u32)e].u & ~CLS_BIT) : 0;   // l.13-15
+    else l = s.hm[0].u;                                             // l.16-18
+    if (l > (us.u & ~CLS_BIT)) us.u = (us.u & CLS_BIT) | l;
     return false;
   }
   __device__ __forceinline__ void arrived(u32 r, i64 tr, bool ovl) {
@@ -247,9 +265,11 @@ struct Engine {
     if (ovl) sum.n_ovl_arrivals++;
     if (o.arrive) { o.arrive[r] = tr; o.ovl[r] = ovl; }
   }
-  __device__ __forceinline__ void newly_queued(u32 k) {
-    s.hk[hk_n] = k; h_up<true>(s.hk, s.hk_pos, hk_n++);
-    s.hm[hm_n] = k; h_up<false>(s.hm, s.hm_pos, hm_n++);
+  __device__ __forceinline__ void newly_queued(UState& us, u32 k) {
+    HK x; x.key = us.u; x.tie = us.tie; x.user = k;
+    hk_up(hk_n++, x);
+    HM y; y.u = us.u & ~CLS_BIT; y.user = k; y.pad = 0;
+    hm_up(hm_n++, y);
   }
 
   // ---------------------------------------------------------------- deliveries (l.11-25)
@@ -257,103 +277,116 @@ struct Engine {
   __device__ int deliver_head(const HEnt& h, i64 tr, bool ovl) {
     u32 r = h.r, k = h.A.x, m = h.A.z;
     u32 upos = h.C.y;
-    if (upos != s.qh_next[k]) { err_code = ERR_ORDER; err_idx = r; return -1; }   // (t, id) order per user
+    UState& us = s.us[k];
+    if (upos != us.qh_next) { err_code = ERR_ORDER; err_idx = r; return -1; }   // (t, id) order per user
     arrived(r, tr, ovl);
-    bool was = lift(k);
+    bool was = lift(us);
     int st = FS_ST_ADMIT;
     if (c->mode == FS_MODE_WI) {
-      if (!static_heads && !ring_push(k, tr, h.B.y + h.B.w, m_app(m), r)) return -1;   // l.19
-      if (ovl) st = act_check(k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);                  // l.20-24
+      if (!static_heads && !ring_push(us, k, tr, h.B.y + h.B.w, m_app(m), r)) return -1;   // l.19
+      if (ovl) st = act_check(us, k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);                 // l.20-24
     }
     digest = sm64(digest ^ ((u64)r * 16 + (u64)st));
-    s.qh_next[k] = upos + 1;
+    us.qh_next = upos + 1;
     if (st != FS_ST_ADMIT) {
       s.blocked[upos >> 5] |= 1u << (upos & 31);
-      if (s.qh_cnt[k] == 0) s.qh_front[k] = upos + 1;
+      if (us.qh_cnt == 0) us.qh_front = upos + 1;
       sum.n_block[st - 1]++;
       sum.n_dropped += m_ncalls(m) - 1;
       if (o.status) o.status[r] = (uint8_t)st;
       return st;
     }
-    if (s.qh_cnt[k] == 0) { s.qh_front[k] = upos; s.hf[k] = r; }
-    s.qh_cnt[k]++;
+    if (us.qh_cnt == 0) { us.qh_front = upos; us.hf = r; }
+    us.qh_cnt++;
     seq++;
-    if (!was) { set_front_key(k, 0); newly_queued(k); }
+    if (!was) {                                             // newly queued: class 1, front = this head
+      us.u |= CLS_BIT; us.tie = r; us.nf = h.B.y + h.B.w;
+      newly_queued(us, k);
+    }
     return FS_ST_ADMIT;
   }
   __device__ int deliver_cont(u32 r, u32 k, u32 m, i64 tr, bool ovl) {
+    UState& us = s.us[k];
     arrived(r, tr, ovl);
-    bool was = lift(k);
+    bool was = lift(us);
     if (c->mode == FS_MODE_WI && !c->heads_only) {          // l.19 (continuations are never throttled)
       uint4 B = ldg4(&sh->recB[r]);
-      if (!ring_push(k, tr, B.y + B.w, m_app(m), r)) return -1;
+      if (!ring_push(us, k, tr, B.y + B.w, m_app(m), r)) return -1;
     }
     digest = sm64(digest ^ ((u64)r * 16));
-    u32 x = r;
-    s.c_next[x] = NONE32; s.c_t[x] = tr;
-    if (s.qc_cnt[k] == 0) s.qc_head[k] = x; else { s.c_next[s.qc_tail[k]] = x; s.c_nseq[s.qc_tail[k]] = seq; }
-    s.qc_tail[k] = x;
-    s.qc_cnt[k]++;
+    CSlot cs; cs.next = NONE32; cs.nseq = 0; cs.t = tr;
+    s.cs[r] = cs;
+    if (us.qc_cnt == 0) us.qc_head = r; else { s.cs[us.qc_tail].next = r; s.cs[us.qc_tail].nseq = seq; }
+    us.qc_tail = r;
+    us.qc_cnt++;
     u32 myseq = seq++;
-    if (!was) { set_front_key(k, myseq); newly_queued(k); }
-    else if (s.qc_cnt[k] == 1) { set_front_key(k, myseq); h_up<true>(s.hk, s.hk_pos, s.hk_pos[k]); }   // class 1 -> 0
+    if (!was) {                                             // newly queued: class 0
+      us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
+      newly_queued(us, k);
+    } else if (us.qc_cnt == 1) {                            // class 1 -> 0: key decreased
+      us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
+      HK x; x.key = us.u; x.tie = myseq; x.user = k;
+      hk_up(us.hk_pos, x);
+    }
     return FS_ST_ADMIT;
   }
 
   // ---------------------------------------------------------------- one pick (l.28-39)
-  struct Adm { u32 r; u64 need, prompt; BEnt b; i64 arr; };
+  struct Adm { u32 r; u64 prompt; BEnt b; i64 arr; };
+  // Returns false if Q is empty or the candidate does not fit (Q16, Q17).
   __device__ bool pick(i64 occ_now, u32 nb, Adm* a) {
-    if (hk_n == 0) return false;
-    if (nb >= c->Bmax) return false;                         // can_add_new_request (Q17): batch slots
-    u32 k = s.hk[0];
-    u32 nfk = s.nf[k];                                       // cached need of the front: a failing
+    if (hk_n == 0 || nb >= c->Bmax) return false;          // can_add_new_request: batch slots
+    u32 k = s.hk[0].user;
+    UState& us = s.us[k];
+    u32 nfk = us.nf;                                         // cached need of the front: a failing
     if (nfk != NONE32 && (u64)occ_now + nfk > c->C) return false;   // candidate costs no global load
-    bool cont = s.qc_cnt[k] != 0;
-    u32 r = cont ? s.qc_head[k] : s.hf[k];
+    bool cont = us.qc_cnt != 0;
+    u32 r = cont ? us.qc_head : us.hf;
     uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
-    u32 nx = 0, nseq = 0; i64 ct = 0;
-    if (cont) { nx = s.c_next[r]; nseq = s.c_nseq[r]; ct = s.c_t[r]; }
+    u64 inc_pre = c->inc ? c->inc[r] : 0;
+    CSlot cs;
+    if (cont) cs = s.cs[r];
     u64 need = (u64)B.y + B.w;
-    s.nf[k] = (u32)need;
-    if ((u64)occ_now + need > c->C) return false;            // can_add_new_request (Q16, Q17): KV
+    us.nf = (u32)need;
+    if ((u64)occ_now + need > c->C) return false;           // can_add_new_request: KV
+    u32 nseq = 0;
     if (cont) {
-      a->arr = ct;
-      s.qc_head[k] = nx;
-      s.qc_cnt[k]--;
+      a->arr = cs.t;
+      us.qc_head = cs.next; nseq = cs.nseq;
+      us.qc_cnt--;
     } else {
       a->arr = (i64)A.y * 1000000;
-      s.qh_cnt[k]--;
-      if (s.qh_cnt[k]) {                                     // next non-blocked queued head
-        u32 f = s.qh_front[k] + 1;
+      us.qh_cnt--;
+      if (us.qh_cnt) {                                       // next non-blocked queued head
+        u32 f = us.qh_front + 1;
         for (;;) {
           u32 w = s.blocked[f >> 5], id = sh->uh_list[f];
-          if (!((w >> (f & 31)) & 1u)) { s.hf[k] = id; break; }
+          if (!((w >> (f & 31)) & 1u)) { us.hf = id; break; }
           f++;
         }
-        s.qh_front[k] = f;
-      } else s.qh_front[k] = s.qh_next[k];
+        us.qh_front = f;
+      } else us.qh_front = us.qh_next;
     }
-    if (!queued(k)) {                                        // user leaves Q: e <- k
-      h_remove<true>(s.hk, s.hk_pos, hk_n, k);
-      h_remove<false>(s.hm, s.hm_pos, hm_n, k);
-      s.u[k] &= ~CLS_BIT;
+    if (us.qh_cnt + us.qc_cnt == 0) {                        // user leaves Q: e <- k
+      heaps_remove(k, us.hk_pos, us.hm_pos);
+      us.u &= ~CLS_BIT;
       e = k;
-    } else {
-      set_front_key(k, nseq);                                // key increased
-      h_down<true>(s.hk, s.hk_pos, hk_n, 0);
+    } else {                                                 // front changed: key increased
+      if (us.qc_cnt) { us.u &= ~CLS_BIT; us.tie = nseq; } else { us.u |= CLS_BIT; us.tie = us.hf; }
+      us.nf = NONE32;
+      HK x; x.key = us.u; x.tie = us.tie; x.user = k;
+      hk_down(0, x);
     }
     a->r = r;
-    a->need = need;
     a->prompt = B.y;
     a->b.r = r; a->b.user = A.x; a->b.meta = A.z; a->b.link = A.w; a->b.think = B.x;
     a->b.rel = B.y + B.z;
     a->b.fi = iter + B.z - 1;
-    a->b.inc = c->inc ? c->inc[r] : increment(A.x, A.z, B, Cc);
+    a->b.inc = c->inc ? inc_pre : increment(A.x, A.z, B, Cc);
     return true;
   }
 
   // ---------------------------------------------------------------- heads source
-  // next head arrival: (t_ms, call id) only; head_take() copies the whole entry
   __device__ __forceinline__ bool head_peek(u32* tms, u32* rid) {
     if (use_ring) {
       if (rc_cons == rc_prod) {
@@ -365,26 +398,10 @@ struct Engine {
         }
         __threadfence_block();
       }
-      uint2 k = ring.key[rc_cons % HRING];
-      *tms = k.x; *rid = k.y;
+      uint2 kk = ring.key[rc_cons % HRING];
+      *tms = kk.x; *rid = kk.y;
       return true;
     }
-    HEnt h;
-    if (!head_peek_direct(&h)) return false;
-    *tms = h.A.y; *rid = h.r;
-    return true;
-  }
-  __device__ __forceinline__ void head_take(HEnt* h) {
-    if (use_ring) {
-      *h = ring.e[rc_cons % HRING];
-      rc_cons++;
-      *ring.cons = rc_cons;
-      return;
-    }
-    *h = cur;
-    cur_ok = false; hp++;
-  }
-  __device__ __forceinline__ bool head_peek_direct(HEnt* h) {
     if (!cur_ok) {
       while (hp < sh->n_heads) {
         u32 r = sh->heads[hp];
@@ -402,19 +419,28 @@ struct Engine {
       }
       if (!cur_ok) return false;
     }
-    *h = cur;
+    *tms = cur.A.y; *rid = cur.r;
     return true;
+  }
+  __device__ __forceinline__ const HEnt* head_take() {
+    if (use_ring) return &ring.e[rc_cons % HRING];
+    cur_ok = false; hp++;
+    return &cur;
+  }
+  __device__ __forceinline__ void head_done() {          // ring slot may be refilled
+    if (use_ring) { rc_cons++; *ring.cons = rc_cons; }
   }
 
   // ---------------------------------------------------------------- pending heap (t, id)
-  __device__ __forceinline__ bool pless(const PEnt& a, const PEnt& b) const { return a.t < b.t || (a.t == b.t && a.r < b.r); }
+  __device__ __forceinline__ static bool pless(const PEnt& a, const PEnt& b) { return a.t < b.t || (a.t == b.t && a.r < b.r); }
   __device__ bool p_push(const PEnt& x) {
     if (p_n == s.p_cap) { err_code = ERR_NOMEM; err_idx = x.r; return false; }
     u32 i = p_n++;
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
-      if (!pless(x, s.p[pi])) break;
-      s.p[i] = s.p[pi]; i = pi;
+      PEnt pp = s.p[pi];
+      if (!pless(x, pp)) break;
+      s.p[i] = pp; i = pi;
     }
     s.p[i] = x;
     return true;
@@ -427,15 +453,15 @@ struct Engine {
     for (;;) {
       u32 l = 2 * i + 1;
       if (l >= p_n) break;
-      u32 m = l;
-      if (l + 1 < p_n && pless(s.p[l + 1], s.p[l])) m = l + 1;
-      if (!pless(s.p[m], x)) break;
-      s.p[i] = s.p[m]; i = m;
+      PEnt cl = s.p[l];
+      if (l + 1 < p_n) { PEnt cr = s.p[l + 1]; if (pless(cr, cl)) { cl = cr; l++; } }
+      if (!pless(cl, x)) break;
+      s.p[i] = cl; i = l;
     }
     s.p[i] = x;
   }
   // B heap keyed (finish iteration, id)
-  __device__ __forceinline__ bool bless(const BEnt& a, const BEnt& b) const { return a.fi < b.fi || (a.fi == b.fi && a.r < b.r); }
+  __device__ __forceinline__ static bool bless(const BEnt& a, const BEnt& b) { return a.fi < b.fi || (a.fi == b.fi && a.r < b.r); }
   __device__ void b_push(const BEnt& x) {
     u32 i = b_n++;
     while (i > 0) {
@@ -461,20 +487,18 @@ struct Engine {
     s.b[i] = x;
   }
 
-  __device__ __forceinline__ bool overloaded() const {   // Q5
-    return (u64)occ >= c->occ_thr;                        // occ * 1000 >= theta * C, exactly
+  __device__ __forceinline__ bool overloaded() const {     // Q5: occ * 1000 >= theta * C, exactly
+    return (u64)occ >= c->occ_thr;
   }
 
   // ---------------------------------------------------------------- the replay (O4 with event skipping)
   __device__ void run() {
-    HEnt hh;
     for (;;) {
       u32 hms = 0, hid = 0;
       bool hok = head_peek(&hms, &hid);
       i64 th = (i64)hms * 1000000;
       bool pok = p_n != 0;
-      // next pending arrival in (t, id) order
-      bool pend = hok || pok;
+      bool pend = hok || pok;                                     // next pending arrival in (t, id) order
       bool is_head = hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hid < s.p[0].r));
       i64 tn = is_head ? th : (pok ? s.p[0].t : 0);
       if (b_n == 0 && hk_n == 0) {                                // 1: idle engine restarts at the arrival
@@ -485,8 +509,9 @@ struct Engine {
       while (pend && tn <= clock) {
         int st;
         if (is_head) {
-          head_take(&hh);
-          st = deliver_head(hh, th, ovl);
+          const HEnt* h = head_take();
+          st = deliver_head(*h, th, ovl);
+          head_done();
         } else {
           PEnt pe = s.p[0];
           p_pop();
@@ -525,7 +550,7 @@ struct Engine {
         m = s.b[0].fi - iter + 1;                                 //   the next finish ...
         if (pend && d > 0) {                                      //   ... or the next arrival
           u64 gap = (u64)(tn - clock);
-          if (gap <= m * d) m = (gap + d - 1) / d;                // first boundary at or after tn
+          if (gap <= m * d) m = (gap + d - 1) / d;                //   first boundary at or after tn
         }
       }
       iter += m;
@@ -552,12 +577,12 @@ struct Engine {
       }
     }
     // STOP: final digest, counters, summary
-    for (u32 k = 0; k < U; k++) digest = sm64(digest ^ uval(k));
+    for (u32 k = 0; k < U; k++) digest = sm64(digest ^ (s.us[k].u & ~CLS_BIT));
     digest = sm64(digest ^ (u64)clock);
     sum.makespan_ns = clock;
     bool any = false;
     for (u32 k = 0; k < U; k++) {
-      u64 v = uval(k);
+      u64 v = s.us[k].u & ~CLS_BIT;
       if (o.counters) o.counters[k] = v;
       if (sh->utier[k] > c->tier_max) continue;
       if (!any) { sum.u_min = sum.u_max = v; any = true; }
@@ -592,8 +617,7 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
     u32 cnt = __popc(mask);
     if (!cnt) continue;
     u32 ab = 0;
-    // ring full: sleep long (the engine consumes ~1 head per microsecond at best)
-    // wait for half a ring of room, sleeping long: the engine needs microseconds per head
+    // wait for half a ring of room, sleeping long: the engine needs about a microsecond per head
     if (lane == 0 && prod + cnt - *ring.cons > HRING)
       while (prod + HRING / 2 - *ring.cons > HRING && !(ab = *ring.abort)) __nanosleep(20000);
     if (__shfl_sync(FULL_MASK, ab, 0)) return;     // the engine stopped on an error
@@ -615,28 +639,23 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
 // ------------------------------------------------------------------ state layout
 struct EngLayout {
   size_t bytes_smem = 0, bytes_glob = 0;
-  size_t off[32];
-  bool smem[32];
+  size_t off[16];
+  bool smem[16];
 };
-enum { L_U, L_TIE, L_HF, L_NF, L_HK, L_HKP, L_HM, L_HMP, L_B, L_NLID, L_NLARR, L_P, L_W, L_QHF, L_QHN, L_QHC, L_QCH, L_QCT,
-       L_QCC, L_CNEXT, L_CNSEQ, L_CT, L_BLK, L_RT, L_RTAU, L_RAPP, L_RHEAD, L_RLEN, L_HR, L_N };
+enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_CS, L_BLK, L_RT, L_RTAU, L_RAPP, L_N };
 
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
                             bool hring, size_t smem_budget) {
   size_t sz[L_N];
-  sz[L_U] = (size_t)U * 8; sz[L_TIE] = sz[L_HF] = sz[L_NF] = (size_t)U * 4;
-  sz[L_HK] = sz[L_HKP] = sz[L_HM] = sz[L_HMP] = (size_t)U * 4;
-  sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
-  sz[L_P] = (size_t)p_cap * sizeof(PEnt); sz[L_W] = (size_t)AJ * 8;
-  sz[L_QHF] = sz[L_QHN] = sz[L_QHC] = sz[L_QCH] = sz[L_QCT] = sz[L_QCC] = (size_t)U * 4;
-  sz[L_CNEXT] = sz[L_CNSEQ] = (size_t)slots * 4; sz[L_CT] = (size_t)slots * 8;
-  sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
-  size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
-  sz[L_RT] = ring * 8; sz[L_RTAU] = ring * 4; sz[L_RAPP] = ring; sz[L_RHEAD] = sz[L_RLEN] = (size_t)U * 4;
   sz[L_HR] = hring ? (size_t)HRING * (sizeof(HEnt) + 8) + 64 : 0;
+  sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
+  sz[L_W] = (size_t)AJ * 8; sz[L_P] = (size_t)p_cap * sizeof(PEnt);
+  sz[L_US] = (size_t)U * sizeof(UState); sz[L_HK] = (size_t)U * sizeof(HK); sz[L_HM] = (size_t)U * sizeof(HM);
+  sz[L_CS] = (size_t)slots * sizeof(CSlot); sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
+  size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
+  sz[L_RT] = ring * 8; sz[L_RTAU] = ring * 4; sz[L_RAPP] = ring;
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_U, L_TIE, L_HF, L_NF, L_HK, L_HKP, L_QCC, L_QHC,
-                             L_QCH, L_QCT, L_QHF, L_QHN, L_HM, L_HMP, L_RHEAD, L_RLEN};
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM};
   EngLayout L;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
@@ -651,16 +670,11 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
 __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned char* gl, u32 p_cap, EngState* s,
                                 HeadRing* hr) {
   auto P = [&](int k) -> void* { return (L.smem[k] ? sm : gl) + L.off[k]; };
-  s->u = (u64*)P(L_U); s->tie = (u32*)P(L_TIE); s->hf = (u32*)P(L_HF); s->nf = (u32*)P(L_NF);
-  s->hk = (u32*)P(L_HK); s->hk_pos = (u32*)P(L_HKP); s->hm = (u32*)P(L_HM); s->hm_pos = (u32*)P(L_HMP);
+  s->us = (UState*)P(L_US); s->hk = (HK*)P(L_HK); s->hm = (HM*)P(L_HM); s->cs = (CSlot*)P(L_CS);
   s->b = (BEnt*)P(L_B); s->nl_id = (u32*)P(L_NLID); s->nl_arr = (i64*)P(L_NLARR);
   s->p = (PEnt*)P(L_P); s->p_cap = p_cap; s->W = (u64*)P(L_W);
-  s->qh_front = (u32*)P(L_QHF); s->qh_next = (u32*)P(L_QHN); s->qh_cnt = (u32*)P(L_QHC);
-  s->qc_head = (u32*)P(L_QCH); s->qc_tail = (u32*)P(L_QCT); s->qc_cnt = (u32*)P(L_QCC);
-  s->c_next = (u32*)P(L_CNEXT); s->c_nseq = (u32*)P(L_CNSEQ); s->c_t = (i64*)P(L_CT);
   s->blocked = (u32*)P(L_BLK);
   s->r_t = (i64*)P(L_RT); s->r_tau = (u32*)P(L_RTAU); s->r_app = (uint8_t*)P(L_RAPP);
-  s->r_head = (u32*)P(L_RHEAD); s->r_len = (u32*)P(L_RLEN);
   if (hr) {
     unsigned char* base = (unsigned char*)P(L_HR);
     hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
@@ -669,13 +683,15 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
   }
 }
 
-// zero / NONE-initialise a replay's state (whole warp cooperates); W copied in
+// zero / NONE-initialise a replay's state (cooperative); W copied in when it lives elsewhere
 __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u64* W, u64 AJ, u32 U, int lane, int nl) {
   for (u32 k = lane; k < U; k += nl) {
-    s.u[k] = 0; s.tie[k] = 0; s.hf[k] = 0; s.nf[k] = NONE32; s.hk_pos[k] = NONE32; s.hm_pos[k] = NONE32;
+    UState z;
+    memset(&z, 0, sizeof(z));
+    z.nf = NONE32; z.hk_pos = NONE32; z.hm_pos = NONE32; z.qc_head = NONE32; z.qc_tail = NONE32;
     u32 o = (u32)sh.uh_off[k];
-    s.qh_front[k] = o; s.qh_next[k] = o; s.qh_cnt[k] = 0; s.qc_head[k] = NONE32; s.qc_tail[k] = NONE32; s.qc_cnt[k] = 0;
-    s.r_head[k] = 0; s.r_len[k] = 0;
+    z.qh_front = o; z.qh_next = o;
+    s.us[k] = z;
   }
   for (u64 w = lane; w < sh.n_heads / 32 + 2; w += nl) s.blocked[w] = 0;
   if (s.W != W) for (u64 k = lane; k < AJ; k += nl) s.W[k] = W[k];
@@ -801,7 +817,7 @@ __global__ void k_step(StepKArgs a) {
   *a.n_admitted = na;
   a.scal[0] = E.e; a.scal[1] = E.seq; a.scal[2] = E.hk_n; a.scal[3] = E.hm_n;
 }
-__global__ void k_step_read(u32 U, const u64* u, u64* out) {
+__global__ void k_step_read(u32 U, const UState* us, u64* out) {
   u32 k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < U) out[k] = u[k] & ~CLS_BIT;
+  if (k < U) out[k] = us[k].u & ~CLS_BIT;
 }
