@@ -140,11 +140,8 @@ def sweep_scenarios(eng, total):
     return [out[i] for i in sorted(idx)]
 
 
-def algo_bytes_profile(n):
-    # ALGORITHMIC bytes per call of fs_build_app_profiles:
-    # read user, t, meta, L_I, L_S, L_O once (24 B) + per order a permutation write+read (8 B)
-    # and the sorted-order gather of (t, tau) (12 B): 24 + 2 * 20 = 64 B
-    return 64 * n
+# ALGORITHMIC bytes per call of the kernels that touch every call once per launch
+ALGO_BYTES = {"prof_stream": 16, "win_gather": 36, "act_flags": 42, "pack_records": 84}
 
 
 def main():
@@ -288,10 +285,6 @@ def main():
         dist.destroy_process_group()
 
 
-# ALGORITHMIC bytes per call of fs_build_app_profiles:
-    # read user, t, meta, L_I, L_S, L_O once (24 B) + per order a permutation write+read (8 B)
-    # and the sorted-order gather of (t, tau) (12 B): 24 + 2 * 20 = 64 B
-    return 64 * n
 
 
 def ncu_csv(path):
