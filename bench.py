@@ -1,17 +1,17 @@
 """Benchmark of the FairServe trace-scale hot path on B200 (one JSON line on rank 0).
 
-A step = one pass of the whole hot path over one synthetic Copilot-shaped trace:
-  1. fs_build_app_profiles   (benign-only profile, tier_max = 0; Q9)
-  2. fs_wsc_replay            FS(W+I) with profile-derived limits, every user present
-  3. fs_act_throttle          standalone ACT on the replay's arrival times and overload
-                              flags (the throttle evaluation; also the P8 cross-check)
-value = calls in the trace / device time of the step (requests throttled+scheduled/s).
+Default workload (BASELINE.json configs[4], the config the metric's "1/2/4/8 B200" is
+quoted on): C5 -- a step is fs_build_app_profiles (A1-A5) on the 1M-call trace and an
+fs_sweep of 4096 FS(W+I) replays over the grid throttle k x (alpha, beta, gamma) x
+E_abusive x tier_max (A6-A9 inside every replay).  value = calls x scenarios / device
+time of the step (requests throttled+scheduled/s).  One single C2 replay (configs[1])
+is timed after the steps and reported as `single_replay`.
 
-Workloads (BASELINE.json configs): c2 (default; 1k users, 6 apps, 1M calls), c3 (10k
-users, 12 apps, 10M calls), c5 (scenario sweep; scenarios sharded across ranks).
-N > 1: one process per GPU (torchrun); the replay does not shard (DESIGN.md
-"Multi-GPU"), so c2/c3 run one independent replica per rank (weak scaling); c5
-shards its scenarios.  Time = max over ranks of CUDA-event time around the K steps.
+Other workloads: c2 / c3 (profile -> FS(W+I) replay -> ACT on the replay's arrival
+times and overload flags), c4 (100M-call profile sharded by user, NCCL rounds).
+N > 1: one process per GPU (torchrun).  c2/c3/c5 give every rank its own independent
+problem (weak scaling; the replay itself does not shard -- DESIGN.md §8); c4 shards one
+trace by user (strong scaling).  Time = max over ranks of CUDA-event time around the K steps.
 
 --impl reference: the CPU oracle (oracle/, plain single-threaded C++) on this host,
 timed on a bounded sample of the same workload, printed as the reference arm.
@@ -38,7 +38,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c5"])
+    ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--calls", type=int, default=0, help="c4: total calls (default 100M)")
     ap.add_argument("--scenarios", type=int, default=4096, help="c5: scenarios per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timings", action="store_true", help="print per-kernel timings to stderr")
@@ -165,18 +166,33 @@ def main():
     ctx = F.Context(local)
     stream = torch.cuda.current_stream()
     wl = args.workload
-    c, eng, pcfg = workload_cfg("c2" if wl == "c5" else wl)
-    # weak scaling: every rank gets its own independent problem (rank 0 = the BASELINE config)
-    tr = G.generate(wl, seed=G.CONFIGS[wl]["seed"] + rank)
+    c, eng, pcfg = workload_cfg("c2" if wl in ("c5", "c4") else wl)
+    if wl == "c4":
+        # C4: one 100M-call profile sharded by user over the ranks (strong scaling): rank r
+        # holds users [r U/G, (r+1) U/G) with its share of the calls; NCCL SUM all-reduce rounds
+        c4 = G.CONFIGS["c4"]
+        total = args.calls or c4["n_calls"]
+        Ur = c4["n_users"] // world
+        tr = G.generate(dict(c4, n_calls=total // world, n_users=Ur, seed=c4["seed"] + rank))
+        tr["user"] = (tr["user"] + np.uint32(rank * Ur)).astype(np.uint32)
+        tr["n_users"] = Ur * world
+        pcfg = dict(tier_max=0, window_ms=60000, max_stage=64)
+    else:
+        # weak scaling: every rank gets its own independent problem (rank 0 = the BASELINE config)
+        tr = G.generate(wl, seed=G.CONFIGS[wl]["seed"] + rank)
     N = tr["n_calls"]
     T = F.Trace(tr)                                                # inputs resident in HBM before timing
     host = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int32)).pin_memory() for k in F.FIELDS}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")   # > 126 MB L2
     scen = sweep_scenarios(eng, args.scenarios) if wl == "c5" else None
-    outs = F.replay_outputs(ctx, T)
+    outs = F.replay_outputs(ctx, T) if wl != "c4" else None
     status = torch.empty(N, dtype=torch.uint8, device="cuda")
 
     def step(trace):
+        if wl == "c4":                                                  # A1-A5 + A10
+            if world > 1:
+                return F.build_app_profiles_dist(ctx, trace, pcfg)
+            return F.build_app_profiles(ctx, trace, pcfg)
         prof = F.build_app_profiles(ctx, trace, pcfg)                 # A1-A5
         if scen is not None:
             return F.sweep(ctx, trace, prof, scen)                       # A9 (A6-A7 inside every replay)
@@ -217,8 +233,10 @@ def main():
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         T2 = F.Trace.from_host_tensors(tr, host)
-        step(T2)                                          # the sweep returns its summaries in host memory
-        if scen is None:
+        res = step(T2)                                    # the sweep returns its summaries in host memory
+        if wl == "c4":
+            res.read()                                    # D2H of the profile tables
+        elif scen is None:
             d2h.copy_(status, non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
@@ -241,7 +259,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e2e_step_ms = float(t[0]), float(t[1])
     units_per_rank = N * (len(scen) if scen is not None else 1)
-    total_units = units_per_rank * world
+    total_units = units_per_rank * world               # c4: the ranks' shards sum to the one trace
     value = total_units * args.steps / (ms_max / 1e3)
     e2e_value = total_units / (e2e_step_ms / 1e3)
     if args.timings and rank == 0:
@@ -259,17 +277,21 @@ def main():
     line = {
         "metric": "trace requests throttled+scheduled/sec",
         "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong" if wl == "c4" else "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive; profile + FS(W+I) replay + ACT",
                                 "c3": "C3: 10k users, 12 apps, 10M calls; profile + FS(W+I) replay + ACT",
+                                "c4": f"C4: app profile of {N * world} calls sharded by user over {world} GPU(s) "
+                                      f"(NCCL u64 SUM all-reduce rounds)",
                                 "c5": f"C5: profile + sweep of {S} replays (throttle k x (alpha,beta,gamma) x "
                                       f"E_abusive x tier_max) of a 1M-call trace"}[wl],
                    "n_calls": N, "n_users": tr["n_users"], "n_apps": tr["n_apps"], "scenarios_per_gpu": S,
-                   "parallelism": (f"independent problem per GPU x{world}"),
+                   "parallelism": (f"user-hash shards x{world}" if wl == "c4" else
+                                   f"independent problem per GPU x{world}"),
                    "l2": "flushed between timed steps (256 MB write, untimed)"},
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
-                "d2h_bytes_per_step": N if scen is None else 144 * S},
+                "d2h_bytes_per_step": {"c4": 0}.get(wl, N if scen is None else 144 * S)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "stage_ms": {k: v[1] / args.steps for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])[:8]},
@@ -335,7 +357,7 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
             traffic = prof["dram__bytes_read.sum"] + prof.get("dram__bytes_write.sum", 0.0)
         return {"bound": "alu", "kernel": name, "achieved": achieved, "peak": peak, "unit": "Ginst/s",
                 "frac": achieved / peak if achieved else None, "traffic": traffic, "ms_per_launch": per_s * 1e3,
-                "peak_source": src + " (2 issuing warps x 1 inst/cycle x sm_max_mhz)",
+                "peak_source": src + (" (2 issuing warps x 1 inst/cycle x sm_max_mhz)" if name == "wsc_replay" else " (148 SMs x 4 schedulers x 1 warp-inst/cycle x sm_max_mhz)"),
                 "instructions_per_call": inst / ncalls if inst else None,
                 "ns_per_call": per_s / N * 1e9, "hbm_stages": stages}
     b = ALGO_BYTES.get(name, 0) * N
@@ -355,10 +377,15 @@ def cpu_baseline(workload, tr):
     if workload == "c3":
         sample = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
         desc = "C3-shaped 1M-call / 1k-user sample: profile + FS(W+I) replay + ACT"
+    if workload == "c4":
+        sample = G.generate(dict(G.CONFIGS["c4"], n_calls=2_000_000, n_users=2000, seed=4))
+        desc = "C4-shaped 2M-call / 2k-user sample: profile"
     t0 = time.perf_counter()
     p = O.profile(sample, pcfg)
     n = sample["n_calls"]
-    if workload == "c5":
+    if workload == "c4":
+        pass
+    elif workload == "c5":
         scen = sweep_scenarios(eng, 4096)
         picks = [scen[0], scen[len(scen) // 2]]
         O.sweep(sample, p, picks)

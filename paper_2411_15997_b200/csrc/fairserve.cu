@@ -72,6 +72,12 @@ extern "C" int fs_ctx_create(int device, void* stream, fs_ctx** out) {
   c->sm_count = p.multiProcessorCount;
   c->smem_optin = p.sharedMemPerBlockOptin;
   if (cudaMalloc(&c->err, sizeof(DevErr)) != cudaSuccess) { delete c; return FS_E_NOMEM; }
+  // keep stream-ordered scratch in the device pool between calls (no re-mapping per call)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = c;
   return FS_OK;
 }
@@ -145,7 +151,9 @@ static void prof_stream(fs_ctx* ctx, const DTrace& t, u32 J, u32 tier_max, u64* 
   u32 chunks = (A + na - 1) / na;
   size_t smem = sums + (size_t)na * per_app;
   cudaFuncSetAttribute(k_prof_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  ProfStreamArgs a{t, J, tier_max, na, cnt, s_in, s_sys, s_out, hist};
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  u32 vec = al(t.meta) && al(t.len_in) && al(t.len_sys) && al(t.len_out);
+  ProfStreamArgs a{t, J, tier_max, na, vec, cnt, s_in, s_sys, s_out, hist};
   dim3 grid(ctx->sm_count, chunks);
   if (t.n) FS_LAUNCH(ctx, "prof_stream", k_prof_stream, grid, 1024, smem, a);
 }

@@ -94,7 +94,7 @@ static void profile_mirror(fs_profile* P, cudaStream_t s) {   // device -> host 
 // when A*5*240*4 B does not fit next to the sums).  Flush: one global atomic per
 // non-zero shared entry.
 struct ProfStreamArgs {
-  DTrace t; u32 J, tier_max, na_chunk;
+  DTrace t; u32 J, tier_max, na_chunk, vec;
   u64 *cnt, *s_in, *s_sys, *s_out, *hist;
 };
 
@@ -110,34 +110,54 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   for (u32 k = threadIdx.x; k < nh; k += blockDim.x) shist[k] = 0;
   __syncthreads();
   const u64 n = a.t.n;
-  const u64 stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i0 = (u64)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {
-    u64 i = i0 + threadIdx.x;
-    bool ok = i < n;
-    u32 m = ok ? __ldg(&a.t.meta[i]) : 0xFF000000u;
+  const int lane = threadIdx.x & 31;
+  // one call: warp-aggregated sums (match on (app, stage')) and histogram bins (match on
+  // (app, field, bin): popular bins such as L_S = 0 would otherwise serialise the warp)
+  auto one = [&](bool ok, u32 m, u32 Li, u32 Ls, u32 Lo) {
     ok = ok && m_tier(m) <= a.tier_max;
     u32 app = m_app(m), st = m_stage(m);
-    u32 Li = 0, Ls = 0, Lo = 0;
-    if (ok) { Li = __ldg(&a.t.len_in[i]); Ls = __ldg(&a.t.len_sys[i]); Lo = __ldg(&a.t.len_out[i]); }
+    if (!ok) { Li = Ls = Lo = 0; }
     if (do_sums) {
       u32 key = ok ? app * J1 + min(st, a.J) : 0xFFFFFFFFu;
       u32 peers = __match_any_sync(FULL_MASK, key);
       u32 ri = __reduce_add_sync(peers, Li), rs = __reduce_add_sync(peers, Ls), ro = __reduce_add_sync(peers, Lo);
-      if (ok && (threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) {
+      if (ok && lane == (int)(__ffs(peers) - 1)) {
         atomicAdd((unsigned long long*)&ssum[key], (unsigned long long)__popc(peers));
         atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)ri);
         atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)rs);
         atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)ro);
       }
     }
-    if (ok && app >= a0 && app < a0 + na) {
-      u32* h = shist + (app - a0) * NF * NBINS;
-      atomicAdd(&h[0 * NBINS + loglin_bin(Li)], 1u);
-      atomicAdd(&h[1 * NBINS + loglin_bin(Ls)], 1u);
-      atomicAdd(&h[2 * NBINS + loglin_bin(Lo)], 1u);
-      atomicAdd(&h[3 * NBINS + loglin_bin(Li + Ls + Lo)], 1u);
-      if (st == 1) atomicAdd(&h[4 * NBINS + loglin_bin(m_ncalls(m))], 1u);
+    bool in = ok && app >= a0 && app < a0 + na;
+    u32 hb = (app - a0) * NF * NBINS;
+    u32 v[5] = {Li, Ls, Lo, Li + Ls + Lo, m_ncalls(m)};
+#pragma unroll
+    for (int f = 0; f < 5; f++) {
+      bool use = in && (f < 4 || st == 1);
+      u32 idx = use ? hb + f * NBINS + loglin_bin(v[f]) : 0xFFFFFFFFu;
+      u32 peers = __match_any_sync(FULL_MASK, idx);
+      if (use && lane == (int)(__ffs(peers) - 1)) atomicAdd(&shist[idx], (u32)__popc(peers));
     }
+  };
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  const u64 n4 = a.vec ? n / 4 : 0;                    // uint4 loads: 4 calls per thread per array
+  for (u64 q0 = (u64)blockIdx.x * blockDim.x; q0 < n4; q0 += stride) {
+    u64 q = q0 + threadIdx.x;
+    bool ok = q < n4;
+    uint4 M = make_uint4(0, 0, 0, 0), I = M, S4 = M, O = M;
+    if (ok) {
+      M = __ldg((const uint4*)a.t.meta + q); I = __ldg((const uint4*)a.t.len_in + q);
+      S4 = __ldg((const uint4*)a.t.len_sys + q); O = __ldg((const uint4*)a.t.len_out + q);
+    }
+    one(ok, M.x, I.x, S4.x, O.x); one(ok, M.y, I.y, S4.y, O.y);
+    one(ok, M.z, I.z, S4.z, O.z); one(ok, M.w, I.w, S4.w, O.w);
+  }
+  for (u64 i0 = n4 * 4 + (u64)blockIdx.x * blockDim.x; i0 < n; i0 += stride) {   // tail (or unaligned)
+    u64 i = i0 + threadIdx.x;
+    bool ok = i < n;
+    u32 m = ok ? __ldg(&a.t.meta[i]) : 0;
+    u32 Li = ok ? __ldg(&a.t.len_in[i]) : 0, Ls = ok ? __ldg(&a.t.len_sys[i]) : 0, Lo = ok ? __ldg(&a.t.len_out[i]) : 0;
+    one(ok, m, Li, Ls, Lo);
   }
   __syncthreads();
   for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) {
