@@ -382,7 +382,8 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
     if (attempt == 1 && caps[1] <= caps[0]) break;
     if (t.n) FS_LAUNCH(ctx, "replay_pre", k_replay_pre, div_up(t.n, B), B, 0, t, cfg->tier_max, o);
     if (o.admitted_per_app) cudaMemsetAsync(o.admitted_per_app, 0, t.A * 8, ctx->stream);
-    EngLayout L = eng_layout(t.U, t.n, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget);
+    // queued-continuation pool: same two-step capacity (n_inters is an exact bound)
+    EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget);
     unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
     if (S.failed) return FS_E_NOMEM;
     ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
@@ -446,7 +447,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   if (S.failed) return FS_E_NOMEM;
   cudaMemcpyAsync(dc, hc.data(), ns * sizeof(EngCfg), cudaMemcpyHostToDevice, ctx->stream);
   u32 p_cap = std::max<u32>(std::min<u32>(t.X, 1u << 16), 1);
-  EngLayout L = eng_layout(t.U, t.n, W.n_heads, Bmax, p_cap, AJ, any_wi, W.ring_slots, false, 0);
+  EngLayout L = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi,
+                           W.ring_slots, false, 0);
   size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -492,7 +494,7 @@ __global__ void k_step_init(EngLayout L, unsigned char* gm, u32 p_cap, EngShared
   eng_bind(L, nullptr, gm, p_cap, &st, nullptr);
   st.W = (u64*)W;
   eng_clear(st, sh, W, 0, U, threadIdx.x, blockDim.x);
-  if (threadIdx.x == 0) { scal[0] = -1; scal[1] = 0; scal[2] = 0; scal[3] = 0; }
+  if (threadIdx.x == 0) { scal[0] = -1; scal[1] = 0; scal[2] = 0; scal[3] = 0; scal[4] = L.c_cap; }
 }
 
 extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
@@ -537,7 +539,7 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
   st->L = eng_layout(st->U, std::max<u64>(st->t.n, 1), st->W.n_heads, cfg->max_batch, st->p_cap, AJ,
                      cfg->mode == FS_MODE_WI, ring_slots, false, 0);
   st->gm = S.alloc<unsigned char>(st->L.bytes_glob + 256);
-  st->scal = S.alloc<i64>(4);
+  st->scal = S.alloc<i64>(8);
   if (S.failed) { delete st; return FS_E_NOMEM; }
   FS_LAUNCH(ctx, "step_init", k_step_init, 1, 256, 0, st->L, st->gm, st->p_cap, st->W.sh, st->ec.W, st->U, st->scal);
   rc = finish(ctx, &S);

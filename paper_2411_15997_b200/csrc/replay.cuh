@@ -60,20 +60,20 @@ struct alignas(16) UState {             // per user, 64 B
   u32 tie, hf, nf;                      // tie of the front; front head id; KV need of the front (NONE = ?)
   u32 hk_pos, hm_pos;                   // heap positions (NONE = not queued)
   u32 qh_front, qh_next, qh_cnt;        // head FIFO: absolute uh_list positions, queued count
-  u32 qc_head, qc_tail, qc_cnt;         // continuation FIFO (call ids)
+  u32 qc_head, qc_tail, qc_cnt;         // continuation FIFO (pool slots)
   u32 r_head, r_len;                    // ACT continuation ring
   u32 pad;
 };
 struct HK { u64 key; u32 tie, user; };  // pick heap entry: (class | u, tie)
 struct HM { u64 u; u32 user, pad; };    // lift heap entry: u
-struct CSlot { u32 next, nseq; i64 t; };   // queued continuation: next in FIFO, its seq, own arrival
+struct CSlot { u32 r, next, nseq, pad; i64 t; };   // queued continuation: call, next slot, next's seq, arrival
 struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
 struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
 
 struct EngState {
   UState* us; HK* hk; HM* hm;
-  CSlot* cs;                            // [slots] per call
+  CSlot* cs; u32* cfree; u32 c_cap;     // pool of queued-continuation slots + free stack
   u32* blocked;                         // [n_heads/32 + 2] bitset over uh positions
   BEnt* b; u32* nl_id; i64* nl_arr;     // B heap [Bmax]; calls admitted this round [Bmax]
   PEnt* p; u32 p_cap;                   // pending continuation heap
@@ -101,7 +101,7 @@ struct Engine {
   EngState s;
   EngOut o;
   u32 U;
-  u32 hk_n, hm_n, b_n, p_n, nl_n;
+  u32 hk_n, hm_n, b_n, p_n, nl_n, c_top;  // c_top: free slots on the pool's stack
   i64 clock, occ;
   u64 iter;
   i64 e;                                 // last user to exit Q (Alg. 1 l.14), -1 = NONE
@@ -169,6 +169,7 @@ struct Engine {
   __device__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
     sh = shr; c = cfg; s = st; o = out; U = nusers;
     hk_n = hm_n = b_n = p_n = nl_n = 0;
+    c_top = st.c_cap;                                      // eng_clear fills cfree[i] = i
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
     use_ring = false; static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
     memset(&sum, 0, sizeof(sum));
@@ -314,10 +315,12 @@ struct Engine {
       if (!ring_push(us, k, tr, B.y + B.w, m_app(m), r)) return -1;
     }
     digest = sm64(digest ^ ((u64)r * 16));
-    CSlot cs; cs.next = NONE32; cs.nseq = 0; cs.t = tr;
-    s.cs[r] = cs;
-    if (us.qc_cnt == 0) us.qc_head = r; else { s.cs[us.qc_tail].next = r; s.cs[us.qc_tail].nseq = seq; }
-    us.qc_tail = r;
+    if (c_top == 0) { err_code = ERR_NOMEM; err_idx = r; return -1; }   // pool capacity (R5)
+    u32 x = s.cfree[--c_top];
+    CSlot cs; cs.r = r; cs.next = NONE32; cs.nseq = 0; cs.pad = 0; cs.t = tr;
+    s.cs[x] = cs;
+    if (us.qc_cnt == 0) us.qc_head = x; else { s.cs[us.qc_tail].next = x; s.cs[us.qc_tail].nseq = seq; }
+    us.qc_tail = x;
     us.qc_cnt++;
     u32 myseq = seq++;
     if (!was) {                                             // newly queued: class 0
@@ -341,11 +344,12 @@ struct Engine {
     u32 nfk = us.nf;                                         // cached need of the front: a failing
     if (nfk != NONE32 && (u64)occ_now + nfk > c->C) return false;   // candidate costs no global load
     bool cont = us.qc_cnt != 0;
-    u32 r = cont ? us.qc_head : us.hf;
+    u32 x = cont ? us.qc_head : 0;
+    CSlot cs;
+    if (cont) cs = s.cs[x];
+    u32 r = cont ? cs.r : us.hf;
     uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
     u64 inc_pre = c->inc ? c->inc[r] : 0;
-    CSlot cs;
-    if (cont) cs = s.cs[r];
     u64 need = (u64)B.y + B.w;
     us.nf = (u32)need;
     if ((u64)occ_now + need > c->C) return false;           // can_add_new_request: KV
@@ -354,6 +358,7 @@ struct Engine {
       a->arr = cs.t;
       us.qc_head = cs.next; nseq = cs.nseq;
       us.qc_cnt--;
+      s.cfree[c_top++] = x;                                  // slot back to the pool
     } else {
       a->arr = (i64)A.y * 1000000;
       us.qh_cnt--;
@@ -641,9 +646,11 @@ struct EngLayout {
   size_t bytes_smem = 0, bytes_glob = 0;
   size_t off[16];
   bool smem[16];
+  u32 c_cap = 0;                        // continuation-slot pool capacity
 };
-enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_CS, L_BLK, L_RT, L_RTAU, L_RAPP, L_N };
+enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_CS, L_CF, L_BLK, L_RT, L_RTAU, L_RAPP, L_N };
 
+// slots: capacity of the pool of queued-continuation slots (R5)
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
                             bool hring, size_t smem_budget) {
   size_t sz[L_N];
@@ -651,12 +658,14 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
   sz[L_W] = (size_t)AJ * 8; sz[L_P] = (size_t)p_cap * sizeof(PEnt);
   sz[L_US] = (size_t)U * sizeof(UState); sz[L_HK] = (size_t)U * sizeof(HK); sz[L_HM] = (size_t)U * sizeof(HM);
-  sz[L_CS] = (size_t)slots * sizeof(CSlot); sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
+  sz[L_CS] = (size_t)slots * sizeof(CSlot); sz[L_CF] = (size_t)slots * 4;
+  sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
   size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
   sz[L_RT] = ring * 8; sz[L_RTAU] = ring * 4; sz[L_RAPP] = ring;
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM};
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_CS, L_CF};
   EngLayout L;
+  L.c_cap = (u32)slots;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
     size_t b = (sz[k] + 15) / 16 * 16;
@@ -671,6 +680,7 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
                                 HeadRing* hr) {
   auto P = [&](int k) -> void* { return (L.smem[k] ? sm : gl) + L.off[k]; };
   s->us = (UState*)P(L_US); s->hk = (HK*)P(L_HK); s->hm = (HM*)P(L_HM); s->cs = (CSlot*)P(L_CS);
+  s->cfree = (u32*)P(L_CF); s->c_cap = L.c_cap;
   s->b = (BEnt*)P(L_B); s->nl_id = (u32*)P(L_NLID); s->nl_arr = (i64*)P(L_NLARR);
   s->p = (PEnt*)P(L_P); s->p_cap = p_cap; s->W = (u64*)P(L_W);
   s->blocked = (u32*)P(L_BLK);
@@ -694,6 +704,7 @@ __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u
     s.us[k] = z;
   }
   for (u64 w = lane; w < sh.n_heads / 32 + 2; w += nl) s.blocked[w] = 0;
+  for (u32 k = lane; k < s.c_cap; k += nl) s.cfree[k] = s.c_cap - 1 - k;   // pops hand out 0, 1, 2, ...
   if (s.W != W) for (u64 k = lane; k < AJ; k += nl) s.W[k] = W[k];
 }
 
@@ -783,6 +794,7 @@ __global__ void k_step(StepKArgs a) {
   Engine E;
   E.init(&a.sh, &a.cfg, st, none, a.U);
   E.e = a.scal[0]; E.seq = (u32)a.scal[1]; E.hk_n = (u32)a.scal[2]; E.hm_n = (u32)a.scal[3];
+  E.c_top = (u32)a.scal[4];
   E.static_heads = false;                                         // caller-given arrival times
   E.occ = a.occ;
   *a.err_code = 0;
@@ -815,7 +827,7 @@ __global__ void k_step(StepKArgs a) {
     nb++;
   }
   *a.n_admitted = na;
-  a.scal[0] = E.e; a.scal[1] = E.seq; a.scal[2] = E.hk_n; a.scal[3] = E.hm_n;
+  a.scal[0] = E.e; a.scal[1] = E.seq; a.scal[2] = E.hk_n; a.scal[3] = E.hm_n; a.scal[4] = E.c_top;
 }
 __global__ void k_step_read(u32 U, const UState* us, u64* out) {
   u32 k = blockIdx.x * blockDim.x + threadIdx.x;
