@@ -440,6 +440,33 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   u64 AJ = (u64)t.A * (P->J + 1);
   std::vector<EngCfg> hc(ns);
   for (u32 s = 0; s < ns; s++) hc[s] = eng_cfg(&scen[s], T, s, t.A, AJ, hl[s]);
+  // Eq. 3 increments depend on (alpha, beta, gamma, E_benign, E_abusive) only: precompute them
+  // once per distinct combination, off the serial path (bounded to 2 GiB of tables)
+  {
+    std::vector<std::vector<u32>> combos;
+    std::vector<u32> combo_of(ns);
+    for (u32 s = 0; s < ns; s++) {
+      std::vector<u32> key = {scen[s].alpha, scen[s].beta, scen[s].gamma, scen[s].prio_benign_q16,
+                              scen[s].prio_abusive_q16};
+      u32 k = 0;
+      while (k < combos.size() && combos[k] != key) k++;
+      if (k == combos.size()) combos.push_back(key);
+      combo_of[s] = k;
+    }
+    if ((u64)combos.size() * (t.n + 1) * 8 <= (2ull << 30)) {
+      std::vector<u64*> tabs(combos.size());
+      for (size_t k = 0; k < combos.size(); k++) tabs[k] = S.alloc<u64>(t.n + 1);
+      if (S.failed) return FS_E_NOMEM;
+      std::vector<char> done(combos.size(), 0);
+      for (u32 s = 0; s < ns; s++) {
+        u32 k = combo_of[s];
+        if (!done[k] && t.n)
+          FS_LAUNCH(ctx, "pack_inc", k_pack_inc, div_up(t.n, 256), 256, 0, t.n, W.recA, W.recB, W.recC, hc[s], tabs[k]);
+        done[k] = 1;
+        hc[s].inc = tabs[k];
+      }
+    }
+  }
   EngCfg* dc = S.alloc<EngCfg>(ns);
   fs_replay_summary* dsum = S.zeros<fs_replay_summary>(ns);
   int* dcodes = S.zeros<int>(ns);

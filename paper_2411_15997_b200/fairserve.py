@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfairserve.so")
+LIB_PATH = os.environ.get("FS_LIB") or os.path.join(_HERE, "lib", "libfairserve.so")   # FS_LIB: A/B experiments
 
 STATUS = {0: "FS_OK", -1: "FS_E_INVAL", -2: "FS_E_RANGE", -3: "FS_E_ORDER", -4: "FS_E_OVERSIZE",
           -5: "FS_E_PROFILE", -6: "FS_E_OVERFLOW", -7: "FS_E_NOMEM", -8: "FS_E_CUDA", -9: "FS_E_PROTOCOL"}
