@@ -1,0 +1,114 @@
+"""GPU edge cases vs the oracle: empty and single-call traces, everything filtered,
+and every error code (same code, same first offending index)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2411_15997_b200 import tracegen as G
+
+pytestmark = pytest.mark.gpu
+MS = 10**6
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_2411_15997_b200 import build, fairserve
+    build.build()
+    return fairserve
+
+
+@pytest.fixture(scope="module")
+def ctx(F):
+    return F.Context(0)
+
+
+def _row(**k):
+    r = dict(user=0, t_ms=0, app=0, inter=0, stage=1, ncalls=1, len_in=10, len_out=3)
+    r.update(k)
+    return r
+
+
+ENG = dict(mode=1, kv_capacity=10**6, max_batch=4, overload_permille=0, iter_base_ns=MS, decode_ns_per_req=0,
+           prefill_ns_per_tok=0, act=dict(window_ms=10, limits_from_profile=0, T_req_g=1, T_req_a=[1, 1]))
+
+
+def _both(F, ctx, tr, op_host, cfg):
+    """Run the replay on both sides; returns (oracle result or error, gpu result or error)."""
+    A, J = op_host[0], op_host[1]
+    op = O.profile_from_host(*op_host)
+    gp = F.profile_from_host(ctx, *op_host)
+    try:
+        e = O.replay(tr, op, cfg)
+    except O.OracleError as x:
+        e = ("err", x.code, x.bad_index)
+    try:
+        g = F.wsc_replay(ctx, F.Trace(tr), gp, cfg)
+    except F.FsError as x:
+        g = ("err", x.code, x.bad_index)
+    return e, g
+
+
+PROF1 = (2, 1, [[0, 1], [0, 1]], [[0, 10], [0, 10]], [[0, 0], [0, 0]], [[0, 3], [0, 3]])
+
+
+def test_empty_trace(F, ctx):
+    tr = G.from_columns(3, 2, [])
+    tr["n_inters"] = 0
+    e, g = _both(F, ctx, tr, PROF1, ENG)
+    assert g[1]["n_arrived"] == 0 and g[1]["digest"] == e[1]["digest"]
+    p = F.build_app_profiles(ctx, F.Trace(tr), {}).read()
+    assert p["cnt"].sum() == 0 and int(p["T_req_g"][0]) == 0
+    st, s = F.act_throttle(ctx, F.Trace(tr), None, dict(limits_from_profile=0))
+    assert s["n_in"] == 0
+
+
+def test_single_call(F, ctx):
+    tr = G.from_columns(1, 2, [_row()])
+    e, g = _both(F, ctx, tr, PROF1, ENG)
+    assert g[1] == e[1]
+    assert int(g[0]["finish_ns"][0]) == int(e[0]["finish_ns"][0]) == 3 * MS
+
+
+def test_all_filtered(F, ctx):
+    rows = [_row(user=0, tier=3, inter=0), _row(user=1, tier=2, t_ms=1, inter=1)]
+    tr = G.from_columns(2, 2, rows)
+    cfg = dict(ENG, tier_max=1)
+    e, g = _both(F, ctx, tr, PROF1, cfg)
+    assert g[1] == e[1] and g[1]["n_filtered"] == 2 and g[1]["n_arrived"] == 0
+    assert list(g[0]["status"].cpu().numpy()) == [6, 6]
+
+
+@pytest.mark.parametrize("case", ["range_user", "range_lenout", "order_time", "order_chain", "order_dup",
+                                  "profile", "oversize", "overflow"])
+def test_error_codes(F, ctx, case):
+    rows = [_row(inter=0, ncalls=2), _row(inter=0, stage=2, ncalls=2, t_ms=1), _row(user=1, inter=1, t_ms=2)]
+    prof = PROF1
+    cfg = dict(ENG)
+    if case == "range_user":
+        rows[2]["user"] = 7
+    elif case == "range_lenout":
+        rows[1]["len_out"] = 0
+    elif case == "order_time":
+        rows[2]["t_ms"] = 0
+    elif case == "order_chain":
+        rows[1]["stage"] = 3
+        rows[1]["ncalls"] = 3
+    elif case == "order_dup":
+        rows.append(_row(inter=0, stage=2, ncalls=2, t_ms=3))
+    elif case == "profile":
+        prof = (2, 1, [[0, 1], [0, 0]], [[0, 10], [0, 0]], [[0, 0], [0, 0]], [[0, 3], [0, 0]])
+        rows[2]["app"] = 1
+    elif case == "oversize":
+        cfg["kv_capacity"] = 12
+    elif case == "overflow":
+        prof = (2, 1, [[0, 65536], [0, 65536]], [[0, 1], [0, 1]], [[0, 0], [0, 0]], [[0, 0], [0, 0]])
+        cfg.update(prio_benign_q16=(1 << 24) - 1, alpha=255, beta=255, gamma=255)
+        for r in rows:
+            r["len_in"] = (1 << 24) - 1
+        cfg["kv_capacity"] = 1 << 26
+    tr = G.from_columns(2, 2, rows)
+    e, g = _both(F, ctx, tr, prof, cfg)
+    assert e[0] == "err" and g[0] == "err", (e, g)
+    assert g[1:] == e[1:], (case, e, g)
