@@ -375,7 +375,7 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   u64* didx = S.zeros<u64>(1);
   if (S.failed) return FS_E_NOMEM;
   // pending-continuation heap: first a shared-memory capacity, on overflow again with every interaction
-  u32 caps[2] = {std::max<u32>(1, std::min<u32>(t.X, 4096)), std::max<u32>(t.X, 1)};
+  u32 caps[2] = {std::max<u32>(1, std::min<u32>(t.X, 2048)), std::max<u32>(t.X, 1)};
   int hcode = 0; u64 hidx = 0;
   for (int attempt = 0; attempt < 2; attempt++) {
     u32 p_cap = caps[attempt];

@@ -482,7 +482,7 @@ static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, 
 
 extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_act_cfg* cfg,
                                const uint8_t* overloaded, const int64_t* tov, uint8_t* status, fs_act_summary* sum) {
-  if (!ctx || !tr || !status || !sum || !act_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
+  if (!ctx || !tr || (!status && tr->n_calls) || !sum || !act_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
   memset(sum, 0, sizeof(*sum));
   if (P && P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
   Scratch S(ctx);

@@ -62,11 +62,11 @@ struct alignas(16) UState {             // per user, 64 B
   u32 qh_front, qh_next, qh_cnt;        // head FIFO: absolute uh_list positions, queued count
   u32 qc_head, qc_tail, qc_cnt;         // continuation FIFO (pool slots)
   u32 r_head, r_len;                    // ACT continuation ring
-  u32 pad;
+  u32 cf;                               // call id of the continuation FIFO's front
 };
 struct HK { u64 key; u32 tie, user; };  // pick heap entry: (class | u, tie)
 struct HM { u64 u; u32 user, pad; };    // lift heap entry: u
-struct CSlot { u32 r, next, nseq, pad; i64 t; };   // queued continuation: call, next slot, next's seq, arrival
+struct CSlot { u32 r, next, nseq, nr; i64 t; };    // queued continuation: call, next slot, next's seq / call, arrival
 struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
 struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
@@ -317,9 +317,10 @@ struct Engine {
     digest = sm64(digest ^ ((u64)r * 16));
     if (c_top == 0) { err_code = ERR_NOMEM; err_idx = r; return -1; }   // pool capacity (R5)
     u32 x = s.cfree[--c_top];
-    CSlot cs; cs.r = r; cs.next = NONE32; cs.nseq = 0; cs.pad = 0; cs.t = tr;
+    CSlot cs; cs.r = r; cs.next = NONE32; cs.nseq = 0; cs.nr = NONE32; cs.t = tr;
     s.cs[x] = cs;
-    if (us.qc_cnt == 0) us.qc_head = x; else { s.cs[us.qc_tail].next = x; s.cs[us.qc_tail].nseq = seq; }
+    if (us.qc_cnt == 0) { us.qc_head = x; us.cf = r; }
+    else { CSlot& tl = s.cs[us.qc_tail]; tl.next = x; tl.nseq = seq; tl.nr = r; }
     us.qc_tail = x;
     us.qc_cnt++;
     u32 myseq = seq++;
@@ -347,7 +348,7 @@ struct Engine {
     u32 x = cont ? us.qc_head : 0;
     CSlot cs;
     if (cont) cs = s.cs[x];
-    u32 r = cont ? cs.r : us.hf;
+    u32 r = cont ? us.cf : us.hf;                            // no dependent load on the slot
     uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
     u64 inc_pre = c->inc ? c->inc[r] : 0;
     u64 need = (u64)B.y + B.w;
@@ -356,7 +357,7 @@ struct Engine {
     u32 nseq = 0;
     if (cont) {
       a->arr = cs.t;
-      us.qc_head = cs.next; nseq = cs.nseq;
+      us.qc_head = cs.next; nseq = cs.nseq; us.cf = cs.nr;
       us.qc_cnt--;
       s.cfree[c_top++] = x;                                  // slot back to the pool
     } else {
