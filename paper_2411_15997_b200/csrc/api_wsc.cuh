@@ -479,14 +479,19 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  u64 slots = std::min<u64>(ns, (u64)ctx->sm_count * 16);
+  // one warp per resident slot: FS_SWEEP_MINB picks the register cap (CTAs per SM)
+  static const int minb = [] { const char* v = getenv("FS_SWEEP_MINB"); return v ? atoi(v) : 1; }();
+  auto kern = minb >= 4 ? k_sweep<4> : minb == 3 ? k_sweep<3> : k_sweep<1>;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
+  u64 slots = std::min<u64>(ns, (u64)ctx->sm_count * std::max(1, per_sm) * 4);
   u64 by_mem = (u64)(free_b / 2) / std::max<size_t>(slot_bytes, 1);
   slots = std::max<u64>(1, std::min(slots, by_mem));
   slots = (slots + 3) / 4 * 4;                      // 4 warps per CTA
   unsigned char* gm = S.alloc<unsigned char>(slots * slot_bytes + 256);
   if (S.failed) return FS_E_NOMEM;
   SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next};
-  FS_LAUNCH(ctx, "wsc_sweep", k_sweep, (u32)(slots / 4), 128, 0, a);
+  FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / 4), 128, 0, a);
   std::vector<int> hcodes(ns);
   cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);
   cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);

@@ -95,7 +95,8 @@ struct HeadRing {                       // producer warp -> engine thread (share
 
 __device__ __forceinline__ uint4 ldg4(const uint4* p) { return __ldg(p); }
 
-struct Engine {
+template <bool RING>                    // RING: heads come from the producer warp's ring
+struct EngineT {
   const EngShared* sh;
   const EngCfg* c;
   EngState s;
@@ -107,7 +108,7 @@ struct Engine {
   i64 e;                                 // last user to exit Q (Alg. 1 l.14), -1 = NONE
   u32 seq;
   u64 hp;                                // next head (trace order) when reading heads directly
-  bool use_ring, static_heads;
+  bool static_heads;
   HeadRing ring;
   u32 rc_cons, rc_prod;                  // ring consumer index, last producer index seen
   HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
@@ -118,7 +119,7 @@ struct Engine {
   // ---------------------------------------------------------------- heaps with inline keys
   __device__ __forceinline__ static bool kl(const HK& a, const HK& b) { return a.key < b.key || (a.key == b.key && a.tie < b.tie); }
   __device__ __forceinline__ static bool ml(const HM& a, const HM& b) { return a.u < b.u || (a.u == b.u && a.user < b.user); }
-  __device__ void hk_up(u32 i, HK x) {
+  __device__ __forceinline__ void hk_up(u32 i, HK x) {
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
       HK p = s.hk[pi];
@@ -127,7 +128,7 @@ struct Engine {
     }
     s.hk[i] = x; s.us[x.user].hk_pos = i;
   }
-  __device__ void hk_down(u32 i, HK x) {
+  __device__ __forceinline__ void hk_down(u32 i, HK x) {
     for (;;) {
       u32 l = 2 * i + 1;
       if (l >= hk_n) break;
@@ -138,7 +139,7 @@ struct Engine {
     }
     s.hk[i] = x; s.us[x.user].hk_pos = i;
   }
-  __device__ void hm_up(u32 i, HM x) {
+  __device__ __forceinline__ void hm_up(u32 i, HM x) {
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
       HM p = s.hm[pi];
@@ -147,7 +148,7 @@ struct Engine {
     }
     s.hm[i] = x; s.us[x.user].hm_pos = i;
   }
-  __device__ void hm_down(u32 i, HM x) {
+  __device__ __forceinline__ void hm_down(u32 i, HM x) {
     for (;;) {
       u32 l = 2 * i + 1;
       if (l >= hm_n) break;
@@ -158,7 +159,7 @@ struct Engine {
     }
     s.hm[i] = x; s.us[x.user].hm_pos = i;
   }
-  __device__ void heaps_remove(u32 k, u32 pk, u32 pm) {   // user k leaves Q
+  __device__ __forceinline__ void heaps_remove(u32 k, u32 pk, u32 pm) {   // user k leaves Q
     hk_n--;
     if (pk != hk_n) { HK last = s.hk[hk_n]; if (pk > 0 && kl(last, s.hk[(pk - 1) >> 1])) hk_up(pk, last); else hk_down(pk, last); }
     hm_n--;
@@ -166,12 +167,12 @@ struct Engine {
     s.us[k].hk_pos = NONE32; s.us[k].hm_pos = NONE32;
   }
 
-  __device__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
+  __device__ __forceinline__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
     sh = shr; c = cfg; s = st; o = out; U = nusers;
     hk_n = hm_n = b_n = p_n = nl_n = 0;
     c_top = st.c_cap;                                      // eng_clear fills cfree[i] = i
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
-    use_ring = false; static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
+    static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
@@ -200,7 +201,7 @@ struct Engine {
     while (num - p >= W) { q++; p += W; }
     return q >= (1ull << 63) ? ~0ull : q;
   }
-  __device__ bool charge(u32 k, u64 inc, u32 r) {
+  __device__ __forceinline__ bool charge(u32 k, u64 inc, u32 r) {
     UState& us = s.us[k];
     u64 cur = us.u & ~CLS_BIT;
     if (inc == ~0ull || cur + inc >= (1ull << 63)) { err_code = ERR_OVERFLOW; err_idx = r; return false; }
@@ -215,13 +216,13 @@ struct Engine {
     }
     return true;
   }
-  __device__ bool charge_call(u32 r) {                    // online step: records from global
+  __device__ __forceinline__ bool charge_call(u32 r) {                    // online step: records from global
     uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
     return charge(A.x, increment(A.x, A.z, B, Cc), r);
   }
 
   // ---------------------------------------------------------------- ACT window check (l.19-24)
-  __device__ int act_check(UState& us, u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
+  __device__ __forceinline__ int act_check(UState& us, u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
     if (!c->heads_only || !static_heads) {
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
       u32 h = us.r_head, len = us.r_len;
@@ -241,7 +242,7 @@ struct Engine {
     if (c->ta[app] && t_a > c->ta[app]) return FS_ST_BLOCK_APP_TOK;
     return FS_ST_ADMIT;
   }
-  __device__ bool ring_push(UState& us, u32 k, i64 tr, u32 tau, u32 app, u32 r) {
+  __device__ __forceinline__ bool ring_push(UState& us, u32 k, i64 tr, u32 tau, u32 app, u32 r) {
     u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
     u32 h = us.r_head, len = us.r_len;
     while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }
@@ -275,7 +276,7 @@ struct Engine {
 
   // ---------------------------------------------------------------- deliveries (l.11-25)
   // returns the arrival status (FS_ST_ADMIT or a BLOCK code), -1 on error
-  __device__ int deliver_head(const HEnt& h, i64 tr, bool ovl) {
+  __device__ __forceinline__ int deliver_head(const HEnt& h, i64 tr, bool ovl) {
     u32 r = h.r, k = h.A.x, m = h.A.z;
     u32 upos = h.C.y;
     UState& us = s.us[k];
@@ -292,7 +293,10 @@ struct Engine {
     if (st != FS_ST_ADMIT) {
       s.blocked[upos >> 5] |= 1u << (upos & 31);
       if (us.qh_cnt == 0) us.qh_front = upos + 1;
-      sum.n_block[st - 1]++;
+      switch (st) {                                        // constant indices keep sum in registers
+        case 1: sum.n_block[0]++; break; case 2: sum.n_block[1]++; break;
+        case 3: sum.n_block[2]++; break; default: sum.n_block[3]++; break;
+      }
       sum.n_dropped += m_ncalls(m) - 1;
       if (o.status) o.status[r] = (uint8_t)st;
       return st;
@@ -306,7 +310,7 @@ struct Engine {
     }
     return FS_ST_ADMIT;
   }
-  __device__ int deliver_cont(u32 r, u32 k, u32 m, i64 tr, bool ovl) {
+  __device__ __forceinline__ int deliver_cont(u32 r, u32 k, u32 m, i64 tr, bool ovl) {
     UState& us = s.us[k];
     arrived(r, tr, ovl);
     bool was = lift(us);
@@ -338,7 +342,7 @@ struct Engine {
   // ---------------------------------------------------------------- one pick (l.28-39)
   struct Adm { u32 r; u64 prompt; BEnt b; i64 arr; };
   // Returns false if Q is empty or the candidate does not fit (Q16, Q17).
-  __device__ bool pick(i64 occ_now, u32 nb, Adm* a) {
+  __device__ __forceinline__ bool pick(i64 occ_now, u32 nb, Adm* a) {
     if (hk_n == 0 || nb >= c->Bmax) return false;          // can_add_new_request: batch slots
     u32 k = s.hk[0].user;
     UState& us = s.us[k];
@@ -394,7 +398,7 @@ struct Engine {
 
   // ---------------------------------------------------------------- heads source
   __device__ __forceinline__ bool head_peek(u32* tms, u32* rid) {
-    if (use_ring) {
+    if (RING) {
       if (rc_cons == rc_prod) {
         for (;;) {
           rc_prod = *ring.prod;
@@ -428,18 +432,18 @@ struct Engine {
     *tms = cur.A.y; *rid = cur.r;
     return true;
   }
-  __device__ __forceinline__ const HEnt* head_take() {
-    if (use_ring) return &ring.e[rc_cons % HRING];
+  __device__ __forceinline__ void head_take(HEnt* h) {   // by value: the engine stays in registers
+    if (RING) { *h = ring.e[rc_cons % HRING]; return; }
     cur_ok = false; hp++;
-    return &cur;
+    *h = cur;
   }
   __device__ __forceinline__ void head_done() {          // ring slot may be refilled
-    if (use_ring) { rc_cons++; *ring.cons = rc_cons; }
+    if (RING) { rc_cons++; *ring.cons = rc_cons; }
   }
 
   // ---------------------------------------------------------------- pending heap (t, id)
   __device__ __forceinline__ static bool pless(const PEnt& a, const PEnt& b) { return a.t < b.t || (a.t == b.t && a.r < b.r); }
-  __device__ bool p_push(const PEnt& x) {
+  __device__ __forceinline__ bool p_push(const PEnt& x) {
     if (p_n == s.p_cap) { err_code = ERR_NOMEM; err_idx = x.r; return false; }
     u32 i = p_n++;
     while (i > 0) {
@@ -451,7 +455,7 @@ struct Engine {
     s.p[i] = x;
     return true;
   }
-  __device__ void p_pop() {
+  __device__ __forceinline__ void p_pop() {
     p_n--;
     if (!p_n) return;
     PEnt x = s.p[p_n];
@@ -468,7 +472,7 @@ struct Engine {
   }
   // B heap keyed (finish iteration, id)
   __device__ __forceinline__ static bool bless(const BEnt& a, const BEnt& b) { return a.fi < b.fi || (a.fi == b.fi && a.r < b.r); }
-  __device__ void b_push(const BEnt& x) {
+  __device__ __forceinline__ void b_push(const BEnt& x) {
     u32 i = b_n++;
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
@@ -477,7 +481,7 @@ struct Engine {
     }
     s.b[i] = x;
   }
-  __device__ void b_pop() {
+  __device__ __forceinline__ void b_pop() {
     b_n--;
     if (!b_n) return;
     BEnt x = s.b[b_n];
@@ -498,7 +502,7 @@ struct Engine {
   }
 
   // ---------------------------------------------------------------- the replay (O4 with event skipping)
-  __device__ void run() {
+  __device__ __forceinline__ void run() {
     for (;;) {
       u32 hms = 0, hid = 0;
       bool hok = head_peek(&hms, &hid);
@@ -515,8 +519,9 @@ struct Engine {
       while (pend && tn <= clock) {
         int st;
         if (is_head) {
-          const HEnt* h = head_take();
-          st = deliver_head(*h, th, ovl);
+          HEnt h;
+          head_take(&h);
+          st = deliver_head(h, th, ovl);
           head_done();
         } else {
           PEnt pe = s.p[0];
@@ -731,9 +736,8 @@ __global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
     return;
   }
   if (threadIdx.x != 0) return;
-  Engine E;
+  EngineT<true> E;
   E.init(&a.sh, &a.cfg, st, a.out, a.U);
-  E.use_ring = true;
   E.ring = hr;
   E.run();
   *a.sum = E.sum;
@@ -747,7 +751,8 @@ struct SweepKArgs {
   EngShared sh; const EngCfg* cfgs; u32 n_scen; EngLayout L; u32 U; unsigned char* gmem; size_t slot_bytes;
   u32 p_cap; fs_replay_summary* sums; int* codes; u32* next;
 };
-__global__ void __launch_bounds__(128) k_sweep(SweepKArgs a) {
+template <int MINB>                       // MINB CTAs per SM: caps registers (occupancy vs spills)
+__global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
   int lane = threadIdx.x & 31;
   u32 slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   unsigned char* g = a.gmem + (size_t)slot * a.slot_bytes;
@@ -767,7 +772,7 @@ __global__ void __launch_bounds__(128) k_sweep(SweepKArgs a) {
     __syncwarp();
     __threadfence_block();
     if (lane == 0) {
-      Engine E;
+      EngineT<false> E;
       E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
       E.run();
       a.sums[sc] = E.sum;
@@ -792,7 +797,7 @@ __global__ void k_step(StepKArgs a) {
   st.W = (u64*)a.cfg.W;
   EngOut none;
   memset(&none, 0, sizeof(none));
-  Engine E;
+  EngineT<false> E;
   E.init(&a.sh, &a.cfg, st, none, a.U);
   E.e = a.scal[0]; E.seq = (u32)a.scal[1]; E.hk_n = (u32)a.scal[2]; E.hm_n = (u32)a.scal[3];
   E.c_top = (u32)a.scal[4];
@@ -821,7 +826,7 @@ __global__ void k_step(StepKArgs a) {
   }
   u32 na = 0;                                                      // l.28-39
   i64 occ = a.occ; u32 nb = a.batch;
-  Engine::Adm ad;
+  EngineT<false>::Adm ad;
   while (E.pick(occ, nb, &ad)) {
     a.admitted[na++] = ad.r;
     occ += (i64)ad.prompt;

@@ -1,5 +1,5 @@
 """Time one fs_sweep of S scenarios over the C5 trace (C2-shaped, 1M calls).
-Usage: python tools/prof_sweep.py [S] [n_calls]"""
+Usage: python tools/prof_sweep.py [S] [n_calls] [n_users]"""
 import os
 import sys
 import time
@@ -16,11 +16,14 @@ from paper_2411_15997_b200 import tracegen as G  # noqa: E402
 
 S = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+nu = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 B.build()
 cfg = dict(G.CONFIGS["c5"])
 if n:
     cfg["n_users"] = max(50, int(cfg["n_users"] * n / cfg["n_calls"]))
     cfg["n_calls"] = n
+if nu:
+    cfg["n_users"] = nu
 tr = G.generate(cfg)
 ctx = F.Context(0)
 T = F.Trace(tr)
