@@ -58,7 +58,7 @@ struct EngCfg {                         // one scenario
 struct alignas(16) UState {             // per user, 64 B
   u64 u;                                // counter, Q32.32; bit 63 = class of the queue front (1 = head)
   u32 tie, hf, nf;                      // tie of the front; front head id; KV need of the front (NONE = ?)
-  u32 hk_pos, hm_pos;                   // heap positions (NONE = not queued)
+  u32 pad0, pad1;
   u32 qh_front, qh_next, qh_cnt;        // head FIFO: absolute uh_list positions, queued count
   u32 qc_head, qc_tail, qc_cnt;         // continuation FIFO (pool slots)
   u32 r_head, r_len;                    // ACT continuation ring
@@ -69,6 +69,7 @@ struct HM { u64 u; u32 user, pad; };    // lift heap entry: u
 struct CSlot { u32 r, next, nseq, nr; i64 t; };    // queued continuation: call, next slot, next's seq / call, arrival
 struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
 struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
+struct REnt { i64 t; u32 tau, app; };   // ACT ring entry: arrival, token load, app (16 B)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
 
 struct EngState {
@@ -77,7 +78,9 @@ struct EngState {
   u32* blocked;                         // [n_heads/32 + 2] bitset over uh positions
   BEnt* b; u32* nl_id; i64* nl_arr;     // B heap [Bmax]; calls admitted this round [Bmax]
   PEnt* p; u32 p_cap;                   // pending continuation heap
-  i64* r_t; u32* r_tau; uint8_t* r_app; // ACT rings [ring slots] (CSR by user)
+  uint2* hpos;                          // [U] heap positions (hk, hm; NONE = not queued): dense, apart
+                                        // from the 64-B user records a sift would otherwise touch
+  REnt* r;                              // ACT rings [ring slots] (CSR by user), one 16-B entry each
   u64* W;                               // stage weights (smem copy or the scenario's table)
 };
 
@@ -95,8 +98,15 @@ struct HeadRing {                       // producer warp -> engine thread (share
 
 __device__ __forceinline__ uint4 ldg4(const uint4* p) { return __ldg(p); }
 
-template <bool RING>                    // RING: heads come from the producer warp's ring
+enum { HS_DIRECT = 0,                   // heads read one at a time (online step: single thread)
+       HS_RING = 1,                     // heads from the producer warp's shared-memory ring (single replay)
+       HS_WARP = 2 };                   // all 32 lanes run the engine in lockstep and refill a per-warp
+                                        // batch of the next 32 participating heads together (sweep)
+struct HeadBatch { HEnt e[32]; };       // per-warp shared-memory head batch (HS_WARP)
+
+template <int HS>
 struct EngineT {
+  static constexpr bool RING = HS == HS_RING;
   const EngShared* sh;
   const EngCfg* c;
   EngState s;
@@ -112,6 +122,8 @@ struct EngineT {
   HeadRing ring;
   u32 rc_cons, rc_prod;                  // ring consumer index, last producer index seen
   HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
+  HeadBatch* hb; u32 hb_i, hb_n;         // HS_WARP: batch, next entry, entries
+  u32 hb_t, hb_r;                        // HS_WARP: (t_ms, id) of the next entry
   u64 digest, n_adm;
   fs_replay_summary sum;
   int err_code; u64 err_idx;
@@ -124,9 +136,9 @@ struct EngineT {
       u32 pi = (i - 1) >> 1;
       HK p = s.hk[pi];
       if (!kl(x, p)) break;
-      s.hk[i] = p; s.us[p.user].hk_pos = i; i = pi;
+      s.hk[i] = p; s.hpos[p.user].x = i; i = pi;
     }
-    s.hk[i] = x; s.us[x.user].hk_pos = i;
+    s.hk[i] = x; s.hpos[x.user].x = i;
   }
   __device__ __forceinline__ void hk_down(u32 i, HK x) {
     for (;;) {
@@ -135,18 +147,18 @@ struct EngineT {
       HK cl = s.hk[l];
       if (l + 1 < hk_n) { HK cr = s.hk[l + 1]; if (kl(cr, cl)) { cl = cr; l++; } }
       if (!kl(cl, x)) break;
-      s.hk[i] = cl; s.us[cl.user].hk_pos = i; i = l;
+      s.hk[i] = cl; s.hpos[cl.user].x = i; i = l;
     }
-    s.hk[i] = x; s.us[x.user].hk_pos = i;
+    s.hk[i] = x; s.hpos[x.user].x = i;
   }
   __device__ __forceinline__ void hm_up(u32 i, HM x) {
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
       HM p = s.hm[pi];
       if (!ml(x, p)) break;
-      s.hm[i] = p; s.us[p.user].hm_pos = i; i = pi;
+      s.hm[i] = p; s.hpos[p.user].y = i; i = pi;
     }
-    s.hm[i] = x; s.us[x.user].hm_pos = i;
+    s.hm[i] = x; s.hpos[x.user].y = i;
   }
   __device__ __forceinline__ void hm_down(u32 i, HM x) {
     for (;;) {
@@ -155,16 +167,16 @@ struct EngineT {
       HM cl = s.hm[l];
       if (l + 1 < hm_n) { HM cr = s.hm[l + 1]; if (ml(cr, cl)) { cl = cr; l++; } }
       if (!ml(cl, x)) break;
-      s.hm[i] = cl; s.us[cl.user].hm_pos = i; i = l;
+      s.hm[i] = cl; s.hpos[cl.user].y = i; i = l;
     }
-    s.hm[i] = x; s.us[x.user].hm_pos = i;
+    s.hm[i] = x; s.hpos[x.user].y = i;
   }
   __device__ __forceinline__ void heaps_remove(u32 k, u32 pk, u32 pm) {   // user k leaves Q
     hk_n--;
     if (pk != hk_n) { HK last = s.hk[hk_n]; if (pk > 0 && kl(last, s.hk[(pk - 1) >> 1])) hk_up(pk, last); else hk_down(pk, last); }
     hm_n--;
     if (pm != hm_n) { HM last = s.hm[hm_n]; if (pm > 0 && ml(last, s.hm[(pm - 1) >> 1])) hm_up(pm, last); else hm_down(pm, last); }
-    s.us[k].hk_pos = NONE32; s.us[k].hm_pos = NONE32;
+    s.hpos[k] = make_uint2(NONE32, NONE32);
   }
 
   __device__ __forceinline__ void init(const EngShared* shr, const EngCfg* cfg, const EngState& st, const EngOut& out, u32 nusers) {
@@ -173,6 +185,7 @@ struct EngineT {
     c_top = st.c_cap;                                      // eng_clear fills cfree[i] = i
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
     static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
+    hb_i = hb_n = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
@@ -207,12 +220,12 @@ struct EngineT {
     if (inc == ~0ull || cur + inc >= (1ull << 63)) { err_code = ERR_OVERFLOW; err_idx = r; return false; }
     u64 nu = us.u + inc;                                 // class bit untouched (no carry: u < 2^63)
     us.u = nu;
-    u32 pk = us.hk_pos;
-    if (pk != NONE32) {                                  // queued: both keys increased
+    if (us.qh_cnt + us.qc_cnt != 0) {                    // queued: both keys increased
+      uint2 ps = s.hpos[k];
       HK x; x.key = nu; x.tie = us.tie; x.user = k;
-      hk_down(pk, x);
+      hk_down(ps.x, x);
       HM y; y.u = nu & ~CLS_BIT; y.user = k; y.pad = 0;
-      hm_down(us.hm_pos, y);
+      hm_down(ps.y, y);
     }
     return true;
   }
@@ -226,13 +239,13 @@ struct EngineT {
     if (!c->heads_only || !static_heads) {
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
       u32 h = us.r_head, len = us.r_len;
-      while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // (Q4)
+      while (len && s.r[base + h].t <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // (Q4)
       us.r_head = h; us.r_len = len;
       for (u32 q = 0; q < len; q++) {
         u32 idx = h + q; if (idx >= cap) idx -= cap;
-        u64 tau = s.r_tau[base + idx];
-        n_g++; t_g += tau;
-        if (s.r_app[base + idx] == app) { n_a++; t_a += tau; }
+        REnt re = s.r[base + idx];
+        n_g++; t_g += re.tau;
+        if (re.app == app) { n_a++; t_a += re.tau; }
       }
     }
     const DLimits& L = c->L;
@@ -245,10 +258,11 @@ struct EngineT {
   __device__ __forceinline__ bool ring_push(UState& us, u32 k, i64 tr, u32 tau, u32 app, u32 r) {
     u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
     u32 h = us.r_head, len = us.r_len;
-    while (len && s.r_t[base + h] <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }
+    while (len && s.r[base + h].t <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }
     if (len == cap) { err_code = ERR_NOMEM; err_idx = r; return false; }
     u32 idx = h + len; if (idx >= cap) idx -= cap;
-    s.r_t[base + idx] = tr; s.r_tau[base + idx] = tau; s.r_app[base + idx] = (uint8_t)app;
+    REnt re; re.t = tr; re.tau = tau; re.app = app;
+    s.r[base + idx] = re;
     us.r_head = h; us.r_len = len + 1;
     return true;
   }
@@ -334,7 +348,7 @@ struct EngineT {
     } else if (us.qc_cnt == 1) {                            // class 1 -> 0: key decreased
       us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
       HK x; x.key = us.u; x.tie = myseq; x.user = k;
-      hk_up(us.hk_pos, x);
+      hk_up(s.hpos[k].x, x);
     }
     return FS_ST_ADMIT;
   }
@@ -378,7 +392,8 @@ struct EngineT {
       } else us.qh_front = us.qh_next;
     }
     if (us.qh_cnt + us.qc_cnt == 0) {                        // user leaves Q: e <- k
-      heaps_remove(k, us.hk_pos, us.hm_pos);
+      uint2 ps = s.hpos[k];
+      heaps_remove(k, ps.x, ps.y);
       us.u &= ~CLS_BIT;
       e = k;
     } else {                                                 // front changed: key increased
@@ -397,7 +412,42 @@ struct EngineT {
   }
 
   // ---------------------------------------------------------------- heads source
+  // HS_WARP: the 32 lanes load the next 32 heads in parallel, keep the participating ones
+  // (tier <= tier_max) in trace order, and prefetch their users' state lines into L1
+  __device__ __forceinline__ bool head_refill() {
+    const u32 lane = threadIdx.x & 31;
+    const bool win = c->mode == FS_MODE_WI && static_heads;
+    while (hp < sh->n_heads) {
+      u64 j = hp + lane;
+      bool ok = j < sh->n_heads;
+      HEnt h;
+      if (ok) {
+        h.r = __ldg(&sh->heads[j]);
+        h.A = ldg4(&sh->recA[h.r]);
+        ok = m_tier(h.A.z) <= c->tier_max;
+      }
+      if (ok) {
+        h.B = ldg4(&sh->recB[h.r]); h.C = ldg4(&sh->recC[h.r]);
+        if (win) {
+          u32 up = h.C.y;
+          h.ng = __ldg(&sh->hw_ng[up]); h.na = __ldg(&sh->hw_na[up]); h.tg = __ldg(&sh->hw_tg[up]); h.ta = __ldg(&sh->hw_ta[up]);
+        } else { h.ng = h.na = 0; h.tg = h.ta = 0; }
+        asm volatile("prefetch.global.L1 [%0];" :: "l"(&s.us[h.A.x]));
+      }
+      u32 mask = __ballot_sync(FULL_MASK, ok);
+      hp += 32;
+      if (ok) hb->e[__popc(mask & lanemask_lt())] = h;
+      __syncwarp();
+      if (mask) { hb_n = __popc(mask); hb_i = 0; hb_t = hb->e[0].A.y; hb_r = hb->e[0].r; return true; }
+    }
+    return false;
+  }
   __device__ __forceinline__ bool head_peek(u32* tms, u32* rid) {
+    if (HS == HS_WARP) {
+      if (hb_i == hb_n && !head_refill()) return false;
+      *tms = hb_t; *rid = hb_r;
+      return true;
+    }
     if (RING) {
       if (rc_cons == rc_prod) {
         for (;;) {
@@ -433,6 +483,11 @@ struct EngineT {
     return true;
   }
   __device__ __forceinline__ void head_take(HEnt* h) {   // by value: the engine stays in registers
+    if (HS == HS_WARP) {
+      *h = hb->e[hb_i];
+      if (++hb_i < hb_n) { hb_t = hb->e[hb_i].A.y; hb_r = hb->e[hb_i].r; }
+      return;
+    }
     if (RING) { *h = ring.e[rc_cons % HRING]; return; }
     cur_ok = false; hp++;
     *h = cur;
@@ -497,6 +552,19 @@ struct EngineT {
     s.b[i] = x;
   }
 
+  // ceil(a / b) for b > 0 when the quotient is known to be <= qmax < 2^31: a float
+  // reciprocal estimate corrected in integers (exact), instead of a 64-bit division
+  __device__ __forceinline__ static u64 ceil_div_small(u64 a, u64 b, u64 qmax) {
+    if (qmax >= (1ull << 31) || a >= (1ull << 62)) return (a + b - 1) / b;
+    float rb = __frcp_rn((float)b);
+    i64 q = (i64)((float)a * rb);
+    i64 r = (i64)a - q * (i64)b;
+    q += (i64)((float)r * rb);
+    r = (i64)a - q * (i64)b;
+    while (r < 0) { q--; r += (i64)b; }
+    while (r >= (i64)b) { q++; r -= (i64)b; }
+    return (u64)q + (r != 0);
+  }
   __device__ __forceinline__ bool overloaded() const {     // Q5: occ * 1000 >= theta * C, exactly
     return (u64)occ >= c->occ_thr;
   }
@@ -504,6 +572,7 @@ struct EngineT {
   // ---------------------------------------------------------------- the replay (O4 with event skipping)
   __device__ __forceinline__ void run() {
     for (;;) {
+      if (HS == HS_WARP) __syncwarp();                            // lanes stay in lockstep
       u32 hms = 0, hid = 0;
       bool hok = head_peek(&hms, &hid);
       i64 th = (i64)hms * 1000000;
@@ -537,13 +606,15 @@ struct EngineT {
         tn = is_head ? th : (pok ? s.p[0].t : 0);
       }
       u64 P_new = 0;                                              // 3: admission round
+      u64 arr_sum = 0;                                            // sum of the admitted calls' arrivals
       nl_n = 0;
       Adm ad;
       while (pick(occ, b_n, &ad)) {
         u32 r = ad.r;
         b_push(ad.b);
         occ += (i64)ad.prompt; P_new += ad.prompt;
-        s.nl_id[nl_n] = r; s.nl_arr[nl_n] = ad.arr; nl_n++;
+        if (o.first) s.nl_id[nl_n] = r;
+        arr_sum += (u64)ad.arr; nl_n++;
         sum.n_admitted++;
         u64 wt = (u64)(clock - ad.arr);
         sum.sum_wait_ns += wt;
@@ -561,18 +632,15 @@ struct EngineT {
         m = s.b[0].fi - iter + 1;                                 //   the next finish ...
         if (pend && d > 0) {                                      //   ... or the next arrival
           u64 gap = (u64)(tn - clock);
-          if (gap <= m * d) m = (gap + d - 1) / d;                //   first boundary at or after tn
+          if (gap <= m * d) m = ceil_div_small(gap, d, m);         //   first boundary at or after tn
         }
       }
       iter += m;
       sum.n_iterations += m;
       clock += (i64)(m * d);
       occ += (i64)(m * b_n);
-      for (u32 q = 0; q < nl_n; q++) {
-        u32 r = s.nl_id[q];
-        if (o.first) o.first[r] = clock;
-        sum.sum_ttft_ns += (u64)(clock - s.nl_arr[q]);
-      }
+      sum.sum_ttft_ns += (u64)nl_n * (u64)clock - arr_sum;       // sum of (first token - arrival), mod 2^64
+      if (o.first) for (u32 q = 0; q < nl_n; q++) o.first[s.nl_id[q]] = clock;
       while (b_n && s.b[0].fi == iter - 1) {                      // finishes (l.43-48)
         BEnt f = s.b[0];
         b_pop();
@@ -654,7 +722,7 @@ struct EngLayout {
   bool smem[16];
   u32 c_cap = 0;                        // continuation-slot pool capacity
 };
-enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_CS, L_CF, L_BLK, L_RT, L_RTAU, L_RAPP, L_N };
+enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_HPOS, L_CS, L_CF, L_BLK, L_RT, L_N };
 
 // slots: capacity of the pool of queued-continuation slots (R5)
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
@@ -667,9 +735,10 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   sz[L_CS] = (size_t)slots * sizeof(CSlot); sz[L_CF] = (size_t)slots * 4;
   sz[L_BLK] = (size_t)(n_heads / 32 + 2) * 4;
   size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
-  sz[L_RT] = ring * 8; sz[L_RTAU] = ring * 4; sz[L_RAPP] = ring;
+  sz[L_RT] = ring * sizeof(REnt);
+  sz[L_HPOS] = (size_t)U * sizeof(uint2);
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_CS, L_CF};
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_US, L_HK, L_HM, L_CS, L_CF};
   EngLayout L;
   L.c_cap = (u32)slots;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
@@ -690,7 +759,7 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
   s->b = (BEnt*)P(L_B); s->nl_id = (u32*)P(L_NLID); s->nl_arr = (i64*)P(L_NLARR);
   s->p = (PEnt*)P(L_P); s->p_cap = p_cap; s->W = (u64*)P(L_W);
   s->blocked = (u32*)P(L_BLK);
-  s->r_t = (i64*)P(L_RT); s->r_tau = (u32*)P(L_RTAU); s->r_app = (uint8_t*)P(L_RAPP);
+  s->r = (REnt*)P(L_RT); s->hpos = (uint2*)P(L_HPOS);
   if (hr) {
     unsigned char* base = (unsigned char*)P(L_HR);
     hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
@@ -704,7 +773,8 @@ __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u
   for (u32 k = lane; k < U; k += nl) {
     UState z;
     memset(&z, 0, sizeof(z));
-    z.nf = NONE32; z.hk_pos = NONE32; z.hm_pos = NONE32; z.qc_head = NONE32; z.qc_tail = NONE32;
+    z.nf = NONE32; z.qc_head = NONE32; z.qc_tail = NONE32;
+    s.hpos[k] = make_uint2(NONE32, NONE32);
     u32 o = (u32)sh.uh_off[k];
     z.qh_front = o; z.qh_next = o;
     s.us[k] = z;
@@ -736,7 +806,7 @@ __global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
     return;
   }
   if (threadIdx.x != 0) return;
-  EngineT<true> E;
+  EngineT<HS_RING> E;
   E.init(&a.sh, &a.cfg, st, a.out, a.U);
   E.ring = hr;
   E.run();
@@ -751,8 +821,11 @@ struct SweepKArgs {
   EngShared sh; const EngCfg* cfgs; u32 n_scen; EngLayout L; u32 U; unsigned char* gmem; size_t slot_bytes;
   u32 p_cap; fs_replay_summary* sums; int* codes; u32* next;
 };
+// Every lane of the warp runs the (warp-uniform) engine: loads and stores of the
+// replicated state are broadcast / merged, and the head batch refills use all 32 lanes.
 template <int MINB>                       // MINB CTAs per SM: caps registers (occupancy vs spills)
 __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
+  __shared__ HeadBatch hbs[4];
   int lane = threadIdx.x & 31;
   u32 slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   unsigned char* g = a.gmem + (size_t)slot * a.slot_bytes;
@@ -771,12 +844,15 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
     eng_clear(st, a.sh, a.cfgs[sc].W, AJ, a.U, lane, 32);
     __syncwarp();
     __threadfence_block();
-    if (lane == 0) {
-      EngineT<false> E;
+    {
+      EngineT<HS_WARP> E;
       E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
+      E.hb = &hbs[threadIdx.x >> 5];
       E.run();
-      a.sums[sc] = E.sum;
-      a.codes[sc] = E.err_code ? E.err_code + 1 : 0;
+      if (lane == 0) {
+        a.sums[sc] = E.sum;
+        a.codes[sc] = E.err_code ? E.err_code + 1 : 0;
+      }
     }
     __syncwarp();
   }
@@ -797,7 +873,7 @@ __global__ void k_step(StepKArgs a) {
   st.W = (u64*)a.cfg.W;
   EngOut none;
   memset(&none, 0, sizeof(none));
-  EngineT<false> E;
+  EngineT<HS_DIRECT> E;
   E.init(&a.sh, &a.cfg, st, none, a.U);
   E.e = a.scal[0]; E.seq = (u32)a.scal[1]; E.hk_n = (u32)a.scal[2]; E.hm_n = (u32)a.scal[3];
   E.c_top = (u32)a.scal[4];
@@ -826,7 +902,7 @@ __global__ void k_step(StepKArgs a) {
   }
   u32 na = 0;                                                      // l.28-39
   i64 occ = a.occ; u32 nb = a.batch;
-  EngineT<false>::Adm ad;
+  EngineT<HS_DIRECT>::Adm ad;
   while (E.pick(occ, nb, &ad)) {
     a.admitted[na++] = ad.r;
     occ += (i64)ad.prompt;

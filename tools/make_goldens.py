@@ -67,4 +67,27 @@ def run(name):
 
 if __name__ == "__main__":
     for nm in sys.argv[1:] or ["c2"]:
-        run(nm)
+        run_c5() if nm == "c5" else run(nm)
+
+
+def run_c5(n_sample=12):
+    """C5: oracle summaries of a seeded sample of the bench's 4096-scenario grid (bench.sweep_scenarios,
+    the same list bench.py times), for the full-size sweep parity test."""
+    import bench
+    c = G.CONFIGS["c5"]
+    tr = G.generate("c5")
+    cfg, eng, pcfg = bench.workload_cfg("c2")
+    p = O.profile(tr, pcfg)
+    scen = bench.sweep_scenarios(eng, 4096)
+    idx = sorted(int(i) for i in np.random.default_rng(55).choice(len(scen), n_sample, replace=False))
+    t0 = time.time()
+    sums, codes = O.sweep(tr, p, [scen[i] for i in idx])
+    out = {"citation": "written by tools/make_goldens.py from oracle/ only (SURVEY.md §8(c) O4, A9); "
+                       "inputs: tracegen config c5 and bench.sweep_scenarios(4096)",
+           "config": "c5", "n_calls": tr["n_calls"], "seed": c["seed"], "profile_cfg": pcfg,
+           "index": idx, "codes": [int(x) for x in codes], "summaries": sums,
+           "oracle_seconds": time.time() - t0}
+    path = os.path.join(ROOT, "tests", "golden", "full_c5_sample.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("c5 sample written", path, out["oracle_seconds"], flush=True)
