@@ -88,8 +88,7 @@ static void profile_mirror(fs_profile* P, cudaStream_t s) {   // device -> host 
 }
 
 // ------------------------------------------------------------------ K3 + K4 streaming pass
-// Persistent grid-stride CTAs.  Sums: warp-aggregated by (app, stage') with
-// __match_any_sync + __reduce_add_sync, then one shared u64 atomic per group.
+// Persistent grid-stride CTAs.  Sums: shared u64 atomics per (app, stage').
 // Histograms: shared u32 bins for apps [a0, a0+na) (blockIdx.y chunks the apps
 // when A*5*240*4 B does not fit next to the sums).  Flush: one global atomic per
 // non-zero shared entry.
@@ -111,33 +110,25 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   __syncthreads();
   const u64 n = a.t.n;
   const int lane = threadIdx.x & 31;
-  // one call: warp-aggregated sums (match on (app, stage')) and histogram bins (match on
-  // (app, field, bin): popular bins such as L_S = 0 would otherwise serialise the warp)
+  // one call: shared-memory atomics straight into the CTA's private sums and bins (integer adds
+  // commute, so the result is order-independent); same-address lanes are merged by the hardware
   auto one = [&](bool ok, u32 m, u32 Li, u32 Ls, u32 Lo) {
-    ok = ok && m_tier(m) <= a.tier_max;
+    if (!ok || m_tier(m) > a.tier_max) return;
     u32 app = m_app(m), st = m_stage(m);
-    if (!ok) { Li = Ls = Lo = 0; }
     if (do_sums) {
-      u32 key = ok ? app * J1 + min(st, a.J) : 0xFFFFFFFFu;
-      u32 peers = __match_any_sync(FULL_MASK, key);
-      u32 ri = __reduce_add_sync(peers, Li), rs = __reduce_add_sync(peers, Ls), ro = __reduce_add_sync(peers, Lo);
-      if (ok && lane == (int)(__ffs(peers) - 1)) {
-        atomicAdd((unsigned long long*)&ssum[key], (unsigned long long)__popc(peers));
-        atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)ri);
-        atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)rs);
-        atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)ro);
-      }
+      u32 key = app * J1 + min(st, a.J);
+      atomicAdd((unsigned long long*)&ssum[key], 1ull);
+      atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)Li);
+      atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)Ls);
+      atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)Lo);
     }
-    bool in = ok && app >= a0 && app < a0 + na;
-    u32 hb = (app - a0) * NF * NBINS;
-    u32 v[5] = {Li, Ls, Lo, Li + Ls + Lo, m_ncalls(m)};
-#pragma unroll
-    for (int f = 0; f < 5; f++) {
-      bool use = in && (f < 4 || st == 1);
-      u32 idx = use ? hb + f * NBINS + loglin_bin(v[f]) : 0xFFFFFFFFu;
-      u32 peers = __match_any_sync(FULL_MASK, idx);
-      if (use && lane == (int)(__ffs(peers) - 1)) atomicAdd(&shist[idx], (u32)__popc(peers));
-    }
+    if (app < a0 || app >= a0 + na) return;
+    u32* hb = shist + (app - a0) * NF * NBINS;
+    atomicAdd(&hb[loglin_bin(Li)], 1u);
+    atomicAdd(&hb[NBINS + loglin_bin(Ls)], 1u);
+    atomicAdd(&hb[2 * NBINS + loglin_bin(Lo)], 1u);
+    atomicAdd(&hb[3 * NBINS + loglin_bin(Li + Ls + Lo)], 1u);
+    if (st == 1) atomicAdd(&hb[4 * NBINS + loglin_bin(m_ncalls(m))], 1u);
   };
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 n4 = a.vec ? n / 4 : 0;                    // uint4 loads: 4 calls per thread per array

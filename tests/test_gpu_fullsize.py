@@ -54,3 +54,39 @@ def test_full_size(name):
         assert sa[k] == v, k
     _, sw = F.wsc_replay(ctx, T, prof, dict(g["engine"], mode=0), outputs=False)
     assert sw["digest"] == g["replay_w"]["digest"]
+
+
+def test_sweep_c5_full():
+    """fs_sweep of the bench's whole 4096-scenario C5 grid (the launch bench.py times): the
+    sampled scenarios equal the oracle's summaries (tests/golden/full_c5_sample.json); every
+    scenario satisfies the engine's conservation properties."""
+    path = os.path.join(GOLD, "full_c5_sample.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = json.load(open(path))
+    import bench
+    from paper_2411_15997_b200 import build, fairserve as F
+    build.build()
+    ctx = F.Context(0)
+    tr = G.generate("c5")
+    assert tr["n_calls"] == g["n_calls"]
+    T = F.Trace(tr)
+    _, eng, pcfg = bench.workload_cfg("c2")
+    assert pcfg == g["profile_cfg"]
+    prof = F.build_app_profiles(ctx, T, pcfg)
+    scen = bench.sweep_scenarios(eng, 4096)
+    sums, codes = F.sweep(ctx, T, prof, scen)
+    for j, i in enumerate(g["index"]):
+        assert int(codes[i]) == g["codes"][j], i
+        assert sums[i] == g["summaries"][j], (i, sums[i], g["summaries"][j])
+    tiers = tr["meta"] >> 24
+    heads = ((tr["meta"] >> 8) & 255) == 1
+    for s, c, sc in zip(sums, codes, scen):
+        assert c == 0
+        part = tiers <= sc["tier_max"]
+        assert s["n_filtered"] == int((~part).sum())
+        assert s["n_admitted"] == s["n_finished"]
+        assert s["n_arrived"] == s["n_admitted"] + sum(s["n_block"])
+        assert s["n_arrived"] + s["n_dropped"] + s["n_filtered"] == tr["n_calls"]
+        assert sum(s["n_block"]) <= int((heads & part).sum())
+        assert s["u_min"] <= s["u_max"]

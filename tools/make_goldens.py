@@ -65,9 +65,6 @@ def run(name):
     print(name, "written", path, out["oracle_seconds"], flush=True)
 
 
-if __name__ == "__main__":
-    for nm in sys.argv[1:] or ["c2"]:
-        run_c5() if nm == "c5" else run(nm)
 
 
 def run_c5(n_sample=12):
@@ -91,3 +88,8 @@ def run_c5(n_sample=12):
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print("c5 sample written", path, out["oracle_seconds"], flush=True)
+
+
+if __name__ == "__main__":
+    for nm in sys.argv[1:] or ["c2"]:
+        run_c5() if nm == "c5" else run(nm)
