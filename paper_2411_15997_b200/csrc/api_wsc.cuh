@@ -480,7 +480,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   // one warp per resident slot: FS_SWEEP_MINB picks the register cap (CTAs per SM)
-  static const int minb = [] { const char* v = getenv("FS_SWEEP_MINB"); return v ? atoi(v) : 3; }();
+  static const int minb = [] { const char* v = getenv("FS_SWEEP_MINB"); return v ? atoi(v) : 4; }();
   auto kern = minb >= 8 ? k_sweep<8> : minb == 7 ? k_sweep<7> : minb == 6 ? k_sweep<6> : minb == 5 ? k_sweep<5> :
               minb == 4 ? k_sweep<4> : minb == 3 ? k_sweep<3> : k_sweep<1>;
   int per_sm = 0;

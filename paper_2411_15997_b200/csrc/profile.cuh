@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   for (u32 k = threadIdx.x; k < nh; k += blockDim.x) shist[k] = 0;
   __syncthreads();
   const u64 n = a.t.n;
-  const int lane = threadIdx.x & 31;
   // one call: shared-memory atomics straight into the CTA's private sums and bins (integer adds
   // commute, so the result is order-independent); same-address lanes are merged by the hardware
   auto one = [&](bool ok, u32 m, u32 Li, u32 Ls, u32 Lo) {

@@ -221,6 +221,7 @@ struct EngineT {
     u64 nu = us.u + inc;                                 // class bit untouched (no carry: u < 2^63)
     us.u = nu;
     if (us.qh_cnt + us.qc_cnt != 0) {                    // queued: both keys increased
+      pick_blocked = false;
       uint2 ps = s.hpos[k];
       HK x; x.key = nu; x.tie = us.tie; x.user = k;
       hk_down(ps.x, x);
@@ -282,6 +283,7 @@ struct EngineT {
     if (o.arrive) { o.arrive[r] = tr; o.ovl[r] = ovl; }
   }
   __device__ __forceinline__ void newly_queued(UState& us, u32 k) {
+    pick_blocked = false;
     HK x; x.key = us.u; x.tie = us.tie; x.user = k;
     hk_up(hk_n++, x);
     HM y; y.u = us.u & ~CLS_BIT; y.user = k; y.pad = 0;
@@ -346,6 +348,7 @@ struct EngineT {
       us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
       newly_queued(us, k);
     } else if (us.qc_cnt == 1) {                            // class 1 -> 0: key decreased
+      pick_blocked = false;
       us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
       HK x; x.key = us.u; x.tie = myseq; x.user = k;
       hk_up(s.hpos[k].x, x);
@@ -356,12 +359,12 @@ struct EngineT {
   // ---------------------------------------------------------------- one pick (l.28-39)
   struct Adm { u32 r; u64 prompt; BEnt b; i64 arr; };
   // Returns false if Q is empty or the candidate does not fit (Q16, Q17).
-  __device__ __forceinline__ bool pick(i64 occ_now, u32 nb, Adm* a) {
-    if (hk_n == 0 || nb >= c->Bmax) return false;          // can_add_new_request: batch slots
+  __device__ __forceinline__ bool pick(i64 occ_now, u32 nb, u64 C, u32 Bmax, Adm* a) {
+    if (hk_n == 0 || nb >= Bmax) return false;             // can_add_new_request: batch slots
     u32 k = s.hk[0].user;
     UState& us = s.us[k];
     u32 nfk = us.nf;                                         // cached need of the front: a failing
-    if (nfk != NONE32 && (u64)occ_now + nfk > c->C) return false;   // candidate costs no global load
+    if (nfk != NONE32 && (u64)occ_now + nfk > C) return false;      // candidate costs no global load
     bool cont = us.qc_cnt != 0;
     u32 x = cont ? us.qc_head : 0;
     CSlot cs;
@@ -371,7 +374,7 @@ struct EngineT {
     u64 inc_pre = c->inc ? c->inc[r] : 0;
     u64 need = (u64)B.y + B.w;
     us.nf = (u32)need;
-    if ((u64)occ_now + need > c->C) return false;           // can_add_new_request: KV
+    if ((u64)occ_now + need > C) return false;              // can_add_new_request: KV
     u32 nseq = 0;
     if (cont) {
       a->arr = cs.t;
@@ -570,91 +573,116 @@ struct EngineT {
   }
 
   // ---------------------------------------------------------------- the replay (O4 with event skipping)
+  // Register caches keep the loop off memory: the next pending arrival (tn), the fronts of the
+  // pending-continuation heap (p0t, p0r) and of the batch heap (bfi), base + dec |B| (dB), and
+  // pick_blocked: after an admission round ends (Q empty, batch full or the front does not fit)
+  // no pick can succeed until Q's top changes (enqueue, class change, charge of a queued user)
+  // or a call finishes (occupancy and |B| drop); occupancy only grows in between.
+  i64 tn; bool tn_head, pend, pick_blocked;
+  i64 p0t; u32 p0r;
+  u64 bfi, dB;
+  __device__ __forceinline__ void p_front() { if (p_n) { p0t = s.p[0].t; p0r = s.p[0].r; } }
+  __device__ __forceinline__ void next_arrival() {
+    u32 hms = 0, hid = 0;
+    bool hok = head_peek(&hms, &hid);
+    i64 th = (i64)hms * 1000000;
+    bool pok = p_n != 0;
+    pend = hok || pok;
+    tn_head = hok && (!pok || th < p0t || (th == p0t && hid < p0r));
+    tn = tn_head ? th : (pok ? p0t : 0);
+  }
   __device__ __forceinline__ void run() {
+    const u64 C = c->C, base = c->base, dec = c->dec, pre = c->pre;
+    const u32 Bmax = c->Bmax;
+    pick_blocked = false; dB = base; bfi = 0; p0t = 0; p0r = 0;
+    next_arrival();
     for (;;) {
       if (HS == HS_WARP) __syncwarp();                            // lanes stay in lockstep
-      u32 hms = 0, hid = 0;
-      bool hok = head_peek(&hms, &hid);
-      i64 th = (i64)hms * 1000000;
-      bool pok = p_n != 0;
-      bool pend = hok || pok;                                     // next pending arrival in (t, id) order
-      bool is_head = hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hid < s.p[0].r));
-      i64 tn = is_head ? th : (pok ? s.p[0].t : 0);
       if (b_n == 0 && hk_n == 0) {                                // 1: idle engine restarts at the arrival
         if (!pend) break;
         if (tn > clock) clock = tn;
       }
-      bool ovl = overloaded();                                    // 2: occupancy at iteration start
-      while (pend && tn <= clock) {
-        int st;
-        if (is_head) {
-          HEnt h;
-          head_take(&h);
-          st = deliver_head(h, th, ovl);
-          head_done();
-        } else {
-          PEnt pe = s.p[0];
-          p_pop();
-          st = deliver_cont(pe.r, pe.user, pe.meta, pe.t, ovl);
-        }
-        if (st < 0) return;
-        hok = head_peek(&hms, &hid);
-        th = (i64)hms * 1000000;
-        pok = p_n != 0;
-        pend = hok || pok;
-        is_head = hok && (!pok || th < s.p[0].t || (th == s.p[0].t && hid < s.p[0].r));
-        tn = is_head ? th : (pok ? s.p[0].t : 0);
+      if (pend && tn <= clock) {
+        bool ovl = overloaded();                                  // 2: occupancy at iteration start
+        do {
+          int st;
+          if (tn_head) {
+            HEnt h;
+            head_take(&h);
+            st = deliver_head(h, tn, ovl);
+            head_done();
+          } else {
+            PEnt pe = s.p[0];
+            p_pop(); p_front();
+            st = deliver_cont(pe.r, pe.user, pe.meta, pe.t, ovl);
+          }
+          if (st < 0) return;
+          next_arrival();
+        } while (pend && tn <= clock);
       }
       u64 P_new = 0;                                              // 3: admission round
       u64 arr_sum = 0;                                            // sum of the admitted calls' arrivals
       nl_n = 0;
-      Adm ad;
-      while (pick(occ, b_n, &ad)) {
-        u32 r = ad.r;
-        b_push(ad.b);
-        occ += (i64)ad.prompt; P_new += ad.prompt;
-        if (o.first) s.nl_id[nl_n] = r;
-        arr_sum += (u64)ad.arr; nl_n++;
-        sum.n_admitted++;
-        u64 wt = (u64)(clock - ad.arr);
-        sum.sum_wait_ns += wt;
-        if (wt > sum.max_wait_ns) sum.max_wait_ns = wt;
-        digest = sm64(digest ^ r);
-        digest = sm64(digest ^ (u64)clock);
-        if (o.admit) { o.admit[r] = clock; o.order[r] = (u32)n_adm; if (o.status) o.status[r] = FS_ST_ADMIT; }
-        if (o.adm_app) o.adm_app[m_app(ad.b.meta)]++;
-        n_adm++;
+      if (!pick_blocked) {
+        Adm ad;
+        while (pick(occ, b_n, C, Bmax, &ad)) {
+          u32 r = ad.r;
+          b_push(ad.b);
+          dB += dec;
+          occ += (i64)ad.prompt; P_new += ad.prompt;
+          if (o.first) s.nl_id[nl_n] = r;
+          arr_sum += (u64)ad.arr; nl_n++;
+          u64 wt = (u64)(clock - ad.arr);
+          sum.sum_wait_ns += wt;
+          if (wt > sum.max_wait_ns) sum.max_wait_ns = wt;
+          digest = sm64(digest ^ r);
+          digest = sm64(digest ^ (u64)clock);
+          if (o.admit) { o.admit[r] = clock; o.order[r] = (u32)n_adm; if (o.status) o.status[r] = FS_ST_ADMIT; }
+          if (o.adm_app) o.adm_app[m_app(ad.b.meta)]++;
+          n_adm++;
+        }
+        pick_blocked = true;
+        if (nl_n) bfi = s.b[0].fi;
       }
       if (b_n == 0) continue;
-      u64 d = c->base + c->dec * b_n + c->pre * P_new;            // 4: iteration(s)
+      u64 d = dB + pre * P_new;                                   // 4: iteration(s)
       u64 m = 1;
       if (nl_n == 0) {                                            // event skipping: B constant until
-        m = s.b[0].fi - iter + 1;                                 //   the next finish ...
+        m = bfi - iter + 1;                                       //   the next finish ...
         if (pend && d > 0) {                                      //   ... or the next arrival
           u64 gap = (u64)(tn - clock);
           if (gap <= m * d) m = ceil_div_small(gap, d, m);         //   first boundary at or after tn
         }
       }
       iter += m;
-      sum.n_iterations += m;
       clock += (i64)(m * d);
       occ += (i64)(m * b_n);
       sum.sum_ttft_ns += (u64)nl_n * (u64)clock - arr_sum;       // sum of (first token - arrival), mod 2^64
       if (o.first) for (u32 q = 0; q < nl_n; q++) o.first[s.nl_id[q]] = clock;
-      while (b_n && s.b[0].fi == iter - 1) {                      // finishes (l.43-48)
-        BEnt f = s.b[0];
-        b_pop();
-        if (o.finish) o.finish[f.r] = clock;
-        sum.n_finished++;
-        occ -= (i64)f.rel;
-        if (!charge(f.user, f.inc, f.r)) return;
-        if (m_stage(f.meta) < m_ncalls(f.meta)) {
-          PEnt pe; pe.t = clock + (i64)f.think * 1000000; pe.r = f.link; pe.user = f.user;
-          pe.meta = f.meta + (1u << 8); pe.pad = 0;
-          if (!p_push(pe)) return;
-        }
+      if (bfi == iter - 1) {                                      // finishes (l.43-48)
+        bool pushed = false;
+        do {
+          BEnt f = s.b[0];
+          b_pop();
+          dB -= dec;
+          if (o.finish) o.finish[f.r] = clock;
+          occ -= (i64)f.rel;
+          if (!charge(f.user, f.inc, f.r)) return;
+          if (m_stage(f.meta) < m_ncalls(f.meta)) {
+            PEnt pe; pe.t = clock + (i64)f.think * 1000000; pe.r = f.link; pe.user = f.user;
+            pe.meta = f.meta + (1u << 8); pe.pad = 0;
+            if (!p_push(pe)) return;
+            pushed = true;
+          }
+          bfi = b_n ? s.b[0].fi : 0;
+        } while (b_n && bfi == iter - 1);
+        pick_blocked = false;
+        if (pushed) { p_front(); next_arrival(); }
       }
     }
+    sum.n_iterations = iter;
+    sum.n_admitted = n_adm;
+    sum.n_finished = n_adm;                                       // the loop ends with B empty
     // STOP: final digest, counters, summary
     for (u32 k = 0; k < U; k++) digest = sm64(digest ^ (s.us[k].u & ~CLS_BIT));
     digest = sm64(digest ^ (u64)clock);
@@ -903,7 +931,7 @@ __global__ void k_step(StepKArgs a) {
   u32 na = 0;                                                      // l.28-39
   i64 occ = a.occ; u32 nb = a.batch;
   EngineT<HS_DIRECT>::Adm ad;
-  while (E.pick(occ, nb, &ad)) {
+  while (E.pick(occ, nb, a.cfg.C, a.cfg.Bmax, &ad)) {
     a.admitted[na++] = ad.r;
     occ += (i64)ad.prompt;
     nb++;
