@@ -479,20 +479,27 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
-  // one warp per resident slot: FS_SWEEP_MINB picks the register cap (CTAs per SM)
+  // one scenario slot per group of LPS lanes (FS_SWEEP_LPS: 32 = a warp, 16, 8); FS_SWEEP_MINB
+  // picks the register cap (CTAs per SM)
   static const int minb = [] { const char* v = getenv("FS_SWEEP_MINB"); return v ? atoi(v) : 4; }();
-  auto kern = minb >= 8 ? k_sweep<8> : minb == 7 ? k_sweep<7> : minb == 6 ? k_sweep<6> : minb == 5 ? k_sweep<5> :
-              minb == 4 ? k_sweep<4> : minb == 3 ? k_sweep<3> : k_sweep<1>;
+  static const int lps = [] { const char* v = getenv("FS_SWEEP_LPS"); return v ? atoi(v) : 32; }();
+  auto kern = lps <= 8 ? (minb >= 4 ? k_sweep<4, 8> : k_sweep<3, 8>) :
+              lps == 16 ? (minb >= 4 ? k_sweep<4, 16> : k_sweep<3, 16>) :
+                          (minb >= 4 ? k_sweep<4, 32> : k_sweep<3, 32>);
+  const u32 per_cta = 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
+  // the replays' state lives in global memory: give L1 every byte shared memory does not need
+  static const int carve = [] { const char* v = getenv("FS_SWEEP_CARVE"); return v ? atoi(v) : -1; }();
+  if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, 0);
-  u64 slots = std::min<u64>(ns, (u64)ctx->sm_count * std::max(1, per_sm) * 4);
+  u64 slots = std::min<u64>(ns, (u64)ctx->sm_count * std::max(1, per_sm) * per_cta);
   u64 by_mem = (u64)(free_b / 2) / std::max<size_t>(slot_bytes, 1);
   slots = std::max<u64>(1, std::min(slots, by_mem));
-  slots = (slots + 3) / 4 * 4;                      // 4 warps per CTA
+  slots = (slots + per_cta - 1) / per_cta * per_cta;   // whole CTAs
   unsigned char* gm = S.alloc<unsigned char>(slots * slot_bytes + 256);
   if (S.failed) return FS_E_NOMEM;
   SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next};
-  FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / 4), 128, 0, a);
+  FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / per_cta), 128, 0, a);
   std::vector<int> hcodes(ns);
   cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);
   cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);

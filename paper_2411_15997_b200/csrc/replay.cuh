@@ -102,9 +102,9 @@ enum { HS_DIRECT = 0,                   // heads read one at a time (online step
        HS_RING = 1,                     // heads from the producer warp's shared-memory ring (single replay)
        HS_WARP = 2 };                   // all 32 lanes run the engine in lockstep and refill a per-warp
                                         // batch of the next 32 participating heads together (sweep)
-struct HeadBatch { HEnt e[32]; };       // per-warp shared-memory head batch (HS_WARP)
-
-template <int HS>
+// HS_WARP with LPS < 32: the warp runs 32 / LPS independent scenarios, each on its own
+// group of LPS lanes (groups diverge freely; a group stays in lockstep)
+template <int HS, int LPS = 32>
 struct EngineT {
   static constexpr bool RING = HS == HS_RING;
   const EngShared* sh;
@@ -122,7 +122,7 @@ struct EngineT {
   HeadRing ring;
   u32 rc_cons, rc_prod;                  // ring consumer index, last producer index seen
   HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
-  HeadBatch* hb; u32 hb_i, hb_n;         // HS_WARP: batch, next entry, entries
+  HEnt* hb; u32 hb_i, hb_n;              // HS_WARP: the group's shared-memory batch (LPS entries), next, count
   u32 hb_t, hb_r;                        // HS_WARP: (t_ms, id) of the next entry
   u64 digest, n_adm;
   fs_replay_summary sum;
@@ -415,13 +415,17 @@ struct EngineT {
   }
 
   // ---------------------------------------------------------------- heads source
-  // HS_WARP: the 32 lanes load the next 32 heads in parallel, keep the participating ones
-  // (tier <= tier_max) in trace order, and prefetch their users' state lines into L1
+  __device__ __forceinline__ static u32 group_mask() {
+    return LPS == 32 ? FULL_MASK : (((1u << LPS) - 1) << ((threadIdx.x & 31) & ~(u32)(LPS - 1)));
+  }
+  // HS_WARP: the group's LPS lanes load the next LPS heads in parallel, keep the participating
+  // ones (tier <= tier_max) in trace order, and prefetch their users' state lines into L1
   __device__ __forceinline__ bool head_refill() {
-    const u32 lane = threadIdx.x & 31;
+    const u32 sub = threadIdx.x & (LPS - 1);
+    const u32 gm = group_mask();
     const bool win = c->mode == FS_MODE_WI && static_heads;
     while (hp < sh->n_heads) {
-      u64 j = hp + lane;
+      u64 j = hp + sub;
       bool ok = j < sh->n_heads;
       HEnt h;
       if (ok) {
@@ -437,11 +441,11 @@ struct EngineT {
         } else { h.ng = h.na = 0; h.tg = h.ta = 0; }
         asm volatile("prefetch.global.L1 [%0];" :: "l"(&s.us[h.A.x]));
       }
-      u32 mask = __ballot_sync(FULL_MASK, ok);
-      hp += 32;
-      if (ok) hb->e[__popc(mask & lanemask_lt())] = h;
-      __syncwarp();
-      if (mask) { hb_n = __popc(mask); hb_i = 0; hb_t = hb->e[0].A.y; hb_r = hb->e[0].r; return true; }
+      u32 mask = __ballot_sync(gm, ok) & gm;
+      hp += LPS;
+      if (ok) hb[__popc(mask & lanemask_lt())] = h;
+      __syncwarp(gm);
+      if (mask) { hb_n = __popc(mask); hb_i = 0; hb_t = hb[0].A.y; hb_r = hb[0].r; return true; }
     }
     return false;
   }
@@ -487,8 +491,8 @@ struct EngineT {
   }
   __device__ __forceinline__ void head_take(HEnt* h) {   // by value: the engine stays in registers
     if (HS == HS_WARP) {
-      *h = hb->e[hb_i];
-      if (++hb_i < hb_n) { hb_t = hb->e[hb_i].A.y; hb_r = hb->e[hb_i].r; }
+      *h = hb[hb_i];
+      if (++hb_i < hb_n) { hb_t = hb[hb_i].A.y; hb_r = hb[hb_i].r; }
       return;
     }
     if (RING) { *h = ring.e[rc_cons % HRING]; return; }
@@ -597,7 +601,7 @@ struct EngineT {
     pick_blocked = false; dB = base; bfi = 0; p0t = 0; p0r = 0;
     next_arrival();
     for (;;) {
-      if (HS == HS_WARP) __syncwarp();                            // lanes stay in lockstep
+      if (HS == HS_WARP) __syncwarp(group_mask());                // the group's lanes stay in lockstep
       if (b_n == 0 && hk_n == 0) {                                // 1: idle engine restarts at the arrival
         if (!pend) break;
         if (tn > clock) clock = tn;
@@ -849,13 +853,15 @@ struct SweepKArgs {
   EngShared sh; const EngCfg* cfgs; u32 n_scen; EngLayout L; u32 U; unsigned char* gmem; size_t slot_bytes;
   u32 p_cap; fs_replay_summary* sums; int* codes; u32* next;
 };
-// Every lane of the warp runs the (warp-uniform) engine: loads and stores of the
-// replicated state are broadcast / merged, and the head batch refills use all 32 lanes.
-template <int MINB>                       // MINB CTAs per SM: caps registers (occupancy vs spills)
+// One scenario slot per group of LPS lanes.  Every lane of a group runs the (group-uniform)
+// engine: loads and stores of the replicated state are broadcast / merged, and head batch
+// refills use all LPS lanes.
+template <int MINB, int LPS>              // MINB CTAs per SM: caps registers (occupancy vs spills)
 __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
-  __shared__ HeadBatch hbs[4];
-  int lane = threadIdx.x & 31;
-  u32 slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  __shared__ HEnt hbs[128];
+  const u32 lane = threadIdx.x & 31, sub = threadIdx.x & (LPS - 1), lead = lane & ~(u32)(LPS - 1);
+  const u32 gm = EngineT<HS_WARP, LPS>::group_mask();
+  u32 slot = (blockIdx.x * blockDim.x + threadIdx.x) / LPS;
   unsigned char* g = a.gmem + (size_t)slot * a.slot_bytes;
   EngState st0;
   eng_bind(a.L, nullptr, g, a.p_cap, &st0, nullptr);
@@ -864,25 +870,25 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
   u64 AJ = (u64)a.sh.A * a.sh.J1;
   for (;;) {
     u32 sc = 0;
-    if (lane == 0) sc = atomicAdd(a.next, 1u);
-    sc = __shfl_sync(FULL_MASK, sc, 0);
+    if (sub == 0) sc = atomicAdd(a.next, 1u);
+    sc = __shfl_sync(gm, sc, lead);
     if (sc >= a.n_scen) return;
     EngState st = st0;
     st.W = (u64*)a.cfgs[sc].W;
-    eng_clear(st, a.sh, a.cfgs[sc].W, AJ, a.U, lane, 32);
-    __syncwarp();
+    eng_clear(st, a.sh, a.cfgs[sc].W, AJ, a.U, sub, LPS);
+    __syncwarp(gm);
     __threadfence_block();
     {
-      EngineT<HS_WARP> E;
+      EngineT<HS_WARP, LPS> E;
       E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
-      E.hb = &hbs[threadIdx.x >> 5];
+      E.hb = &hbs[threadIdx.x & ~(u32)(LPS - 1)];
       E.run();
-      if (lane == 0) {
+      if (sub == 0) {
         a.sums[sc] = E.sum;
         a.codes[sc] = E.err_code ? E.err_code + 1 : 0;
       }
     }
-    __syncwarp();
+    __syncwarp(gm);
   }
 }
 
