@@ -105,6 +105,7 @@ struct ActOrder {
   u64* lb;        // window lower bound per position (heads only)
   u32* pos;       // position of each call
   u32* flag; u64* tau;       // per pass
+  uint2* pre;                // static per position (k_act_pre)
   u32* pc; u64* ptau;        // exclusive scans
 };
 
@@ -124,21 +125,40 @@ __global__ void k_act_lb(u64 n, const u32* key, const u64* seg, const u32* perm,
   ao.lb[p] = window_lb<i64>(ao.ts, seg[key[p]], p, tp - W);
 }
 
-struct ActFlagArgs { u64 n; const u32* perm; const u32* meta; const u32* head_of; const uint8_t* status;
-                     const u64* tau_call; const i64* ts; u32 heads_only; };
+// Per position of an order, once per call (static over the Jacobi passes): {x, tau} with
+// x = NONE: never counted (never arrived / filtered, or a continuation in heads-only mode),
+// x = NONE - 1: a head (always counted), else the call's head id (counted iff that head is
+// admitted).  A pass then reads 8 B coalesced + one status byte for continuations.
+static const u32 ACT_HEAD = 0xFFFFFFFEu;
+// per call (coalesced): {x, tau} as above but without the arrival test
+__global__ void k_act_pack(u64 n, const u32* meta, const u32* head_of, const uint8_t* status, const u64* tau_call,
+                           u32 heads_only, uint2* pk) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  u32 x = NONE32;
+  if (status[i] != FS_ST_FILTERED) {
+    if (m_stage(meta[i]) == 1) x = ACT_HEAD;
+    else if (!heads_only) x = head_of[i];
+  }
+  pk[i] = make_uint2(x, x == NONE32 ? 0u : (u32)tau_call[i]);
+}
+// per position: 8 B gathered through the permutation; never-arrived calls are never counted
+__global__ void k_act_pre(u64 n, const u32* perm, const uint2* pk, const i64* ts, uint2* pre) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint2 v = pk[__ldg(&perm[p])];
+  if (ts[p] == INT64_MAX) v = make_uint2(NONE32, 0u);
+  pre[p] = v;
+}
 // counted(x): arrived, not filtered, and a head (any decision) or, in ALL mode, a
 // continuation whose head is admitted (Alg. 1 l.19; Q3)
-__global__ void k_act_flags(ActFlagArgs a, u32* flag, u64* tau) {
+__global__ void k_act_flags(u64 n, const uint2* pre, const uint8_t* status, u32* flag, u64* tau) {
   u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.n) return;
-  u32 i = a.perm[p];
-  bool c = false;
-  if (a.ts[p] != INT64_MAX && a.status[i] != FS_ST_FILTERED) {
-    if (m_stage(a.meta[i]) == 1) c = true;
-    else c = !a.heads_only && a.status[a.head_of[i]] == FS_ST_ADMIT;
-  }
+  if (p >= n) return;
+  uint2 v = pre[p];
+  bool c = v.x == ACT_HEAD || (v.x != NONE32 && status[v.x] == FS_ST_ADMIT);
   flag[p] = c;
-  tau[p] = c ? a.tau_call[i] : 0;
+  tau[p] = c ? v.y : 0;
 }
 
 struct ActDecideArgs {

@@ -158,7 +158,7 @@ static void prof_stream(fs_ctx* ctx, const DTrace& t, u32 J, u32 tier_max, u64* 
   if (t.n) FS_LAUNCH(ctx, "prof_stream", k_prof_stream, grid, 1024, smem, a);
 }
 
-static void prof_windows(fs_profile_partial* pp, const Order& o, u32* peak_r, u64* peak_t) {
+static void prof_windows(fs_profile_partial* pp, const Order& o, const uint2* pk, u32* peak_r, u64* peak_t) {
   fs_ctx* ctx = pp->ctx;
   Scratch& S = *pp->S;
   const DTrace& t = pp->t;
@@ -171,7 +171,7 @@ static void prof_windows(fs_profile_partial* pp, const Order& o, u32* peak_r, u6
   u32* pc = S.alloc<u32>(n + 1);
   if (S.failed) return;
   int B = 256;
-  WinGatherArgs g{t, o.perm, pp->cfg.max_stage, pp->cfg.tier_max, pp->cfg.count_mode, pp->P->ohat, ts, tau, flag};
+  WinGatherArgs g{n, o.perm, pk, ts, tau, flag};
   FS_LAUNCH(ctx, "win_gather", k_win_gather, div_up(n, B), B, 0, g);
   excl_scan<u64>(ctx, S, tau, ptau, n, ptau + n);
   excl_scan<u32>(ctx, S, flag, pc, n, pc + n);
@@ -286,8 +286,13 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
     cudaMemsetAsync(P->peak_t_u, 0, U * 8, ctx->stream);
     cudaMemsetAsync(P->peak_r_ua, 0, (u64)U * A * 4, ctx->stream);
     cudaMemsetAsync(P->peak_t_ua, 0, (u64)U * A * 8, ctx->stream);
-    prof_windows(pp, pp->ou, P->peak_r_u, P->peak_t_u);
-    prof_windows(pp, pp->oua, P->peak_r_ua, P->peak_t_ua);
+    uint2* wpk = pp->S->alloc<uint2>(pp->t.n + 1);
+    if (pp->t.n && wpk) {
+      WinPackArgs wp{pp->t, J, pp->cfg.tier_max, pp->cfg.count_mode, P->ohat, wpk};
+      FS_LAUNCH(ctx, "win_pack", k_win_pack, div_up(pp->t.n, B), B, 0, wp);
+    }
+    prof_windows(pp, pp->ou, wpk, P->peak_r_u, P->peak_t_u);
+    prof_windows(pp, pp->oua, wpk, P->peak_r_ua, P->peak_t_ua);
     u64 w = prof_q_next(pp, buf);
     u64* pk = buf + w;
     if (U) {
@@ -510,13 +515,21 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   const i64 W = (i64)cfg->window_ms * 1000000;
   ActOrder ou, oua;
   if (!act_order(ctx, S, t, tov, false, W, &ou) || !act_order(ctx, S, t, tov, true, W, &oua)) return FS_E_NOMEM;
+  const u32 heads_only = cfg->count_mode == FS_COUNT_HEADS_ONLY;
+  uint2* apk = S.alloc<uint2>(n);
+  if (S.failed) return FS_E_NOMEM;
+  FS_LAUNCH(ctx, "act_pack", k_act_pack, div_up(n, B), B, 0, n, t.meta, L.head_of, status, tau_call, heads_only, apk);
+  for (ActOrder* ao : {&ou, &oua}) {
+    ao->pre = S.alloc<uint2>(n);
+    if (S.failed) return FS_E_NOMEM;
+    FS_LAUNCH(ctx, "act_pre", k_act_pre, div_up(n, B), B, 0, n, ao->o.perm, apk, ao->ts, ao->pre);
+  }
   u32* changed = S.alloc<u32>(1);
   u32* uchg = S.alloc<u32>(t.U + 1);
   u32* ulist = S.alloc<u32>(t.U + 1);
   u32* nlist = S.alloc<u32>(1);
   if (S.failed) return FS_E_NOMEM;
   u64 passes = 0, fixup = 0;
-  const u32 heads_only = cfg->count_mode == FS_COUNT_HEADS_ONLY;
   // Jacobi passes before the exact per-user sequential walk of the users still changing
   // (FS_ACT_JACOBI_MAX overrides the default 2, for tests of both paths)
   const char* jenv = getenv("FS_ACT_JACOBI_MAX");
@@ -525,8 +538,7 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
     cudaMemsetAsync(changed, 0, 4, ctx->stream);
     cudaMemsetAsync(uchg, 0, (t.U + 1) * 4, ctx->stream);
     for (ActOrder* ao : {&ou, &oua}) {
-      ActFlagArgs fa{n, ao->o.perm, t.meta, L.head_of, status, tau_call, ao->ts, heads_only};
-      FS_LAUNCH(ctx, "act_flags", k_act_flags, div_up(n, B), B, 0, fa, ao->flag, ao->tau);
+      FS_LAUNCH(ctx, "act_flags", k_act_flags, div_up(n, B), B, 0, n, ao->pre, status, ao->flag, ao->tau);
       excl_scan<u32>(ctx, S, ao->flag, ao->pc, n, ao->pc + n);
       excl_scan<u64>(ctx, S, ao->tau, ao->ptau, n, ao->ptau + n);
     }

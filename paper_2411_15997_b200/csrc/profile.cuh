@@ -184,22 +184,35 @@ __global__ void k_prof_finish(u32 A, u32 J, const u64* cnt, const u64* s_out, u6
 // Gather the order's times and token loads, exclusive-scan counts and loads, then
 // per position the half-open window (t - W, t] by galloping search (Q4); peaks per
 // segment by a warp segmented max over the sorted keys + one atomicMax per run.
-struct WinGatherArgs {
-  DTrace t; const u32* perm; u32 J, tier_max, heads_only;
+// One coalesced pass packs what the window scans need per call: {t_ms, tau | counted << 31}
+// (tau = L_I + L_S + O-hat(a, j') < 2^26); each order then gathers 8 B per call through its
+// permutation instead of four scattered 4-B fields.
+struct WinPackArgs {
+  DTrace t; u32 J, tier_max, heads_only;
   const u64* ohat;                 // [A][J1]
+  uint2* pk;                       // per call
+};
+__global__ void k_win_pack(WinPackArgs a) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.t.n) return;
+  u32 m = __ldg(&a.t.meta[i]);
+  bool c = m_tier(m) <= a.tier_max && (!a.heads_only || m_stage(m) == 1);
+  u32 v = 0;
+  if (c) v = 0x80000000u | (__ldg(&a.t.len_in[i]) + __ldg(&a.t.len_sys[i]) +
+                            (u32)a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)]);
+  a.pk[i] = make_uint2(__ldg(&a.t.t_ms[i]), v);
+}
+struct WinGatherArgs {
+  u64 n; const u32* perm; const uint2* pk;
   u32* ts; u64* tau; u32* flag;    // per position
 };
 __global__ void k_win_gather(WinGatherArgs a) {
   u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.t.n) return;
-  u32 i = a.perm[p];
-  u32 m = a.t.meta[i];
-  bool c = m_tier(m) <= a.tier_max && (!a.heads_only || m_stage(m) == 1);
-  a.ts[p] = a.t.t_ms[i];
-  u64 tau = 0;
-  if (c) tau = (u64)a.t.len_in[i] + a.t.len_sys[i] + a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)];
-  a.tau[p] = tau;
-  a.flag[p] = c ? 1u : 0u;
+  if (p >= a.n) return;
+  uint2 v = a.pk[__ldg(&a.perm[p])];
+  a.ts[p] = v.x;
+  a.tau[p] = v.y & 0x7FFFFFFFu;
+  a.flag[p] = v.y >> 31;
 }
 
 __device__ __forceinline__ void atomic_max_u64(u64* p, u64 v) { atomicMax((unsigned long long*)p, (unsigned long long)v); }
