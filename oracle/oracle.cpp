@@ -424,7 +424,7 @@ extern "C" int or_act(const or_trace* t, const or_profile_view* p, const or_act_
 
 // ---------------------------------------------------------------- replay (O4)
 typedef struct {
-  u32 mode;                                   // 0 = FS(W), 1 = FS(W+I)
+  u32 mode;                                   // 0 = FS(W), 1 = FS(W+I), 2 = VTC, 3 = RPM, 4 = FCFS (NEXT-1)
   u32 alpha, beta, gamma;
   u32 prio_benign_q16, prio_abusive_q16;
   const u32* prio_q16;                        // optional per-user E (host)
@@ -468,6 +468,7 @@ struct Sched {
   i64 e = -1;                  // most recent user to exit Q (Alg.1 l.14)
   u64 seq = 0;
   std::vector<std::vector<std::tuple<i64, u64, u32>>> logs;   // ACT logs per user (t, tau, app)
+  std::vector<std::pair<i64, u32>> rpm_log;   // RPM: every arrival (t, call), delivery order
   u64 digest = 0;
   u64 n_adm = 0;
 
@@ -477,7 +478,17 @@ struct Sched {
   u64 prompt(u64 i) const { return (u64)t->len_in[i] + t->len_sys[i]; }
   u64 reserve(u64 i) const { return ohat_at(p, weight_slot(i)); }
   bool queued(u32 k) const { return !Qc[k].empty() || !Qh[k].empty(); }
+  // the user's front call: FS modes serve its continuations first (l.31-35); VTC, RPM
+  // and FCFS serve each user's calls in delivery order (R7)
+  bool front_is_cont(u32 k) const {
+    if (Qc[k].empty()) return false;
+    if (c->mode <= 1 || Qh[k].empty()) return true;
+    return Qc[k].front().second < Qh[k].front().second;
+  }
+  u64 front_seq(u32 k) const { return front_is_cont(k) ? Qc[k].front().second : Qh[k].front().second; }
   std::tuple<u32, u64, u64, u32> key_of(u32 k) const {
+    if (c->mode == 2) return std::make_tuple(0u, u[k], front_seq(k), k);        // VTC: argmin counter
+    if (c->mode >= 3) return std::make_tuple(0u, (u64)0, front_seq(k), k);      // RPM / FCFS: earliest
     if (!Qc[k].empty()) return std::make_tuple(0u, u[k], Qc[k].front().second, k);
     return std::make_tuple(1u, u[k], Qh[k].front().second, k);
   }
@@ -486,9 +497,11 @@ struct Sched {
   // Eq. 3 / Alg.1 l.48: u += floor(E * N * 2^32 / W_aj)
   int charge(u64 r) {
     u32 k = t->user[r];
+    if (c->mode >= 3) return OK;                              // RPM / FCFS keep no counters
     u64 E = c->prio_q16 ? c->prio_q16[k] : (tier_of(t, r) == 0 ? c->prio_benign_q16 : c->prio_abusive_q16);
     u64 N = (u64)c->alpha * t->len_in[r] + (u64)c->beta * t->len_sys[r] + (u64)c->gamma * t->len_out[r];
-    u128 inc = ((u128)E * N << 32) / W[weight_slot(r)];
+    // VTC: tokens weighted without app normalisation or priority, Q32.32
+    u128 inc = c->mode == 2 ? (u128)N << 32 : ((u128)E * N << 32) / W[weight_slot(r)];
     if (inc >= ((u128)1 << 63) || (u128)u[k] + inc >= ((u128)1 << 63)) return E_OVERFLOW;
     unindex(k);
     u[k] += (u64)inc;
@@ -513,6 +526,19 @@ struct Sched {
       if (c->act.count_mode == COUNT_ALL || head) logs[k].push_back(std::make_tuple(tr, tau_r, a));  // l.19
     }
     int st = ST_ADMIT;
+    if (c->mode == 3) {                                       // RPM: every
+      rpm_log.push_back(std::make_pair(tr, (u32)r));          // arrival, any stage, any load
+      const i64 Wn = (i64)c->act.window_ms * 1000000;
+      u64 n_u = 0, n_app = 0;                                 // user count / app count over all users
+      for (size_t q = rpm_log.size(); q-- > 0;) {
+        if (rpm_log[q].first <= tr - Wn) break;               // half-open window (Q4)
+        u32 x = rpm_log[q].second;
+        if (t->user[x] == k) n_u++;
+        if (app_of(t, x) == a) n_app++;
+      }
+      if (L.rg && n_u > L.rg) st = ST_USER_REQ;
+      else if (L.ra[a] && n_app > L.ra[a]) st = ST_APP_REQ;
+    }
     if (c->mode == 1 && ovl && head) {                        // l.20
       const i64 Wn = (i64)c->act.window_ms * 1000000;
       u64 n_g = 0, tau_g = 0, n_a = 0, tau_a = 0;
@@ -539,10 +565,11 @@ struct Sched {
   u32 pick(i64 occ, u64 batch, u64 C, u64 Bmax) {
     if (keys.empty()) return NONE;
     u32 k = std::get<3>(*keys.begin());
-    u32 r = !Qc[k].empty() ? Qc[k].front().first : Qh[k].front().first;
+    u32 r = front_is_cont(k) ? Qc[k].front().first : Qh[k].front().first;
     if ((u128)(u64)occ + prompt(r) + reserve(r) > C || batch >= Bmax) return NONE;  // can_add_new_request
+    bool fc = front_is_cont(k);
     unindex(k);
-    if (!Qc[k].empty()) Qc[k].pop_front(); else Qh[k].pop_front();
+    if (fc) Qc[k].pop_front(); else Qh[k].pop_front();
     if (!queued(k)) { n_queued_users--; e = k; }
     reindex(k);
     return r;
@@ -551,7 +578,7 @@ struct Sched {
 
 static int sched_init(Sched& S, const or_trace* t, const or_profile_view* p, const or_replay_cfg* c,
                       u64* bad_index, std::vector<u32>* head_of, std::vector<u32>* next_call) {
-  if (!t || !p || !c || c->max_batch == 0 || c->mode > 1 || c->alpha >= 256 || c->beta >= 256 ||
+  if (!t || !p || !c || c->max_batch == 0 || c->mode > 4 || c->alpha >= 256 || c->beta >= 256 ||
       c->gamma >= 256 || c->prio_benign_q16 >= (1u << 24) || c->prio_abusive_q16 >= (1u << 24))
     return E_INVAL;
   if (c->mode == 1 && (c->act.app_scope != 0 || c->act.count_mode > 1)) return E_INVAL;
@@ -560,7 +587,8 @@ static int sched_init(Sched& S, const or_trace* t, const or_profile_view* p, con
   int rc = or_validate(t, bad_index, head_of->data(), next_call->data());
   if (rc) return rc;
   S.t = t; S.p = p; S.c = c;
-  if (c->mode == 1) { rc = resolve_limits(p, &c->act, t->A, &S.L); if (rc) return rc; }
+  if (c->mode == 3 && (c->act.limits_from_profile || c->act.limit_mult_q8)) return E_INVAL;   // RPM: explicit limits (R8)
+  if (c->mode == 1 || c->mode == 3) { rc = resolve_limits(p, &c->act, t->A, &S.L); if (rc) return rc; }
   else resolve_limits(p, &c->act, t->A, &S.L);
   // W_aj = floor((a*SI + b*SS + g*SO) * 2^16 / C_aj)  (Eq. 2 with exact means, Q23)
   u64 J1 = p->J + 1;
@@ -635,9 +663,9 @@ extern "C" int or_replay(const or_trace* t, const or_profile_view* p, const or_r
       arrive[idn] = tn; ovlv[idn] = ovl; s->n_arrived++;
       if (ovl) s->n_ovl_arrivals++;
       int st = S.deliver(idn, tn, ovl);
-      if (st != ST_ADMIT) {
-        status[idn] = (uint8_t)st; s->n_block[st - 1]++;
-        s->n_dropped += ncalls_of(t, idn) - 1;
+      if (st != ST_ADMIT) {                                       // the interaction ends here (RPM:
+        status[idn] = (uint8_t)st; s->n_block[st - 1]++;          //  possibly midway, R8)
+        s->n_dropped += ncalls_of(t, idn) - stage_of(t, idn);
       }
     }
     u64 P_new = 0;                                                // 3
@@ -687,9 +715,17 @@ extern "C" int or_replay(const or_trace* t, const or_profile_view* p, const or_r
     if (!any) { s->u_min = s->u_max = S.u[k]; any = true; }
     s->u_min = std::min(s->u_min, S.u[k]); s->u_max = std::max(s->u_max, S.u[k]);
   }
-  for (u64 i = 0; i < n; i++)
-    if (status[i] == ST_NOT_ARRIVED && stage_of(t, i) > 1 && status[head_of[i]] != ST_ADMIT &&
-        status[head_of[i]] != ST_FILTERED) status[i] = ST_DROPPED;
+  // calls after a blocked call of their interaction never arrive: DROPPED (stage order)
+  std::vector<u32> prev(n, NONE);
+  for (u64 i = 0; i < n; i++) if (next_call[i] != NONE) prev[next_call[i]] = (u32)i;
+  std::vector<u64> by_stage(n);
+  for (u64 i = 0; i < n; i++) by_stage[i] = i;
+  std::stable_sort(by_stage.begin(), by_stage.end(), [&](u64 x, u64 y) { return stage_of(t, x) < stage_of(t, y); });
+  for (u64 i : by_stage)
+    if (status[i] == ST_NOT_ARRIVED && stage_of(t, i) > 1) {
+      uint8_t ps = status[prev[i]];
+      if (ps == ST_DROPPED || (ps >= ST_USER_REQ && ps <= ST_APP_TOK)) status[i] = ST_DROPPED;
+    }
   s->digest = S.digest;
   if (o) {
     if (o->status) std::memcpy(o->status, status.data(), n);
@@ -710,6 +746,7 @@ struct or_step_state { Sched S; std::vector<u32> head_of, next_call; };
 
 extern "C" int or_step_create(const or_trace* t, const or_profile_view* p, const or_replay_cfg* c,
                    or_step_state** out, u64* bad_index) {
+  if (c && c->mode == 3) return E_INVAL;                      // RPM needs the replay's time order (R8)
   or_step_state* st = new or_step_state();
   int rc = sched_init(st->S, t, p, c, bad_index, &st->head_of, &st->next_call);
   if (rc) { delete st; return rc; }

@@ -70,6 +70,7 @@ class Sched:
         self.e = None
         self.seq = 0
         self.log = []            # (t, tau, user, app) of counted arrivals
+        self.rlog = []           # RPM: (t, user, app) of every arrival
         self.digest = 0
 
     def weight(self, c):         # Eq. 2 with exact integer means, Q16
@@ -93,7 +94,10 @@ class Sched:
     def finish(self, r):         # Alg. 1 l.44-48, Eq. 3
         c = self.calls[r]
         N = self.al * c["L_I"] + self.be * c["L_S"] + self.ga * c["L_O"]
-        self.u[c["user"]] += (self.prio(c) * N << 32) // self.weight(c)
+        if self.mode == 2:       # VTC: weighted tokens, no app normalisation, no priority
+            self.u[c["user"]] += N << 32
+        elif self.mode <= 1:
+            self.u[c["user"]] += (self.prio(c) * N << 32) // self.weight(c)
 
     def deliver(self, r, t, ovl):   # Alg. 1 l.11-25
         c = self.calls[r]
@@ -109,6 +113,13 @@ class Sched:
         if self.mode == 1 and (not self.heads_only or c["stage"] == 1):
             self.log.append((t, tau, k, c["app"]))                     # l.19
         st = ADMIT
+        if self.mode == 3:                                               # RPM: every arrival
+            self.rlog.append((t, k, c["app"]))
+            win = [x for x in self.rlog if t - self.Wn < x[0] <= t]
+            if self.Trg and len([x for x in win if x[1] == k]) > self.Trg:
+                st = USER_REQ
+            elif self.Tra[c["app"]] and len([x for x in win if x[2] == c["app"]]) > self.Tra[c["app"]]:
+                st = APP_REQ
         if self.mode == 1 and ovl and c["stage"] == 1:                   # l.20
             win = [x for x in self.log if x[2] == k and t - self.Wn < x[0] <= t]
             n_g, tau_g = len(win), sum(x[1] for x in win)
@@ -133,11 +144,16 @@ class Sched:
         Q = self.Q
         if not Q:
             return None
-        conts = [q for q in Q if q[2]]
-        pool = conts if conts else Q                                     # l.31-35 vs l.36-38
-        ku = min(pool, key=lambda q: (self.u[self.calls[q[0]]["user"]], q[1]))
-        k = self.calls[ku[0]]["user"]
-        cand = min((q for q in Q if self.calls[q[0]]["user"] == k and q[2] == ku[2]), key=lambda q: q[1])
+        if self.mode >= 2:       # VTC: argmin (counter, delivery); RPM / FCFS: earliest delivery
+            w = (lambda q: (self.u[self.calls[q[0]]["user"]], q[1])) if self.mode == 2 else (lambda q: q[1])
+            cand = min(Q, key=w)
+            k = self.calls[cand[0]]["user"]
+        else:
+            conts = [q for q in Q if q[2]]
+            pool = conts if conts else Q                                 # l.31-35 vs l.36-38
+            ku = min(pool, key=lambda q: (self.u[self.calls[q[0]]["user"]], q[1]))
+            k = self.calls[ku[0]]["user"]
+            cand = min((q for q in Q if self.calls[q[0]]["user"] == k and q[2] == ku[2]), key=lambda q: q[1])
         c = self.calls[cand[0]]
         if occ + c["L_I"] + c["L_S"] + self.reserve(c) > self.C or nb >= self.Bmax:
             return None                                                  # can_add_new_request
@@ -188,7 +204,7 @@ def replay(tr, prof, cfg):
             if st != ADMIT:
                 status[r] = st
                 summ["n_block"][st - 1] += 1
-                summ["n_dropped"] += calls[r]["ncalls"] - 1
+                summ["n_dropped"] += calls[r]["ncalls"] - calls[r]["stage"]
         P_new = 0
         newly = []
         while True:
@@ -230,10 +246,10 @@ def replay(tr, prof, cfg):
     for k in range(S.U):
         S.digest = _sm64(S.digest ^ S.u[k])
     S.digest = _sm64(S.digest ^ (clock & MASK))
-    for c in calls:
+    for c in sorted(calls, key=lambda c: c["stage"]):   # after a blocked call: DROPPED
         if status[c["id"]] == NOT_ARRIVED and c["stage"] > 1:
-            h = next(d for d in calls if d["inter"] == c["inter"] and d["stage"] == 1)
-            if status[h["id"]] not in (ADMIT, FILTERED):
+            p = next(d for d in calls if d["inter"] == c["inter"] and d["stage"] == c["stage"] - 1)
+            if status[p["id"]] in (USER_REQ, USER_TOK, APP_REQ, APP_TOK, DROPPED):
                 status[c["id"]] = DROPPED
     summ.update(n_iterations=iters, makespan_ns=clock, digest=S.digest)
     out = dict(status=status, ovl=ovl_at, arrive_ns=arrive, admit_ns=admit, first_ns=first,

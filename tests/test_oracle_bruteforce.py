@@ -46,6 +46,26 @@ def test_replay_vs_stepper(seed):
         assert s[k] == es[k], (k, seed)
 
 
+@pytest.mark.parametrize("seed", range(300))
+def test_replay_vs_stepper_baselines(seed):
+    """NEXT-1 baseline policies (VTC, RPM, FCFS) against the literal stepper."""
+    rng = np.random.default_rng(9000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(1, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    prof = O.profile_from_host(A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A, modes=(2, 3, 4))
+    if _oversize(tr, prof, cfg):
+        return
+    o, s = O.replay(tr, prof, cfg)
+    eo, es = S.replay(tr, prof, cfg)
+    for k in ("status", "ovl", "arrive_ns", "admit_ns", "first_ns", "finish_ns", "order", "counters"):
+        assert list(o[k]) == list(eo[k]), (k, seed)
+    for k in ("n_arrived", "n_block", "n_dropped", "n_admitted", "n_finished", "n_iterations",
+              "n_ovl_arrivals", "makespan_ns", "digest"):
+        assert s[k] == es[k], (k, seed)
+
+
 def test_replay_exhaustive_pairs():
     """Exhaustive grid: two single-call users x arrival times x lengths x Bmax."""
     n = 0
@@ -62,7 +82,7 @@ def test_replay_exhaustive_pairs():
                         tr = from_columns(2, 2, rows)
                         prof = O.profile_from_host(2, 2, [[0, 2, 1], [0, 1, 0]], [[0, 4, 2], [0, 3, 0]],
                                                    [[0, 0, 0], [0, 0, 0]], [[0, 3, 1], [0, 2, 0]])
-                        for mode in (0, 1):
+                        for mode in (0, 1, 2, 3, 4):
                             cfg = dict(mode=mode, kv_capacity=C, max_batch=Bmax, overload_permille=500,
                                        iter_base_ns=1_000_000, decode_ns_per_req=0, prefill_ns_per_tok=0,
                                        act=dict(window_ms=3, limits_from_profile=0, T_req_g=1, T_req_a=[1, 1]))
@@ -72,7 +92,7 @@ def test_replay_exhaustive_pairs():
                                 assert list(o[k]) == list(eo[k])
                             assert s["digest"] == es["digest"]
                             n += 1
-    assert n == 4 * 4 * 3 * 2 * 2 * 2
+    assert n == 4 * 4 * 3 * 2 * 2 * 5
 
 
 @pytest.mark.parametrize("seed", range(200))

@@ -41,8 +41,8 @@ def tiny_trace(rng, n_users=3, n_apps=2, max_inters=4, times=(0, 1, 2, 5), lens=
     return from_columns(n_users, n_apps, rows)
 
 
-def tiny_replay_cfg(rng, n_apps):
-    cfg = dict(mode=int(rng.integers(0, 2)), alpha=int(rng.choice((1, 2))), beta=int(rng.choice((1, 2))),
+def tiny_replay_cfg(rng, n_apps, modes=(0, 1)):
+    cfg = dict(mode=int(modes[int(rng.integers(0, len(modes)))]), alpha=int(rng.choice((1, 2))), beta=int(rng.choice((1, 2))),
                gamma=int(rng.choice((1, 3))), prio_benign_q16=65536,
                prio_abusive_q16=int(rng.choice((65536, 131072, 32768))),
                kv_capacity=int(rng.choice((14, 20, 30, 100))), max_batch=int(rng.choice((1, 2, 3))),
@@ -56,6 +56,9 @@ def tiny_replay_cfg(rng, n_apps):
                       T_tok_g=int(rng.choice((0, 0, 12))),
                       T_tok_a=[int(rng.choice((0, 0, 9))) for _ in range(n_apps)],
                       count_mode=int(rng.integers(0, 2)))
+    if cfg["mode"] == 3:         # RPM: explicit request limits only (R8)
+        cfg["act"]["T_tok_g"] = 0
+        cfg["act"]["T_tok_a"] = [0] * n_apps
     return cfg
 
 
