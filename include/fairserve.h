@@ -171,7 +171,17 @@ int fs_act_throttle(fs_ctx* ctx, const fs_trace* trace, const fs_profile* profil
  * W_aj = floor((alpha SI + beta SS + gamma SO) 2^16 / cnt) (Eq. 2, Q23).
  * Lift on arrival of a user with nothing queued (l.12-18); pick = lexicographic
  * argmin of (continuation ? 0 : 1, u, delivery order) (l.31-38, Q13-Q15). */
-enum { FS_MODE_W = 0 /* FS(W) */, FS_MODE_WI = 1 /* FS(W+I) */ };
+enum { FS_MODE_W = 0 /* FS(W) */, FS_MODE_WI = 1 /* FS(W+I) */,
+       /* NEXT-1 baselines (R7-R8):        */
+       FS_MODE_VTC = 2,   /* WSC without app normalisation / priority / continuation priority:
+                             u += (alpha L_I + beta L_S + gamma L_O) 2^32, users' calls in
+                             delivery order; never blocks                                      */
+       FS_MODE_RPM = 3,   /* FCFS + overload-oblivious throttling of every arrival: USER_REQ if
+                             the user's arrivals in (t-W, t] > act.T_req_g, else APP_REQ if the
+                             app's arrivals (all users) > act.T_req_a[a]; a blocked continuation
+                             aborts its interaction; explicit limits only (else FS_E_INVAL);
+                             not supported by fs_wsc_step (FS_E_INVAL)                        */
+       FS_MODE_FCFS = 4   /* the globally earliest queued call (delivery = (t, id) order)     */ };
 typedef struct {
   uint32_t mode;
   uint32_t alpha, beta, gamma;                 /* token weights (1,2,1) P:475 */
@@ -181,7 +191,7 @@ typedef struct {
   uint32_t max_batch, overload_permille;       /* UINT32_MAX = never overloaded */
   uint64_t iter_base_ns, decode_ns_per_req, prefill_ns_per_tok;
   uint32_t tier_max;                           /* users with tier > tier_max do not exist (FILTERED) */
-  fs_act_cfg act;                              /* used when mode == FS_MODE_WI */
+  fs_act_cfg act;                              /* used when mode == FS_MODE_WI or FS_MODE_RPM */
 } fs_replay_cfg;
 typedef struct {                               /* DEVICE, caller-owned; any pointer may be NULL */
   uint8_t* status; uint8_t* overloaded_at_arrival;

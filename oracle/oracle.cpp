@@ -581,13 +581,13 @@ static int sched_init(Sched& S, const or_trace* t, const or_profile_view* p, con
   if (!t || !p || !c || c->max_batch == 0 || c->mode > 4 || c->alpha >= 256 || c->beta >= 256 ||
       c->gamma >= 256 || c->prio_benign_q16 >= (1u << 24) || c->prio_abusive_q16 >= (1u << 24))
     return E_INVAL;
-  if (c->mode == 1 && (c->act.app_scope != 0 || c->act.count_mode > 1)) return E_INVAL;
+  if ((c->mode == 1 || c->mode == 3) && (c->act.app_scope != 0 || c->act.count_mode > 1)) return E_INVAL;
+  if (c->mode == 3 && (c->act.limits_from_profile || c->act.limit_mult_q8)) return E_INVAL;   // RPM: explicit limits (R8)
   if (p->A != t->A) { *bad_index = 0; return E_PROFILE; }
   head_of->resize(t->n); next_call->resize(t->n);
   int rc = or_validate(t, bad_index, head_of->data(), next_call->data());
   if (rc) return rc;
   S.t = t; S.p = p; S.c = c;
-  if (c->mode == 3 && (c->act.limits_from_profile || c->act.limit_mult_q8)) return E_INVAL;   // RPM: explicit limits (R8)
   if (c->mode == 1 || c->mode == 3) { rc = resolve_limits(p, &c->act, t->A, &S.L); if (rc) return rc; }
   else resolve_limits(p, &c->act, t->A, &S.L);
   // W_aj = floor((a*SI + b*SS + g*SO) * 2^16 / C_aj)  (Eq. 2 with exact means, Q23)

@@ -91,7 +91,7 @@ __global__ void k_pack_inc(u64 n, const uint4* recA, const uint4* recB, const ui
   u64 E = c.prio_q16 ? c.prio_q16[A.x] : (m_tier(A.z) == 0 ? c.prio_b : c.prio_a);
   u64 N = (u64)c.alpha * Cv.z + (u64)c.beta * Cv.w + (u64)c.gamma * Bv.z;
   u64 w = c.W[Cv.x];
-  u128 q = w ? (((u128)E * N) << 32) / w : 0;
+  u128 q = c.mode == FS_MODE_VTC ? (u128)N << 32 : w ? (((u128)E * N) << 32) / w : 0;   // VTC: R7
   inc[i] = q >= ((u128)1 << 63) ? ~0ull : (u64)q;
 }
 
@@ -255,25 +255,33 @@ __global__ void k_replay_pre(DTrace t, u32 tier_max, fs_replay_out o) {
   if (o.finish_ns) o.finish_ns[i] = -1;
   if (o.order) o.order[i] = NONE32;
 }
-__global__ void k_replay_post(DTrace t, const u32* head_of, uint8_t* status) {
+// a call that never arrived after a blocked call of its interaction is DROPPED (the walk from
+// the head reads only block codes, which no thread changes here)
+__global__ void k_replay_post(DTrace t, const u32* head_of, const u32* next_call, uint8_t* status) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= t.n || !status) return;
   if (status[i] == FS_ST_NOT_ARRIVED && m_stage(t.meta[i]) > 1) {
-    uint8_t hs = status[head_of[i]];
-    if (hs >= FS_ST_BLOCK_USER_REQ && hs <= FS_ST_BLOCK_APP_TOK) status[i] = FS_ST_DROPPED;
+    for (u32 x = head_of[i]; x != (u32)i && x != NONE32; x = next_call[x]) {
+      uint8_t hs = status[x];
+      if (hs >= FS_ST_BLOCK_USER_REQ && hs <= FS_ST_BLOCK_APP_TOK) { status[i] = FS_ST_DROPPED; break; }
+    }
   }
 }
 
 static bool replay_cfg_ok(const fs_replay_cfg* c) {
-  return c && c->mode <= 1 && c->alpha < 256 && c->beta < 256 && c->gamma < 256 && c->prio_benign_q16 < (1u << 24) &&
-         c->prio_abusive_q16 < (1u << 24) && c->max_batch >= 1 && (c->mode == 0 || act_cfg_ok(&c->act));
+  if (!c || c->mode > FS_MODE_FCFS) return false;
+  if (c->mode == FS_MODE_RPM && (c->act.limits_from_profile || c->act.limit_mult_q8)) return false;   // R8
+  return c->alpha < 256 && c->beta < 256 && c->gamma < 256 && c->prio_benign_q16 < (1u << 24) &&
+         c->prio_abusive_q16 < (1u << 24) && c->max_batch >= 1 &&
+         ((c->mode != FS_MODE_WI && c->mode != FS_MODE_RPM) || act_cfg_ok(&c->act));
 }
 
 static ScenParam scen_param(const fs_replay_cfg* c) {
   ScenParam p;
   memset(&p, 0, sizeof(p));
   p.alpha = c->alpha; p.beta = c->beta; p.gamma = c->gamma;
-  p.from_profile = c->act.limits_from_profile; p.kq8 = c->mode == FS_MODE_WI ? c->act.limit_mult_q8 : 0xFFFFFFFFu;
+  p.from_profile = c->act.limits_from_profile;
+  p.kq8 = (c->mode == FS_MODE_WI || c->mode == FS_MODE_RPM) ? c->act.limit_mult_q8 : 0xFFFFFFFFu;
   p.xrg = c->act.T_req_g; p.xtg = c->act.T_tok_g; p.tier_max = c->tier_max; p.C = c->kv_capacity;
   return p;
 }
@@ -288,7 +296,7 @@ static bool scen_tables(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profi
   std::vector<u64> hta((size_t)ns * A, 0);
   for (u32 s = 0; s < ns; s++) {
     hp[s] = scen_param(&cfgs[s]);
-    if (cfgs[s].mode == FS_MODE_WI && !cfgs[s].act.limits_from_profile) {
+    if ((cfgs[s].mode == FS_MODE_WI || cfgs[s].mode == FS_MODE_RPM) && !cfgs[s].act.limits_from_profile) {
       if (cfgs[s].act.T_req_a_h) for (u32 a = 0; a < A; a++) hra[(size_t)s * A + a] = cfgs[s].act.T_req_a_h[a];
       if (cfgs[s].act.T_tok_a_h) for (u32 a = 0; a < A; a++) hta[(size_t)s * A + a] = cfgs[s].act.T_tok_a_h[a];
     }
@@ -383,19 +391,23 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
     if (t.n) FS_LAUNCH(ctx, "replay_pre", k_replay_pre, div_up(t.n, B), B, 0, t, cfg->tier_max, o);
     if (o.admitted_per_app) cudaMemsetAsync(o.admitted_per_app, 0, t.A * 8, ctx->stream);
     // queued-continuation pool: same two-step capacity (n_inters is an exact bound)
-    EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget);
+    EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget,
+                             cfg->mode >= FS_MODE_VTC, cfg->mode == FS_MODE_RPM ? (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull) : 0,
+                             t.A);
     unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
     if (S.failed) return FS_E_NOMEM;
     ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
-    cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
-    FS_LAUNCH(ctx, "wsc_replay", k_replay, 1, 64, L.bytes_smem, a);
+    auto rk = cfg->mode >= FS_MODE_VTC ? k_replay<true> : k_replay<false>;
+    cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
+    FS_LAUNCH(ctx, "wsc_replay", rk, 1, 64, L.bytes_smem, a);
     cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
     cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
     rc = finish(ctx, &S);
     if (rc) return rc;
     if (!(hcode && ERR_TO_FS[hcode - 1] == FS_E_NOMEM)) break;     // retry only a capacity overflow
   }
-  if (t.n && o.status) FS_LAUNCH(ctx, "replay_post", k_replay_post, div_up(t.n, B), B, 0, t, W.L.head_of, o.status);
+  if (t.n && o.status)
+    FS_LAUNCH(ctx, "replay_post", k_replay_post, div_up(t.n, B), B, 0, t, W.L.head_of, W.L.next_call, o.status);
   cudaMemcpyAsync(sum, dsum, sizeof(*sum), cudaMemcpyDeviceToHost, ctx->stream);
   rc = finish(ctx, &S);
   if (rc) return rc;
@@ -408,9 +420,11 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
                         fs_replay_summary* out, int32_t* codes) {
   if (!ctx || !tr || !P || !scen || !out || !codes || tr->n_apps == 0) return FS_E_INVAL;
   if (ns == 0) return FS_OK;
-  bool any_wi = false;
+  bool any_wi = false, any_dq = false, any_rpm = false;
   u32 Bmax = 1;
   for (u32 s = 0; s < ns; s++) {
+    any_dq |= scen[s].mode >= FS_MODE_VTC;
+    any_rpm |= scen[s].mode == FS_MODE_RPM;
     if (!replay_cfg_ok(&scen[s]) || scen[s].prio_q16) return FS_E_INVAL;
     if (scen[s].mode == FS_MODE_WI) {
       for (u32 q = 0; q < s; q++)          // one static head window per call
@@ -447,7 +461,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
     std::vector<u32> combo_of(ns);
     for (u32 s = 0; s < ns; s++) {
       std::vector<u32> key = {scen[s].alpha, scen[s].beta, scen[s].gamma, scen[s].prio_benign_q16,
-                              scen[s].prio_abusive_q16};
+                              scen[s].prio_abusive_q16, scen[s].mode == FS_MODE_VTC ? 1u : 0u};
       u32 k = 0;
       while (k < combos.size() && combos[k] != key) k++;
       if (k == combos.size()) combos.push_back(key);
@@ -475,7 +489,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   cudaMemcpyAsync(dc, hc.data(), ns * sizeof(EngCfg), cudaMemcpyHostToDevice, ctx->stream);
   u32 p_cap = std::max<u32>(std::min<u32>(t.X, 1u << 16), 1);
   EngLayout L = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi,
-                           W.ring_slots, false, 0);
+                           W.ring_slots, false, 0, any_dq, any_rpm ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0, t.A);
   size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -483,9 +497,13 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   // picks the register cap (CTAs per SM)
   static const int minb = [] { const char* v = getenv("FS_SWEEP_MINB"); return v ? atoi(v) : 4; }();
   static const int lps = [] { const char* v = getenv("FS_SWEEP_LPS"); return v ? atoi(v) : 32; }();
-  auto kern = lps <= 8 ? (minb >= 4 ? k_sweep<4, 8> : k_sweep<3, 8>) :
-              lps == 16 ? (minb >= 4 ? k_sweep<4, 16> : k_sweep<3, 16>) :
-                          (minb >= 4 ? k_sweep<4, 32> : k_sweep<3, 32>);
+  // scenarios of the FairServe modes only: the engine without the baseline-mode paths
+  auto kern = any_dq ? (lps <= 8 ? (minb >= 4 ? k_sweep<4, 8, true> : k_sweep<3, 8, true>) :
+                        lps == 16 ? (minb >= 4 ? k_sweep<4, 16, true> : k_sweep<3, 16, true>) :
+                                    (minb >= 4 ? k_sweep<4, 32, true> : k_sweep<3, 32, true>))
+                     : (lps <= 8 ? (minb >= 4 ? k_sweep<4, 8, false> : k_sweep<3, 8, false>) :
+                        lps == 16 ? (minb >= 4 ? k_sweep<4, 16, false> : k_sweep<3, 16, false>) :
+                                    (minb >= 4 ? k_sweep<4, 32, false> : k_sweep<3, 32, false>));
   const u32 per_cta = 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
   // the replays' state lives in global memory: give L1 every byte shared memory does not need
   static const int carve = [] { const char* v = getenv("FS_SWEEP_CARVE"); return v ? atoi(v) : -1; }();
@@ -540,6 +558,7 @@ __global__ void k_step_init(EngLayout L, unsigned char* gm, u32 p_cap, EngShared
 extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
                                    fs_wsc_state** out) {
   if (!ctx || !tr || !P || !out || !replay_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
+  if (cfg->mode == FS_MODE_RPM) return FS_E_INVAL;         // RPM needs the replay's time order (R8)
   *out = nullptr;
   if (P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
   fs_wsc_state* st = new fs_wsc_state();
@@ -577,7 +596,7 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
   if (rc) { delete st; return rc; }
   st->W.sh.r_off = roff;
   st->L = eng_layout(st->U, std::max<u64>(st->t.n, 1), st->W.n_heads, cfg->max_batch, st->p_cap, AJ,
-                     cfg->mode == FS_MODE_WI, ring_slots, false, 0);
+                     cfg->mode == FS_MODE_WI, ring_slots, false, 0, cfg->mode >= FS_MODE_VTC, 0, tr->n_apps);
   st->gm = S.alloc<unsigned char>(st->L.bytes_glob + 256);
   st->scal = S.alloc<i64>(8);
   if (S.failed) { delete st; return FS_E_NOMEM; }

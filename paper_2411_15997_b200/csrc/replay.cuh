@@ -27,6 +27,7 @@
 
 static const u32 SWEEP_RING_CAP = 512;  // sweep: continuation arrivals kept per user window (FS_E_NOMEM beyond)
 static const u32 HRING = 128;           // head prefetch ring entries
+static const u32 SWEEP_RPM_CAP = 65536; // sweep: RPM window log entries per scenario (FS_E_NOMEM beyond, R5)
 
 struct EngShared {                      // read-only, shared by every replay of a trace
   DTrace t;
@@ -58,10 +59,10 @@ struct EngCfg {                         // one scenario
 struct alignas(16) UState {             // per user, 64 B
   u64 u;                                // counter, Q32.32; bit 63 = class of the queue front (1 = head)
   u32 tie, hf, nf;                      // tie of the front; front head id; KV need of the front (NONE = ?)
-  u32 pad0, pad1;
+  u32 hs, cs;                           // VTC / RPM / FCFS: delivery seq of the head / continuation front
   u32 qh_front, qh_next, qh_cnt;        // head FIFO: absolute uh_list positions, queued count
   u32 qc_head, qc_tail, qc_cnt;         // continuation FIFO (pool slots)
-  u32 r_head, r_len;                    // ACT continuation ring
+  u32 r_head, r_len;                    // ACT continuation ring (FS(W+I)); RPM: r_len = live arrivals
   u32 cf;                               // call id of the continuation FIFO's front
 };
 struct HK { u64 key; u32 tie, user; };  // pick heap entry: (class | u, tie)
@@ -70,6 +71,7 @@ struct CSlot { u32 r, next, nseq, nr; i64 t; };    // queued continuation: call,
 struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batch entry (48 B)
 struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
 struct REnt { i64 t; u32 tau, app; };   // ACT ring entry: arrival, token load, app (16 B)
+struct RPEnt { i64 t; u32 user, app; }; // RPM window log entry (16 B)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
 
 struct EngState {
@@ -81,6 +83,8 @@ struct EngState {
   uint2* hpos;                          // [U] heap positions (hk, hm; NONE = not queued): dense, apart
                                         // from the 64-B user records a sift would otherwise touch
   REnt* r;                              // ACT rings [ring slots] (CSR by user), one 16-B entry each
+  u32* hseq;                            // VTC / RPM / FCFS: delivery seq of each head (uh position)
+  RPEnt* rf; u32 rf_cap; u32* rapp;     // RPM: window log of every arrival (FIFO), live arrivals per app
   u64* W;                               // stage weights (smem copy or the scenario's table)
 };
 
@@ -104,7 +108,7 @@ enum { HS_DIRECT = 0,                   // heads read one at a time (online step
                                         // batch of the next 32 participating heads together (sweep)
 // HS_WARP with LPS < 32: the warp runs 32 / LPS independent scenarios, each on its own
 // group of LPS lanes (groups diverge freely; a group stays in lockstep)
-template <int HS, int LPS = 32>
+template <int HS, int LPS = 32, bool BASE = true>   // BASE: the NEXT-1 baseline modes compiled in
 struct EngineT {
   static constexpr bool RING = HS == HS_RING;
   const EngShared* sh;
@@ -124,6 +128,7 @@ struct EngineT {
   HEnt cur; bool cur_ok;                 // next head arrival (direct mode cache)
   HEnt* hb; u32 hb_i, hb_n;              // HS_WARP: the group's shared-memory batch (LPS entries), next, count
   u32 hb_t, hb_r;                        // HS_WARP: (t_ms, id) of the next entry
+  u32 rf_head, rf_len;                   // RPM window log: oldest entry, live entries
   u64 digest, n_adm;
   fs_replay_summary sum;
   int err_code; u64 err_idx;
@@ -185,15 +190,16 @@ struct EngineT {
     c_top = st.c_cap;                                      // eng_clear fills cfree[i] = i
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
     static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
-    hb_i = hb_n = 0;
+    hb_i = hb_n = 0; rf_head = rf_len = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
 
   // ---------------------------------------------------------------- Eq. 3 (l.44-48)
   __device__ __forceinline__ u64 increment(u32 user, u32 meta, const uint4& B, const uint4& Cc) const {
-    u64 E = c->prio_q16 ? c->prio_q16[user] : (m_tier(meta) == 0 ? c->prio_b : c->prio_a);
     u64 N = (u64)c->alpha * Cc.z + (u64)c->beta * Cc.w + (u64)c->gamma * B.z;
+    if (BASE && c->mode == FS_MODE_VTC) return N >= (1ull << 31) ? ~0ull : N << 32;   // R7: tokens, no W or E
+    u64 E = c->prio_q16 ? c->prio_q16[user] : (m_tier(meta) == 0 ? c->prio_b : c->prio_a);
     return q32_div(E * N, s.W[Cc.x]);
   }
   // floor(n * 2^32 / W) exactly (n < 2^60, W >= 1), ~0 if >= 2^63: a double-precision
@@ -215,6 +221,7 @@ struct EngineT {
     return q >= (1ull << 63) ? ~0ull : q;
   }
   __device__ __forceinline__ bool charge(u32 k, u64 inc, u32 r) {
+    if (BASE && c->mode >= FS_MODE_RPM) return true;     // RPM / FCFS keep no counters (R7, R8)
     UState& us = s.us[k];
     u64 cur = us.u & ~CLS_BIT;
     if (inc == ~0ull || cur + inc >= (1ull << 63)) { err_code = ERR_OVERFLOW; err_idx = r; return false; }
@@ -268,6 +275,28 @@ struct EngineT {
     return true;
   }
 
+  // RPM (R8): log every arrival, expire the window (t - W, t] in FIFO order (deliveries come in
+  // time order), then the user's and the app's (all users) live arrival counts
+  __device__ __forceinline__ int rpm_check(UState& us, u32 k, u32 app, i64 tr, u32 r) {
+    const i64 lim = tr - c->Wns;
+    while (rf_len) {
+      RPEnt g = s.rf[rf_head];
+      if (g.t > lim) break;
+      s.us[g.user].r_len--; s.rapp[g.app]--;
+      rf_head = rf_head + 1 == s.rf_cap ? 0 : rf_head + 1;
+      rf_len--;
+    }
+    if (rf_len == s.rf_cap) { err_code = ERR_NOMEM; err_idx = r; return -1; }
+    u32 idx = rf_head + rf_len; if (idx >= s.rf_cap) idx -= s.rf_cap;
+    RPEnt g; g.t = tr; g.user = k; g.app = app;
+    s.rf[idx] = g;
+    rf_len++;
+    u32 nu = ++us.r_len, na = ++s.rapp[app];
+    if (c->L.rg && nu > c->L.rg) return FS_ST_BLOCK_USER_REQ;
+    if (c->ra[app] && na > c->ra[app]) return FS_ST_BLOCK_APP_REQ;
+    return FS_ST_ADMIT;
+  }
+
   // lift (l.12-18); returns whether the user was queued
   __device__ __forceinline__ bool lift(UState& us) {
     if (us.qh_cnt + us.qc_cnt != 0) return true;
@@ -303,6 +332,9 @@ struct EngineT {
     if (c->mode == FS_MODE_WI) {
       if (!static_heads && !ring_push(us, k, tr, h.B.y + h.B.w, m_app(m), r)) return -1;   // l.19
       if (ovl) st = act_check(us, k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);                 // l.20-24
+    } else if (BASE && c->mode == FS_MODE_RPM) {
+      st = rpm_check(us, k, m_app(m), tr, r);
+      if (st < 0) return -1;
     }
     digest = sm64(digest ^ ((u64)r * 16 + (u64)st));
     us.qh_next = upos + 1;
@@ -317,11 +349,15 @@ struct EngineT {
       if (o.status) o.status[r] = (uint8_t)st;
       return st;
     }
-    if (us.qh_cnt == 0) { us.qh_front = upos; us.hf = r; }
+    const bool dq = BASE && c->mode >= FS_MODE_VTC;         // users' calls in delivery order (R7)
+    if (dq) s.hseq[upos] = seq;
+    if (us.qh_cnt == 0) { us.qh_front = upos; us.hf = r; if (dq) us.hs = seq; }
     us.qh_cnt++;
-    seq++;
-    if (!was) {                                             // newly queued: class 1, front = this head
-      us.u |= CLS_BIT; us.tie = r; us.nf = h.B.y + h.B.w;
+    u32 myseq = seq++;
+    if (!was) {                                             // newly queued, front = this head
+      if (dq) us.tie = myseq;                               //   VTC / RPM / FCFS: no class
+      else { us.u |= CLS_BIT; us.tie = r; }                 //   FS: class 1
+      us.nf = h.B.y + h.B.w;
       newly_queued(us, k);
     }
     return FS_ST_ADMIT;
@@ -334,12 +370,23 @@ struct EngineT {
       uint4 B = ldg4(&sh->recB[r]);
       if (!ring_push(us, k, tr, B.y + B.w, m_app(m), r)) return -1;
     }
+    if (BASE && c->mode == FS_MODE_RPM) {                   // RPM throttles continuations too (R8)
+      int st = rpm_check(us, k, m_app(m), tr, r);
+      if (st < 0) return -1;
+      if (st != FS_ST_ADMIT) {                              // the interaction is aborted midway
+        digest = sm64(digest ^ ((u64)r * 16 + (u64)st));
+        if (st == FS_ST_BLOCK_USER_REQ) sum.n_block[0]++; else sum.n_block[2]++;
+        sum.n_dropped += m_ncalls(m) - m_stage(m);
+        if (o.status) o.status[r] = (uint8_t)st;
+        return st;
+      }
+    }
     digest = sm64(digest ^ ((u64)r * 16));
     if (c_top == 0) { err_code = ERR_NOMEM; err_idx = r; return -1; }   // pool capacity (R5)
     u32 x = s.cfree[--c_top];
     CSlot cs; cs.r = r; cs.next = NONE32; cs.nseq = 0; cs.nr = NONE32; cs.t = tr;
     s.cs[x] = cs;
-    if (us.qc_cnt == 0) { us.qc_head = x; us.cf = r; }
+    if (us.qc_cnt == 0) { us.qc_head = x; us.cf = r; if (BASE) us.cs = seq; }
     else { CSlot& tl = s.cs[us.qc_tail]; tl.next = x; tl.nseq = seq; tl.nr = r; }
     us.qc_tail = x;
     us.qc_cnt++;
@@ -347,7 +394,7 @@ struct EngineT {
     if (!was) {                                             // newly queued: class 0
       us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
       newly_queued(us, k);
-    } else if (us.qc_cnt == 1) {                            // class 1 -> 0: key decreased
+    } else if ((!BASE || c->mode <= FS_MODE_WI) && us.qc_cnt == 1) {   // FS: class 1 -> 0, key decreased
       pick_blocked = false;
       us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
       HK x; x.key = us.u; x.tie = myseq; x.user = k;
@@ -365,7 +412,8 @@ struct EngineT {
     UState& us = s.us[k];
     u32 nfk = us.nf;                                         // cached need of the front: a failing
     if (nfk != NONE32 && (u64)occ_now + nfk > C) return false;      // candidate costs no global load
-    bool cont = us.qc_cnt != 0;
+    const bool dq = BASE && c->mode >= FS_MODE_VTC;
+    bool cont = us.qc_cnt != 0 && (!dq || us.qh_cnt == 0 || us.cs < us.hs);   // l.31-35 | R7
     u32 x = cont ? us.qc_head : 0;
     CSlot cs;
     if (cont) cs = s.cs[x];
@@ -379,6 +427,7 @@ struct EngineT {
     if (cont) {
       a->arr = cs.t;
       us.qc_head = cs.next; nseq = cs.nseq; us.cf = cs.nr;
+      if (dq) us.cs = nseq;
       us.qc_cnt--;
       s.cfree[c_top++] = x;                                  // slot back to the pool
     } else {
@@ -392,6 +441,7 @@ struct EngineT {
           f++;
         }
         us.qh_front = f;
+        if (dq) us.hs = s.hseq[f];
       } else us.qh_front = us.qh_next;
     }
     if (us.qh_cnt + us.qc_cnt == 0) {                        // user leaves Q: e <- k
@@ -400,7 +450,8 @@ struct EngineT {
       us.u &= ~CLS_BIT;
       e = k;
     } else {                                                 // front changed: key increased
-      if (us.qc_cnt) { us.u &= ~CLS_BIT; us.tie = nseq; } else { us.u |= CLS_BIT; us.tie = us.hf; }
+      if (dq) us.tie = (us.qc_cnt && (us.qh_cnt == 0 || us.cs < us.hs)) ? us.cs : us.hs;
+      else if (us.qc_cnt) { us.u &= ~CLS_BIT; us.tie = nseq; } else { us.u |= CLS_BIT; us.tie = us.hf; }
       us.nf = NONE32;
       HK x; x.key = us.u; x.tie = us.tie; x.user = k;
       hk_down(0, x);
@@ -748,17 +799,20 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
 }
 
 // ------------------------------------------------------------------ state layout
+enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_HPOS, L_CS, L_CF, L_BLK, L_RT, L_HSEQ, L_RF,
+       L_RAPP, L_N };
 struct EngLayout {
   size_t bytes_smem = 0, bytes_glob = 0;
-  size_t off[16];
-  bool smem[16];
+  size_t off[L_N];
+  bool smem[L_N];
   u32 c_cap = 0;                        // continuation-slot pool capacity
+  u32 rf_cap = 0, A = 0;                // RPM window log capacity, apps
 };
-enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_HPOS, L_CS, L_CF, L_BLK, L_RT, L_N };
 
 // slots: capacity of the pool of queued-continuation slots (R5)
+// hseq: per-head delivery seqs (VTC / RPM / FCFS); rf_cap > 0: the RPM window log + per-app counts
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
-                            bool hring, size_t smem_budget) {
+                            bool hring, size_t smem_budget, bool hseq = false, u32 rf_cap = 0, u32 A = 0) {
   size_t sz[L_N];
   sz[L_HR] = hring ? (size_t)HRING * (sizeof(HEnt) + 8) + 64 : 0;
   sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
@@ -769,10 +823,14 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   size_t ring = act_ring ? (size_t)ring_slots + 1 : 0;
   sz[L_RT] = ring * sizeof(REnt);
   sz[L_HPOS] = (size_t)U * sizeof(uint2);
+  sz[L_HSEQ] = hseq ? (size_t)(n_heads + 1) * 4 : 0;
+  sz[L_RF] = (size_t)rf_cap * sizeof(RPEnt);
+  sz[L_RAPP] = rf_cap ? (size_t)A * 4 : 0;
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_US, L_HK, L_HM, L_CS, L_CF};
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_RAPP, L_US, L_HK, L_HM, L_CS, L_CF};
   EngLayout L;
   L.c_cap = (u32)slots;
+  L.rf_cap = rf_cap; L.A = A;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
     size_t b = (sz[k] + 15) / 16 * 16;
@@ -792,6 +850,7 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
   s->p = (PEnt*)P(L_P); s->p_cap = p_cap; s->W = (u64*)P(L_W);
   s->blocked = (u32*)P(L_BLK);
   s->r = (REnt*)P(L_RT); s->hpos = (uint2*)P(L_HPOS);
+  s->hseq = (u32*)P(L_HSEQ); s->rf = (RPEnt*)P(L_RF); s->rf_cap = L.rf_cap; s->rapp = (u32*)P(L_RAPP);
   if (hr) {
     unsigned char* base = (unsigned char*)P(L_HR);
     hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
@@ -812,6 +871,7 @@ __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u
     s.us[k] = z;
   }
   for (u64 w = lane; w < sh.n_heads / 32 + 2; w += nl) s.blocked[w] = 0;
+  if (s.rf_cap) for (u32 a = lane; a < sh.A; a += nl) s.rapp[a] = 0;
   for (u32 k = lane; k < s.c_cap; k += nl) s.cfree[k] = s.c_cap - 1 - k;   // pops hand out 0, 1, 2, ...
   if (s.W != W) for (u64 k = lane; k < AJ; k += nl) s.W[k] = W[k];
 }
@@ -823,6 +883,7 @@ struct ReplayKArgs {
 
 // single replay: one CTA of two warps -- warp 0 lane 0 runs the serial engine,
 // warp 1 streams head arrivals into the shared ring
+template <bool BASE>
 __global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   EngState st;
@@ -838,7 +899,7 @@ __global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
     return;
   }
   if (threadIdx.x != 0) return;
-  EngineT<HS_RING> E;
+  EngineT<HS_RING, 32, BASE> E;
   E.init(&a.sh, &a.cfg, st, a.out, a.U);
   E.ring = hr;
   E.run();
@@ -856,11 +917,11 @@ struct SweepKArgs {
 // One scenario slot per group of LPS lanes.  Every lane of a group runs the (group-uniform)
 // engine: loads and stores of the replicated state are broadcast / merged, and head batch
 // refills use all LPS lanes.
-template <int MINB, int LPS>              // MINB CTAs per SM: caps registers (occupancy vs spills)
+template <int MINB, int LPS, bool BASE>  // MINB CTAs per SM: caps registers (occupancy vs spills)
 __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
   __shared__ HEnt hbs[128];
   const u32 lane = threadIdx.x & 31, sub = threadIdx.x & (LPS - 1), lead = lane & ~(u32)(LPS - 1);
-  const u32 gm = EngineT<HS_WARP, LPS>::group_mask();
+  const u32 gm = EngineT<HS_WARP, LPS, BASE>::group_mask();
   u32 slot = (blockIdx.x * blockDim.x + threadIdx.x) / LPS;
   unsigned char* g = a.gmem + (size_t)slot * a.slot_bytes;
   EngState st0;
@@ -879,7 +940,7 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
     __syncwarp(gm);
     __threadfence_block();
     {
-      EngineT<HS_WARP, LPS> E;
+      EngineT<HS_WARP, LPS, BASE> E;
       E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
       E.hb = &hbs[threadIdx.x & ~(u32)(LPS - 1)];
       E.run();

@@ -380,3 +380,64 @@ def test_error_parity(F, ctx):
     with pytest.raises(F.FsError) as e2:
         F.wsc_replay(ctx, T(tr), gp, cfg)
     assert (e2.value.code, e2.value.bad_index) == (e1.value.code, e1.value.bad_index)
+
+
+# ------------------------------------------------------------------ NEXT-1 baselines (VTC, RPM, FCFS)
+@pytest.mark.parametrize("seed", range(120))
+def test_replay_tiny_baselines(F, ctx, seed):
+    rng = np.random.default_rng(9000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(1, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    cmp_replay(F, ctx, tr, gp, op, tiny_replay_cfg(rng, A, modes=(2, 3, 4)), f"base{seed}")
+
+
+@pytest.mark.parametrize("mode", [2, 3, 4])
+def test_replay_c2_shape_baselines(F, ctx, mode):
+    """C2-shaped 100k-call trace: VTC (weights 1, 1, 2), RPM (user and app request limits), FCFS."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=200, n_calls=100_000, seed=51))
+    pcfg = dict(tier_max=0)
+    op = O.profile(tr, pcfg)
+    gp = F.build_app_profiles(ctx, F.Trace(tr), pcfg)
+    cfg = dict(G.CONFIGS["c2"]["engine"], mode=mode, tier_max=255, alpha=1, beta=1, gamma=2,
+               act=dict(window_ms=60000, limits_from_profile=0, T_req_g=6,
+                        T_req_a=[40] * tr["n_apps"]))
+    cmp_replay(F, ctx, tr, gp, op, cfg, f"c2base{mode}")
+
+
+def test_sweep_baselines(F, ctx):
+    """One sweep mixing FS(W+I), FS(W), VTC, RPM and FCFS scenarios over tier mixes."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=100, n_calls=20_000, seed=61))
+    op = O.profile(tr, dict(tier_max=0))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=0))
+    base = dict(G.CONFIGS["c2"]["engine"], act=dict(window_ms=60000, limits_from_profile=0, T_req_g=4,
+                                                   T_req_a=[30] * tr["n_apps"]))
+    scen = []
+    for mode, tm in [(2, 15), (3, 15), (4, 15), (2, 0), (3, 3), (4, 7), (0, 15)]:
+        scen.append(dict(base, mode=mode, tier_max=tm, alpha=1, beta=1, gamma=2))
+    scen.append(dict(base, mode=1, act=dict(window_ms=60000, limits_from_profile=1)))
+    es, ecodes = O.sweep(tr, op, scen)
+    gs, gcodes = F.sweep(ctx, F.Trace(tr), gp, scen)
+    assert list(gcodes) == list(ecodes)
+    for a, b in zip(gs, es):
+        assert a == b
+
+
+def test_rpm_profile_limits_rejected(F, ctx):
+    """R8: RPM takes explicit limits; profile-derived ones are FS_E_INVAL on both sides, and the
+    online step rejects RPM."""
+    tr = G.generate("c1")
+    op = O.profile(tr, dict(tier_max=255))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=255))
+    cfg = dict(G.CONFIGS["c1"]["engine"], mode=3, act=dict(window_ms=60000, limits_from_profile=1))
+    with pytest.raises(O.OracleError) as eo:
+        O.replay(tr, op, cfg)
+    with pytest.raises(F.FsError) as eg:
+        F.wsc_replay(ctx, F.Trace(tr), gp, cfg)
+    assert eo.value.code == eg.value.code == -1
+    cfg["act"] = dict(window_ms=60000, limits_from_profile=0, T_req_g=3)
+    with pytest.raises(F.FsError) as eg:
+        F.WscState(ctx, F.Trace(tr), gp, cfg)
+    assert eg.value.code == -1
