@@ -230,6 +230,31 @@ void fs_wsc_state_free(fs_wsc_state* st);
 int fs_sweep(fs_ctx* ctx, const fs_trace* trace, const fs_profile* profile, const fs_replay_cfg* scen_h,
              uint32_t n_scen, fs_replay_summary* out_h, int32_t* codes_h);
 
+/* ------------------------------------------------------------------ §5 metrics (NEXT-2)
+ * fs_replay_metrics: the paper's evaluation quantities (
+ * DESIGN.md R9) over one completed fs_wsc_replay's per-call outputs (DEVICE arrays of
+ * n_calls: status, arrive_ns, admit_ns, first_ns).  Participating = status != FILTERED;
+ * served = ADMIT; an interaction is completed / blocked at its head / aborted midway (head
+ * served, a later call blocked); wasted tokens = L_I + L_S + L_O of the served calls of
+ * aborted interactions; TTFT = first - arrival of served calls, p50 / p99 by nearest rank;
+ * users with feedback = with a participating interaction, served = with a completed one,
+ * delayed = with a served call whose admit - arrival > delay_threshold_ns; Jain's index
+ * (sum x)^2 / (n sum x^2) over the per-user served tokens of users with feedback (0 if all
+ * are 0).  global_h: host, 1 entry; per_app_h: host, n_apps entries (NULL = skip), each
+ * restricted to that app's calls, interactions and users.  Integer-exact; jain in double.
+ * Errors: FS_E_INVAL (null pointers, TTFT >= 2^56 ns), FS_E_NOMEM, FS_E_CUDA. */
+typedef struct {
+  uint64_t requests_total, requests_served, requests_blocked, requests_dropped;
+  uint64_t interactions_total, interactions_completed, interactions_blocked_at_head, interactions_aborted_midway;
+  uint64_t wasted_tokens, prompt_tokens, decode_tokens, abuser_tokens;
+  uint64_t users_feedback, users_served, users_delayed;
+  uint64_t ttft_n, ttft_sum_ns, ttft_p50_ns, ttft_p99_ns;
+  double jain;
+} fs_metrics;
+int fs_replay_metrics(fs_ctx* ctx, const fs_trace* trace, const uint8_t* status, const int64_t* arrive_ns,
+                      const int64_t* admit_ns, const int64_t* first_ns, int64_t delay_threshold_ns,
+                      fs_metrics* global_h, fs_metrics* per_app_h);
+
 #ifdef __cplusplus
 }
 #endif

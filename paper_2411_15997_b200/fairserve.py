@@ -55,6 +55,7 @@ def lib():
             "fs_wsc_step": [V, V, I64, I64, U32, V, U32, V, V, U32, V, V, PU32],
             "fs_wsc_state_read": [V, V, V, PI32], "fs_wsc_state_free": [V],
             "fs_sweep": [V, V, V, V, U32, V, V],
+            "fs_replay_metrics": [V, V, V, V, V, V, I64, V, V],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -424,6 +425,34 @@ def sweep(ctx, trace, profile, scenarios):
     codes = np.zeros(len(scenarios), np.int32)
     ctx._check(lib().fs_sweep(ctx.h, _a(trace.c), profile.h, _a(arr), len(scenarios), _a(outs), _hp(codes)))
     return [_summary(s) for s in outs], codes
+
+
+METRIC_FIELDS = ["requests_total", "requests_served", "requests_blocked", "requests_dropped",
+                 "interactions_total", "interactions_completed", "interactions_blocked_at_head",
+                 "interactions_aborted_midway", "wasted_tokens", "prompt_tokens", "decode_tokens", "abuser_tokens",
+                 "users_feedback", "users_served", "users_delayed", "ttft_n", "ttft_sum_ns", "ttft_p50_ns",
+                 "ttft_p99_ns"]
+
+
+class _Metrics(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in METRIC_FIELDS] + [("jain", C.c_double)]
+
+
+def _metrics(m):
+    d = {k: int(getattr(m, k)) for k in METRIC_FIELDS}
+    d["jain"] = float(m.jain)
+    return d
+
+
+def replay_metrics(ctx, trace, out, delay_threshold_ns):
+    """§5 metric suite (fs_replay_metrics) over fs_wsc_replay outputs (device tensors);
+    returns (global dict, list of per-app dicts)."""
+    g = _Metrics()
+    per = (_Metrics * trace.A)()
+    ctx._check(lib().fs_replay_metrics(ctx.h, _a(trace.c), _dp(out["status"]), _dp(out["arrive_ns"]),
+                                       _dp(out["admit_ns"]), _dp(out["first_ns"]), C.c_int64(delay_threshold_ns),
+                                       _a(g), _a(per)))
+    return _metrics(g), [_metrics(m) for m in per]
 
 
 def to_np(t, dtype):

@@ -441,3 +441,49 @@ def test_rpm_profile_limits_rejected(F, ctx):
     with pytest.raises(F.FsError) as eg:
         F.WscState(ctx, F.Trace(tr), gp, cfg)
     assert eg.value.code == -1
+
+
+# ------------------------------------------------------------------ NEXT-2 metric suite
+def _cmp_metrics(F, ctx, tr, gout, eout, thr, name):
+    from oracle import metrics as M
+    g, per = F.replay_metrics(ctx, F.Trace(tr), gout, thr)
+    eg, eper = M.replay_metrics(tr, eout, thr)
+    for a, b in [(g, eg)] + list(zip(per, eper)):
+        for k in M.FIELDS:
+            if k == "jain":
+                assert a[k] == pytest.approx(b[k], rel=1e-12, abs=0), (name, k)
+            else:
+                assert a[k] == b[k], (name, k, a[k], b[k])
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
+def test_metrics_c2_shape(F, ctx, mode):
+    """fs_replay_metrics vs oracle/metrics.py on the outputs of each policy's replay."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=200, n_calls=30_000, seed=83))
+    pcfg = dict(tier_max=255)
+    op = O.profile(tr, pcfg)
+    gp = F.build_app_profiles(ctx, F.Trace(tr), pcfg)
+    act = dict(window_ms=60000, limits_from_profile=1) if mode == 1 else \
+        dict(window_ms=60000, limits_from_profile=0, T_req_g=4, T_req_a=[30] * tr["n_apps"])
+    cfg = dict(G.CONFIGS["c2"]["engine"], mode=mode, tier_max=255, act=act)
+    go, _ = F.wsc_replay(ctx, F.Trace(tr), gp, cfg)
+    eo, _ = O.replay(tr, op, cfg)
+    for thr in (0, 5_000_000, 10**12):
+        _cmp_metrics(F, ctx, tr, go, eo, thr, f"m{mode}-{thr}")
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_metrics_tiny(F, ctx, seed):
+    rng = np.random.default_rng(4400 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=3, n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A, modes=(0, 1, 2, 3, 4))
+    try:
+        eo, _ = O.replay(tr, op, cfg)
+    except O.OracleError:
+        return
+    go, _ = F.wsc_replay(ctx, F.Trace(tr), gp, cfg)
+    _cmp_metrics(F, ctx, tr, go, eo, int(rng.choice((0, 1_000_000, 10**9))), f"tiny{seed}")
