@@ -498,13 +498,13 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   static const int minb = [] { const char* v = getenv("FS_SWEEP_MINB"); return v ? atoi(v) : 4; }();
   static const int lps = [] { const char* v = getenv("FS_SWEEP_LPS"); return v ? atoi(v) : 32; }();
   // scenarios of the FairServe modes only: the engine without the baseline-mode paths
-  auto kern = any_dq ? (lps <= 8 ? (minb >= 4 ? k_sweep<4, 8, true> : k_sweep<3, 8, true>) :
-                        lps == 16 ? (minb >= 4 ? k_sweep<4, 16, true> : k_sweep<3, 16, true>) :
-                                    (minb >= 4 ? k_sweep<4, 32, true> : k_sweep<3, 32, true>))
-                     : (lps <= 8 ? (minb >= 4 ? k_sweep<4, 8, false> : k_sweep<3, 8, false>) :
-                        lps == 16 ? (minb >= 4 ? k_sweep<4, 16, false> : k_sweep<3, 16, false>) :
-                                    (minb >= 4 ? k_sweep<4, 32, false> : k_sweep<3, 32, false>));
-  const u32 per_cta = 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
+  // (FS_SWEEP_LPS = 16 / 8, several replays per warp, measured slower: FS-mode engine only)
+  auto kern = any_dq ? (minb >= 6 ? k_sweep<6, 32, true> : minb == 5 ? k_sweep<5, 32, true> :
+                        minb == 4 ? k_sweep<4, 32, true> : k_sweep<3, 32, true>)
+            : lps <= 8 ? k_sweep<4, 8, false> : lps == 16 ? k_sweep<4, 16, false>
+            : (minb >= 6 ? k_sweep<6, 32, false> : minb == 5 ? k_sweep<5, 32, false> :
+               minb == 4 ? k_sweep<4, 32, false> : k_sweep<3, 32, false>);
+  const u32 per_cta = any_dq ? 4 : 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
   // the replays' state lives in global memory: give L1 every byte shared memory does not need
   static const int carve = [] { const char* v = getenv("FS_SWEEP_CARVE"); return v ? atoi(v) : -1; }();
   if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
@@ -516,7 +516,23 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   slots = (slots + per_cta - 1) / per_cta * per_cta;   // whole CTAs
   unsigned char* gm = S.alloc<unsigned char>(slots * slot_bytes + 256);
   if (S.failed) return FS_E_NOMEM;
-  SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next};
+  // longest-processing-time order: scenarios with the most participating calls start first, so
+  // the last wave holds the short ones (the cost of a replay grows with its calls)
+  std::vector<unsigned long long> htc(256);
+  cudaMemcpyAsync(htc.data(), W.tier_calls, 256 * 8, cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) return rc;
+  std::vector<u64> cum(257, 0);
+  for (int k = 0; k < 256; k++) cum[k + 1] = cum[k] + htc[k];
+  std::vector<u32> ord(ns);
+  for (u32 s = 0; s < ns; s++) ord[s] = s;
+  std::stable_sort(ord.begin(), ord.end(), [&](u32 x, u32 y) {
+    return cum[std::min<u32>(scen[x].tier_max, 255) + 1] > cum[std::min<u32>(scen[y].tier_max, 255) + 1];
+  });
+  u32* dord = S.alloc<u32>(ns);
+  if (S.failed) return FS_E_NOMEM;
+  cudaMemcpyAsync(dord, ord.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream);
+  SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next, dord};
   FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / per_cta), 128, 0, a);
   std::vector<int> hcodes(ns);
   cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);

@@ -1,6 +1,7 @@
 // fairserve.cu -- the C ABI (include/fairserve.h): context, error handling and the
 // host orchestration of the kernels in *.cuh.  Every step of the path runs in those
 // kernels; host code here only sizes buffers, launches and reads back status words.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>

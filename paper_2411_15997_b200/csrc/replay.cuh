@@ -913,6 +913,7 @@ __global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
 struct SweepKArgs {
   EngShared sh; const EngCfg* cfgs; u32 n_scen; EngLayout L; u32 U; unsigned char* gmem; size_t slot_bytes;
   u32 p_cap; fs_replay_summary* sums; int* codes; u32* next;
+  const u32* order;                       // queue order of the scenarios (host LPT by participating calls)
 };
 // One scenario slot per group of LPS lanes.  Every lane of a group runs the (group-uniform)
 // engine: loads and stores of the replicated state are broadcast / merged, and head batch
@@ -930,10 +931,11 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
   memset(&none, 0, sizeof(none));
   u64 AJ = (u64)a.sh.A * a.sh.J1;
   for (;;) {
-    u32 sc = 0;
-    if (sub == 0) sc = atomicAdd(a.next, 1u);
-    sc = __shfl_sync(gm, sc, lead);
-    if (sc >= a.n_scen) return;
+    u32 q = 0;
+    if (sub == 0) q = atomicAdd(a.next, 1u);
+    q = __shfl_sync(gm, q, lead);
+    if (q >= a.n_scen) return;
+    const u32 sc = a.order ? a.order[q] : q;   // longest scenarios first
     EngState st = st0;
     st.W = (u64*)a.cfgs[sc].W;
     eng_clear(st, a.sh, a.cfgs[sc].W, AJ, a.U, sub, LPS);
