@@ -884,7 +884,7 @@ struct ReplayKArgs {
 // single replay: one CTA of two warps -- warp 0 lane 0 runs the serial engine,
 // warp 1 streams head arrivals into the shared ring
 template <bool BASE>
-__global__ void __launch_bounds__(64) k_replay(ReplayKArgs a) {
+__global__ void __launch_bounds__(64) k_replay(const __grid_constant__ ReplayKArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   EngState st;
   HeadRing hr;
@@ -919,7 +919,7 @@ struct SweepKArgs {
 // engine: loads and stores of the replicated state are broadcast / merged, and head batch
 // refills use all LPS lanes.
 template <int MINB, int LPS, bool BASE>  // MINB CTAs per SM: caps registers (occupancy vs spills)
-__global__ void __launch_bounds__(128, MINB) k_sweep(SweepKArgs a) {
+__global__ void __launch_bounds__(128, MINB) k_sweep(const __grid_constant__ SweepKArgs a) {
   __shared__ HEnt hbs[128];
   const u32 lane = threadIdx.x & 31, sub = threadIdx.x & (LPS - 1), lead = lane & ~(u32)(LPS - 1);
   const u32 gm = EngineT<HS_WARP, LPS, BASE>::group_mask();
@@ -963,7 +963,7 @@ struct StepKArgs {
   const u32* fin; u32 nfin; const u32* arr; const i64* arr_t; u32 narr;
   uint8_t* arr_status; u32* admitted; u32* n_admitted; int* err_code; u64* err_idx;
 };
-__global__ void k_step(StepKArgs a) {
+__global__ void k_step(const __grid_constant__ StepKArgs a) {
   if (threadIdx.x != 0) return;
   EngState st;
   eng_bind(a.L, nullptr, a.gmem, a.p_cap, &st, nullptr);
