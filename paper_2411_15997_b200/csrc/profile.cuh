@@ -111,17 +111,26 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   const u64 n = a.t.n;
   // one call: shared-memory atomics straight into the CTA's private sums and bins (integer adds
   // commute, so the result is order-independent); same-address lanes are merged by the hardware
+  const int lane = threadIdx.x & 31;
+  // one call: few hot (app, stage') keys, so the sums take one warp-aggregated shared atomic
+  // per key (__match_any_sync); histogram bins take one shared atomic per call (measured
+  // faster than matching every field: 275 vs 416 / 438 us at C3)
   auto one = [&](bool ok, u32 m, u32 Li, u32 Ls, u32 Lo) {
-    if (!ok || m_tier(m) > a.tier_max) return;
+    ok = ok && m_tier(m) <= a.tier_max;
     u32 app = m_app(m), st = m_stage(m);
     if (do_sums) {
-      u32 key = app * J1 + min(st, a.J);
-      atomicAdd((unsigned long long*)&ssum[key], 1ull);
-      atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)Li);
-      atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)Ls);
-      atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)Lo);
+      u32 key = ok ? app * J1 + min(st, a.J) : 0xFFFFFFFFu;
+      u32 peers = __match_any_sync(FULL_MASK, key);
+      u32 ri = __reduce_add_sync(peers, ok ? Li : 0u), rs = __reduce_add_sync(peers, ok ? Ls : 0u);
+      u32 ro = __reduce_add_sync(peers, ok ? Lo : 0u);
+      if (ok && lane == (int)(__ffs(peers) - 1)) {
+        atomicAdd((unsigned long long*)&ssum[key], (unsigned long long)__popc(peers));
+        atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)ri);
+        atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)rs);
+        atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)ro);
+      }
     }
-    if (app < a0 || app >= a0 + na) return;
+    if (!ok || app < a0 || app >= a0 + na) return;
     u32* hb = shist + (app - a0) * NF * NBINS;
     atomicAdd(&hb[loglin_bin(Li)], 1u);
     atomicAdd(&hb[NBINS + loglin_bin(Ls)], 1u);
