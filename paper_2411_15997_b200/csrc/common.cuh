@@ -194,6 +194,18 @@ void excl_scan(fs_ctx* ctx, Scratch& S, const T* in, T* out, u64 n, T* total_dev
 // digit-major scan, stable scatter with __match_any_sync warp ranking.
 static const int RS_T = 256, RS_R = 16, RS_TILE = RS_T * RS_R;
 
+// lanes of the warp holding the same 8-bit digit (ok lanes only): bit-sliced ballots,
+// cheaper than __match_any_sync
+__device__ __forceinline__ u32 digit_peers(u32 d, bool ok) {
+  u32 peers = __ballot_sync(FULL_MASK, ok);
+#pragma unroll
+  for (int b = 0; b < 8; b++) {
+    u32 bb = __ballot_sync(FULL_MASK, (d >> b) & 1u);
+    peers &= ((d >> b) & 1u) ? bb : ~bb;
+  }
+  return peers;
+}
+
 template <class K>
 __global__ void k_radix_hist(const K* keys, u64 n, int shift, u32* tile_hist, int ntiles) {
   __shared__ u32 h[256];
@@ -203,9 +215,10 @@ __global__ void k_radix_hist(const K* keys, u64 n, int shift, u32* tile_hist, in
 #pragma unroll 4
   for (int r = 0; r < RS_R; r++) {
     u64 i = base + (u64)r * RS_T + threadIdx.x;
-    u32 d = i < n ? (u32)((keys[i] >> shift) & 255) : 256u;
-    u32 peers = __match_any_sync(FULL_MASK, d);
-    if (d < 256 && (threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) atomicAdd(&h[d], (u32)__popc(peers));
+    bool ok = i < n;
+    u32 d = ok ? (u32)((keys[i] >> shift) & 255) : 0u;
+    u32 peers = digit_peers(d, ok);
+    if (ok && (threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) atomicAdd(&h[d], (u32)__popc(peers));
   }
   __syncthreads();
   tile_hist[(u64)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
@@ -238,14 +251,25 @@ __global__ void k_radix_scan_digits(u32* dtot) {   // 256 threads, exclusive in 
   dtot[threadIdx.x] = ex;
 }
 
+// Stable scatter, staged through shared memory: ranks give every item its place in the tile
+// sorted by digit (digit start in the tile + earlier warps' count + rank within the warp);
+// the tile is written there, then read back in order so that consecutive threads store
+// consecutive addresses of each digit's run (coalesced instead of one sector per item).
 template <class K>
 __global__ void __launch_bounds__(RS_T) k_radix_scatter(const K* kin, const u32* vin, K* kout, u32* vout, u64 n,
                                                         int shift, const u32* tile_off, const u32* dbase, int ntiles) {
   __shared__ u32 wcnt[8][257];
+  __shared__ u32 dstart[256], gbase[256];
+  __shared__ u32 sh_scan[32];
+  __shared__ unsigned long long sbuf[RS_TILE];     // keys, then values (two phases: fits 48 KB with u64 keys)
+  __shared__ uint8_t sdig[RS_TILE];
+  K* skey = (K*)sbuf;
+  u32* sval = (u32*)sbuf;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 8 * 257; i += RS_T) (&wcnt[0][0])[i] = 0;
   __syncthreads();
-  u64 base = (u64)blockIdx.x * RS_TILE + (u64)w * (RS_R * 32);
+  const u64 tile0 = (u64)blockIdx.x * RS_TILE;
+  u64 base = tile0 + (u64)w * (RS_R * 32);
   K key[RS_R];
   u32 val[RS_R], rank[RS_R];
   u32 lt = lanemask_lt();
@@ -256,7 +280,9 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter(const K* kin, const u32*
     key[r] = ok ? kin[i] : (K)0;
     val[r] = ok ? (vin ? vin[i] : (u32)i) : 0u;
     u32 d = ok ? (u32)((key[r] >> shift) & 255) : 256u;
-    u32 peers = __match_any_sync(FULL_MASK, d);
+    u32 vm = __ballot_sync(FULL_MASK, ok);
+    u32 peers = digit_peers(d & 255u, ok);
+    if (!ok) peers = ~vm;                              // tail lanes: one group of their own (digit 256)
     u32 pre = wcnt[w][d];
     __syncwarp();
     rank[r] = pre + __popc(peers & lt);
@@ -264,10 +290,13 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter(const K* kin, const u32*
     __syncwarp();
   }
   __syncthreads();
-  {
+  {                                                    // per digit: warp offsets, tile count
     u32 d = threadIdx.x, s = 0;
 #pragma unroll
     for (int ww = 0; ww < 8; ww++) { u32 c = wcnt[ww][d]; wcnt[ww][d] = s; s += c; }
+    u32 ex = block_excl_scan<u32>(s, sh_scan, nullptr);   // digit start inside the tile
+    dstart[d] = ex;
+    gbase[d] = dbase[d] + tile_off[(u64)d * ntiles + blockIdx.x];
   }
   __syncthreads();
 #pragma unroll
@@ -275,10 +304,28 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter(const K* kin, const u32*
     u64 i = base + (u64)r * 32 + lane;
     if (i < n) {
       u32 d = (u32)((key[r] >> shift) & 255);
-      u64 pos = (u64)dbase[d] + tile_off[(u64)d * ntiles + blockIdx.x] + wcnt[w][d] + rank[r];
-      kout[pos] = key[r];
-      vout[pos] = val[r];
+      u32 lp = dstart[d] + wcnt[w][d] + rank[r];
+      skey[lp] = key[r];
+      sdig[lp] = (uint8_t)d;
+      rank[r] = lp;
     }
+  }
+  __syncthreads();
+  const u32 cnt = n - tile0 < (u64)RS_TILE ? (u32)(n - tile0) : (u32)RS_TILE;
+  for (u32 j = threadIdx.x; j < cnt; j += RS_T) {
+    u32 d = sdig[j];
+    kout[(u64)gbase[d] + (j - dstart[d])] = skey[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < RS_R; r++) {
+    u64 i = base + (u64)r * 32 + lane;
+    if (i < n) sval[rank[r]] = val[r];
+  }
+  __syncthreads();
+  for (u32 j = threadIdx.x; j < cnt; j += RS_T) {
+    u32 d = sdig[j];
+    vout[(u64)gbase[d] + (j - dstart[d])] = sval[j];
   }
 }
 
