@@ -189,10 +189,10 @@ void excl_scan(fs_ctx* ctx, Scratch& S, const T* in, T* out, u64 n, T* total_dev
 }
 
 // ------------------------------------------------------------------ stable LSD radix sort
-// 8-bit digits, tiles of 4096 items (8 warps x 16 rounds x 32 lanes, tile order =
+// 8-bit digits, tiles of 2048 items (8 warps x 8 rounds x 32 lanes, tile order =
 // warp, round, lane so ranks preserve input order).  Per pass: tile digit histograms,
 // digit-major scan, stable scatter with __match_any_sync warp ranking.
-static const int RS_T = 256, RS_R = 16, RS_TILE = RS_T * RS_R;
+static const int RS_T = 256, RS_R = 8, RS_TILE = RS_T * RS_R;
 
 // lanes of the warp holding the same 8-bit digit (ok lanes only): bit-sliced ballots,
 // cheaper than __match_any_sync
