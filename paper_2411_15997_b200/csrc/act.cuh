@@ -187,101 +187,102 @@ __global__ void k_act_decide(ActDecideArgs a) {
   if (st != a.status[i]) { a.status[i] = st; *a.changed = 1; a.user_changed[a.user[i]] = 1; }
 }
 
-// ------------------------------------------------------------------ sequential fix-up (exact)
-// One warp per user whose decisions still changed in the last Jacobi pass: the warp
-// walks the user's calls in (t, id) order in lock-step (every lane computes the same
-// thing from values broadcast with shuffles), recomputing counted flags, window counts
-// and decisions from scratch -- the sequential definition itself.  Prefix values of
-// the recent positions live in a per-warp shared ring; older ones in the pass's global
-// prefix arrays, which the walk overwrites for its user.
-static const int WALK_R = 256;
-struct WalkRing { u32 cu, ca; u64 tu, ta; u32 st, pad; };
-struct ActWalkArgs {
-  const u32* users; u32 n_users_walk; const u64* seg_u;
-  const u32* perm_u; const u32* perm_ua; const u32* pos_ua; const u32* pos_u;
-  const u64* lb_u; const u64* lb_ua; const i64* ts_u;
+// ------------------------------------------------------------------ per-user Jacobi to the fixed point
+// Windows are per user and per (user, app) (FS_SCOPE_USER_APP), so users are independent: one
+// CTA per user whose decisions still changed runs Jacobi passes over that user's segments alone
+// (counted flags -> segment-local exclusive scans -> head decisions) until nothing changes.
+// The fixed point is unique (decisions depend only on earlier positions), so this equals the
+// sequential definition.  Counts use exc[p] + flag[p] - exc[lb]: segment-local prefixes never
+// touch the next user's positions.
+static const int UJ_T = 512, UJ_IPT = 8;
+struct ActUserJacobiArgs {
+  const u32* users; u32 n_users_j; u32 A;
+  const u64* seg_u; const u64* seg_ua;
+  const u32* perm_u; const u32* pos_ua;
+  const uint2* pre_u; const uint2* pre_ua;
+  const i64* ts_u; const u64* lb_u; const u64* lb_ua;
   u32* pc_u; u64* ptau_u; u32* pc_ua; u64* ptau_ua;
-  const u32* meta; const u32* head_of; const u64* tau_call; const uint8_t* ovl;
-  const DLimits* L; const u32* ra; const u64* ta; u32 heads_only, A;
-  uint8_t* status;
+  const u32* meta; const uint8_t* ovl; const DLimits* L; const u32* ra; const u64* ta;
+  uint8_t* status; u32* iters;
 };
-__global__ void __launch_bounds__(128) k_act_walk(ActWalkArgs a) {
-  extern __shared__ __align__(16) unsigned char sm[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  WalkRing* ring = (WalkRing*)sm + wib * WALK_R;
-  u32* Ca = (u32*)((WalkRing*)sm + 4 * WALK_R) + wib * a.A;
-  u64* Ta = (u64*)((u32*)((WalkRing*)sm + 4 * WALK_R) + 4 * a.A) + wib * a.A;
-  u32 w = blockIdx.x * 4 + wib;
-  if (w >= a.n_users_walk) return;
-  const u32 u = a.users[w];
-  const u64 s = a.seg_u[u], e = a.seg_u[u + 1];
-  const DLimits L = *a.L;
-  for (u32 k = lane; k < a.A; k += 32) { Ca[k] = 0; Ta[k] = 0; }
-  __syncwarp();
-  u32 cu = s < e ? a.pc_u[s] : 0;          // running counts (any base: only differences matter)
-  u64 tu = s < e ? a.ptau_u[s] : 0;
-  for (u64 p0 = s; p0 < e; p0 += 32) {
-    u64 p = p0 + lane;
-    bool ok = p < e;
-    u32 id = 0, m = 0, q = 0, hp = 0; u64 tau = 0, lbu = 0, lbq = 0, lbx = 0; bool arr = false, ov = true;
-    if (ok) {
-      id = a.perm_u[p]; m = a.meta[id]; tau = a.tau_call[id]; q = a.pos_ua[id];
-      arr = a.ts_u[p] != INT64_MAX;
-      ov = a.ovl ? a.ovl[id] != 0 : true;
-      if (m_stage(m) == 1) { lbu = a.lb_u[p]; lbq = a.lb_ua[q]; lbx = a.pos_u[a.perm_ua[lbq]]; }
-      else hp = a.pos_u[a.head_of[id]];
-    }
-    u32 n = e - p0 < 32 ? (u32)(e - p0) : 32u;
-    for (u32 j = 0; j < n; j++) {
-      u64 pj = p0 + j;
-      u32 idj = __shfl_sync(FULL_MASK, id, j), mj = __shfl_sync(FULL_MASK, m, j), qj = __shfl_sync(FULL_MASK, q, j);
-      u64 tj = __shfl_sync(FULL_MASK, tau, j);
-      bool aj = __shfl_sync(FULL_MASK, arr, j), oj = __shfl_sync(FULL_MASK, ov, j);
-      u32 app = m_app(mj);
-      bool head = m_stage(mj) == 1;
-      u32 st = a.status[idj];                              // FILTERED / NOT_ARRIVED are final
-      bool live = st != FS_ST_FILTERED && aj;
-      bool counted = false;
-      if (live) {
-        if (head) counted = true;
-        else if (!a.heads_only) {
-          u64 hpj = __shfl_sync(FULL_MASK, (u64)hp, j);
-          u32 hs = pj - hpj < WALK_R ? ring[hpj % WALK_R].st : a.status[a.head_of[idj]];
-          counted = hs == FS_ST_ADMIT;
-        }
+// segment-local exclusive scans of counted flags and token loads over [s, e)
+// (from position s on, continuing the prefix already stored at s)
+__device__ void uj_scan(u64 s, u64 e, const uint2* pre, const uint8_t* status, u32* pc, u64* ptau,
+                        u32* shc, u64* sht, u32 carry_c, u64 carry_t) {
+  for (u64 c0 = s; c0 < e; c0 += (u64)UJ_T * UJ_IPT) {
+    u64 p0 = c0 + (u64)threadIdx.x * UJ_IPT;
+    u32 fc[UJ_IPT]; u32 ft[UJ_IPT];
+    u32 lc = 0; u64 lt = 0;
+#pragma unroll
+    for (int k = 0; k < UJ_IPT; k++) {
+      u64 p = p0 + k;
+      u32 f = 0, tv = 0;
+      if (p < e) {
+        uint2 v = pre[p];
+        f = v.x == ACT_HEAD || (v.x != NONE32 && status[v.x] == FS_ST_ADMIT);
+        tv = f ? v.y : 0u;
       }
-      u32 ca = Ca[app]; u64 ta_ = Ta[app];
-      // before-values of this position (exclusive prefixes)
-      WalkRing rv; rv.cu = cu; rv.ca = ca; rv.tu = tu; rv.ta = ta_; rv.st = st; rv.pad = 0;
-      if (counted) { cu++; tu += tj; ca++; ta_ += tj; }
-      if (head && live && oj) {                            // Alg. 1 l.20-24 on the window (Q4)
-        u64 lbuj = __shfl_sync(FULL_MASK, lbu, j), lbxj = __shfl_sync(FULL_MASK, lbx, j);
-        u64 lbqj = __shfl_sync(FULL_MASK, lbq, j);
-        u32 bcu; u64 btu; u32 bca; u64 bta;
-        if (pj - lbuj < WALK_R && lbuj < pj) { bcu = ring[lbuj % WALK_R].cu; btu = ring[lbuj % WALK_R].tu; }
-        else if (lbuj == pj) { bcu = rv.cu; btu = rv.tu; }
-        else { bcu = a.pc_u[lbuj]; btu = a.ptau_u[lbuj]; }
-        if (pj - lbxj < WALK_R && lbxj < pj) { bca = ring[lbxj % WALK_R].ca; bta = ring[lbxj % WALK_R].ta; }
-        else if (lbxj == pj) { bca = rv.ca; bta = rv.ta; }
-        else { bca = a.pc_ua[lbqj]; bta = a.ptau_ua[lbqj]; }
-        u64 n_g = cu - bcu, t_g = tu - btu, n_a = ca - bca, t_a = ta_ - bta;
-        st = FS_ST_ADMIT;
-        if (L.rg && n_g > L.rg) st = FS_ST_BLOCK_USER_REQ;
-        else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
-        else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
-        else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
-      } else if (head && live) st = FS_ST_ADMIT;
-      rv.st = st;
-      __syncwarp();
-      if (lane == 0) {
-        ring[pj % WALK_R] = rv;
-        Ca[app] = ca; Ta[app] = ta_;
-        a.pc_u[pj] = rv.cu; a.ptau_u[pj] = rv.tu; a.pc_ua[qj] = rv.ca; a.ptau_ua[qj] = rv.ta;
-        if (head && live) a.status[idj] = (uint8_t)st;
-      }
-      __syncwarp();
+      fc[k] = f; ft[k] = tv; lc += f; lt += tv;
     }
+    u32 totc; u64 tott;
+    u32 ec = block_excl_scan<u32>(lc, shc, &totc);
+    u64 et = block_excl_scan<u64>(lt, sht, &tott);
+    ec += carry_c; et += carry_t;
+#pragma unroll
+    for (int k = 0; k < UJ_IPT; k++) {
+      u64 p = p0 + k;
+      if (p < e) { pc[p] = ec; ptau[p] = et; }
+      ec += fc[k]; et += ft[k];
+    }
+    carry_c += totc; carry_t += tott;
   }
+}
+__global__ void __launch_bounds__(UJ_T) k_act_user_jacobi(ActUserJacobiArgs a) {
+  __shared__ u32 shc[32];
+  __shared__ u64 sht[32];
+  __shared__ int chg;
+  __shared__ unsigned long long fu, fa;   // first user / (user, app) position whose flag may change
+  const u32 u = a.users[blockIdx.x];
+  const u64 s = a.seg_u[u], e = a.seg_u[u + 1];
+  const u64 sa = a.seg_ua[(u64)u * a.A], ea = a.seg_ua[(u64)u * a.A + a.A];
+  const DLimits L = *a.L;
+  u32 it = 0;
+  u64 f = s, fq = sa;
+  // Positions before the first changed head keep their flags, prefixes and decisions (each
+  // depends on earlier positions only), so every pass restarts there.
+  for (;;) {
+    uj_scan(f, e, a.pre_u, a.status, a.pc_u, a.ptau_u, shc, sht, f > s ? a.pc_u[f] : 0u, f > s ? a.ptau_u[f] : 0ull);
+    uj_scan(fq, ea, a.pre_ua, a.status, a.pc_ua, a.ptau_ua, shc, sht, fq > sa ? a.pc_ua[fq] : 0u,
+            fq > sa ? a.ptau_ua[fq] : 0ull);
+    if (threadIdx.x == 0) { chg = 0; fu = ~0ull; fa = ~0ull; }
+    __syncthreads();
+    for (u64 p = f + threadIdx.x; p < e; p += UJ_T) {          // Alg. 1 l.20-24 for the user's heads
+      uint2 v = a.pre_u[p];
+      if (v.x != ACT_HEAD) continue;                           // arrived, not filtered heads only
+      u32 i = a.perm_u[p];
+      if (a.ovl && !a.ovl[i]) continue;
+      u64 q = a.pos_ua[i];
+      u64 lbu = a.lb_u[p], lba = a.lb_ua[q];
+      u64 n_g = (u64)a.pc_u[p] + 1 - a.pc_u[lbu], t_g = a.ptau_u[p] + v.y - a.ptau_u[lbu];
+      u64 n_a = (u64)a.pc_ua[q] + 1 - a.pc_ua[lba], t_a = a.ptau_ua[q] + v.y - a.ptau_ua[lba];
+      u32 app = m_app(a.meta[i]);
+      uint8_t st = FS_ST_ADMIT;
+      if (L.rg && n_g > L.rg) st = FS_ST_BLOCK_USER_REQ;
+      else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
+      else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
+      else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
+      if (st != a.status[i]) {
+        a.status[i] = st; chg = 1;
+        atomicMin(&fu, (unsigned long long)p); atomicMin(&fa, (unsigned long long)q);
+      }
+    }
+    __syncthreads();
+    it++;
+    if (!chg) break;
+    f = fu; fq = fa;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicMax(a.iters, it);
 }
 
 __global__ void k_act_list(u32 U, const u32* uchg, u32* list, u32* n) {

@@ -531,8 +531,8 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   u32* nlist = S.alloc<u32>(1);
   if (S.failed) return FS_E_NOMEM;
   u64 passes = 0, fixup = 0;
-  // Jacobi passes before the exact per-user sequential walk of the users still changing
-  // (FS_ACT_JACOBI_MAX overrides the default 2, for tests of both paths)
+  // global Jacobi passes, then per-user Jacobi (one CTA per user still changing) to the fixed
+  // point (FS_ACT_JACOBI_MAX overrides the default 2, for tests of both paths)
   const char* jenv = getenv("FS_ACT_JACOBI_MAX");
   const u64 JACOBI_MAX = jenv ? (u64)std::max(1L, atol(jenv)) : 2;
   for (;;) {
@@ -557,12 +557,17 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
       cudaMemcpyAsync(&nw, nlist, 4, cudaMemcpyDeviceToHost, ctx->stream);
       cudaStreamSynchronize(ctx->stream);
       fixup = nw;
-      ActWalkArgs wa{ulist, nw, ou.o.seg, ou.o.perm, oua.o.perm, oua.pos, ou.pos, ou.lb, oua.lb, ou.ts,
-                     ou.pc, ou.ptau, oua.pc, oua.ptau, t.meta, L.head_of, tau_call, overloaded, LD.L, LD.ra,
-                     LD.ta, heads_only, t.A, status};
-      size_t smem = (size_t)4 * WALK_R * sizeof(WalkRing) + (size_t)4 * t.A * 12;
-      cudaFuncSetAttribute(k_act_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (nw) FS_LAUNCH(ctx, "act_walk", k_act_walk, div_up(nw, 4), 128, smem, wa);
+      // users still changing: per-user Jacobi to the fixed point, one CTA each (k_act_user_jacobi)
+      u32* uit = S.zeros<u32>(1);
+      if (S.failed) return FS_E_NOMEM;
+      ActUserJacobiArgs ja{ulist, nw, t.A, ou.o.seg, oua.o.seg, ou.o.perm, oua.pos, ou.pre, oua.pre, ou.ts, ou.lb,
+                           oua.lb, ou.pc, ou.ptau, oua.pc, oua.ptau, t.meta, overloaded, LD.L, LD.ra, LD.ta, status,
+                           uit};
+      if (nw) FS_LAUNCH(ctx, "act_user_jacobi", k_act_user_jacobi, nw, UJ_T, 0, ja);
+      u32 hit = 0;
+      cudaMemcpyAsync(&hit, uit, 4, cudaMemcpyDeviceToHost, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      passes += hit;
       break;
     }
   }
