@@ -350,7 +350,9 @@ typedef struct { u64 n_in, n_admit, n_block[4], n_dropped, n_filtered, n_inter_b
 extern "C" int or_act(const or_trace* t, const or_profile_view* p, const or_act_cfg* c,
            const uint8_t* overloaded, const i64* t_ns_override,
            uint8_t* status, or_act_summary* s, u64* bad_index) {
-  if (!t || !c || !status || c->app_scope != 0 || c->count_mode > 1) return E_INVAL;
+  if (!t || !c || !status || c->app_scope > 1 || c->count_mode > 1) return E_INVAL;
+  // app-global counters (NEXT-3, R10): explicit limits only
+  if (c->app_scope == 1 && (c->limits_from_profile || c->limit_mult_q8)) return E_INVAL;
   if (p && p->A != t->A) { *bad_index = 0; return E_PROFILE; }
   std::vector<u32> head_of(t->n), next_call(t->n);
   int rc = or_validate(t, bad_index, head_of.data(), next_call.data());
@@ -374,48 +376,58 @@ extern "C" int or_act(const or_trace* t, const or_profile_view* p, const or_act_
     if (h == i || tns(i) < 0 || tns(h) < 0) continue;
     if (std::make_pair(tns(h), h) > std::make_pair(tns(i), i)) { *bad_index = i; return E_ORDER; }
   }
-  // per-user walk in (t_ns, id) order
-  std::vector<std::vector<std::pair<i64, u64>>> seqs(t->U);
-  for (u64 i = 0; i < t->n; i++) seqs[t->user[i]].push_back(std::make_pair(tns(i), i));
+  // one walk over all calls in (t_ns, id) order (arrived calls first, then those that never
+  // arrived): per-user logs give c_{g,u} and c_{a,u}; with app-global scope (R10) the app
+  // count c_a is taken over every user's logged calls of app a
+  std::vector<std::pair<i64, u64>> S;
+  for (u64 i = 0; i < t->n; i++) S.push_back(std::make_pair(tns(i), i));
+  std::sort(S.begin(), S.end(), [](const std::pair<i64, u64>& x, const std::pair<i64, u64>& y) {
+    return std::make_tuple(x.first < 0, x.first, x.second) < std::make_tuple(y.first < 0, y.first, y.second);
+  });
   const i64 W = (i64)c->window_ms * 1000000;
   std::memset(s, 0, sizeof(*s));
   for (u64 i = 0; i < t->n; i++) status[i] = 0xFF;            // undecided
-  for (u32 u = 0; u < t->U; u++) {
-    std::vector<std::pair<i64, u64>>& S = seqs[u];
-    // arrived calls in (t, id) order, then the calls that never arrived (t < 0):
-    // a call is DROPPED iff its head's final status is not ADMIT.
-    std::sort(S.begin(), S.end(), [](const std::pair<i64, u64>& x, const std::pair<i64, u64>& y) {
-      return std::make_tuple(x.first < 0, x.first, x.second) < std::make_tuple(y.first < 0, y.first, y.second);
-    });
-    std::vector<std::tuple<i64, u64, u32>> log;   // (t, tau, app) of counted calls
-    for (auto& e : S) {
-      u64 i = e.second;
-      u32 a = app_of(t, i);
-      if (tier_of(t, i) > c->tier_max) { status[i] = ST_FILTERED; s->n_filtered++; continue; }
-      if (stage_of(t, i) > 1 && status[head_of[i]] != ST_ADMIT) {
-        status[i] = ST_DROPPED; s->n_dropped++; continue;
-      }
-      if (e.first < 0) { status[i] = ST_NOT_ARRIVED; s->n_not_arrived++; continue; }
-      s->n_in++;
-      if (stage_of(t, i) == 1) {
-        log.push_back(std::make_tuple(e.first, tau[i], a));      // Alg.1 l.19: counted before the test
-        int st = ST_ADMIT;
-        if (!overloaded || overloaded[i]) {                        // l.20 (heads only)
-          u64 n_g = 0, tau_g = 0, n_a = 0, tau_a = 0;
-          for (size_t q = log.size(); q-- > 0;) {                // log is in (t, id) order
-            const auto& x = log[q];
-            if (std::get<0>(x) <= e.first - W) break;              // half-open window (Q4)
-            n_g++; tau_g += std::get<1>(x);
+  std::vector<std::vector<std::tuple<i64, u64, u32>>> logs(t->U);   // (t, tau, app) of counted calls
+  std::vector<std::tuple<i64, u64, u32>> glog;                      // all users (app-global scope)
+  for (auto& e : S) {
+    u64 i = e.second;
+    u32 a = app_of(t, i);
+    auto& log = logs[t->user[i]];
+    if (tier_of(t, i) > c->tier_max) { status[i] = ST_FILTERED; s->n_filtered++; continue; }
+    // a continuation is DROPPED iff its head's final status is not ADMIT
+    if (stage_of(t, i) > 1 && status[head_of[i]] != ST_ADMIT) {
+      status[i] = ST_DROPPED; s->n_dropped++; continue;
+    }
+    if (e.first < 0) { status[i] = ST_NOT_ARRIVED; s->n_not_arrived++; continue; }
+    s->n_in++;
+    if (stage_of(t, i) == 1) {
+      log.push_back(std::make_tuple(e.first, tau[i], a));        // Alg.1 l.19: counted before the test
+      glog.push_back(std::make_tuple(e.first, tau[i], a));
+      int st = ST_ADMIT;
+      if (!overloaded || overloaded[i]) {                          // l.20 (heads only)
+        u64 n_g = 0, tau_g = 0, n_a = 0, tau_a = 0;
+        for (size_t q = log.size(); q-- > 0;) {                  // log is in (t, id) order
+          const auto& x = log[q];
+          if (std::get<0>(x) <= e.first - W) break;                // half-open window (Q4)
+          n_g++; tau_g += std::get<1>(x);
+          if (c->app_scope == 0 && std::get<2>(x) == a) { n_a++; tau_a += std::get<1>(x); }
+        }
+        if (c->app_scope == 1)
+          for (size_t q = glog.size(); q-- > 0;) {
+            const auto& x = glog[q];
+            if (std::get<0>(x) <= e.first - W) break;
             if (std::get<2>(x) == a) { n_a++; tau_a += std::get<1>(x); }
           }
-          st = act_chain(L, a, n_g, tau_g, n_a, tau_a);
-        }
-        status[i] = (uint8_t)st;
-        if (st == ST_ADMIT) s->n_admit++;
-        else { s->n_block[st - 1]++; if (ncalls_of(t, i) > 1) s->n_inter_blocked++; }
-      } else {
-        status[i] = ST_ADMIT; s->n_admit++;
-        if (c->count_mode == COUNT_ALL) log.push_back(std::make_tuple(e.first, tau[i], a));
+        st = act_chain(L, a, n_g, tau_g, n_a, tau_a);
+      }
+      status[i] = (uint8_t)st;
+      if (st == ST_ADMIT) s->n_admit++;
+      else { s->n_block[st - 1]++; if (ncalls_of(t, i) > 1) s->n_inter_blocked++; }
+    } else {
+      status[i] = ST_ADMIT; s->n_admit++;
+      if (c->count_mode == COUNT_ALL) {
+        log.push_back(std::make_tuple(e.first, tau[i], a));
+        glog.push_back(std::make_tuple(e.first, tau[i], a));
       }
     }
   }
@@ -469,6 +481,7 @@ struct Sched {
   u64 seq = 0;
   std::vector<std::vector<std::tuple<i64, u64, u32>>> logs;   // ACT logs per user (t, tau, app)
   std::vector<std::pair<i64, u32>> rpm_log;   // RPM: every arrival (t, call), delivery order
+  std::vector<std::tuple<i64, u64, u32>> glog;  // app-global scope (R10): every user's logged calls
   u64 digest = 0;
   u64 n_adm = 0;
 
@@ -523,7 +536,10 @@ struct Sched {
     u64 tau_r = 0;
     if (c->mode == 1) {
       tau_r = prompt(r) + reserve(r);
-      if (c->act.count_mode == COUNT_ALL || head) logs[k].push_back(std::make_tuple(tr, tau_r, a));  // l.19
+      if (c->act.count_mode == COUNT_ALL || head) {
+        logs[k].push_back(std::make_tuple(tr, tau_r, a));                                        // l.19
+        if (c->act.app_scope == 1) glog.push_back(std::make_tuple(tr, tau_r, a));
+      }
     }
     int st = ST_ADMIT;
     if (c->mode == 3) {                                       // RPM: every
@@ -546,8 +562,13 @@ struct Sched {
       for (size_t q = lg.size(); q-- > 0;) {
         if (std::get<0>(lg[q]) <= tr - Wn) break;             // half-open window (Q4)
         n_g++; tau_g += std::get<1>(lg[q]);
-        if (std::get<2>(lg[q]) == a) { n_a++; tau_a += std::get<1>(lg[q]); }
+        if (c->act.app_scope == 0 && std::get<2>(lg[q]) == a) { n_a++; tau_a += std::get<1>(lg[q]); }
       }
+      if (c->act.app_scope == 1)                              // app-global counts (R10)
+        for (size_t q = glog.size(); q-- > 0;) {
+          if (std::get<0>(glog[q]) <= tr - Wn) break;
+          if (std::get<2>(glog[q]) == a) { n_a++; tau_a += std::get<1>(glog[q]); }
+        }
       st = act_chain(L, a, n_g, tau_g, n_a, tau_a);           // l.21-24
     }
     digest = sm64(digest ^ (r * 16 + (u64)st));
@@ -581,7 +602,10 @@ static int sched_init(Sched& S, const or_trace* t, const or_profile_view* p, con
   if (!t || !p || !c || c->max_batch == 0 || c->mode > 4 || c->alpha >= 256 || c->beta >= 256 ||
       c->gamma >= 256 || c->prio_benign_q16 >= (1u << 24) || c->prio_abusive_q16 >= (1u << 24))
     return E_INVAL;
-  if ((c->mode == 1 || c->mode == 3) && (c->act.app_scope != 0 || c->act.count_mode > 1)) return E_INVAL;
+  if ((c->mode == 1 || c->mode == 3) && (c->act.app_scope > (c->mode == 1 ? 1u : 0u) || c->act.count_mode > 1))
+    return E_INVAL;
+  if (c->mode == 1 && c->act.app_scope == 1 && (c->act.limits_from_profile || c->act.limit_mult_q8))
+    return E_INVAL;                                                  // app-global: explicit limits (R10)
   if (c->mode == 3 && (c->act.limits_from_profile || c->act.limit_mult_q8)) return E_INVAL;   // RPM: explicit limits (R8)
   if (p->A != t->A) { *bad_index = 0; return E_PROFILE; }
   head_of->resize(t->n); next_call->resize(t->n);
@@ -747,6 +771,7 @@ struct or_step_state { Sched S; std::vector<u32> head_of, next_call; };
 extern "C" int or_step_create(const or_trace* t, const or_profile_view* p, const or_replay_cfg* c,
                    or_step_state** out, u64* bad_index) {
   if (c && c->mode == 3) return E_INVAL;                      // RPM needs the replay's time order (R8)
+  if (c && c->mode == 1 && c->act.app_scope == 1) return E_INVAL;   // app-global windows too (R10)
   or_step_state* st = new or_step_state();
   int rc = sched_init(st->S, t, p, c, bad_index, &st->head_of, &st->next_call);
   if (rc) { delete st; return rc; }

@@ -65,6 +65,7 @@ class Sched:
             self.Tta = list(act.get("T_tok_a") or [0] * A)
         self.Wn = act.get("window_ms", 60000) * 1_000_000
         self.heads_only = act.get("count_mode", 0) == 1
+        self.app_global = act.get("app_scope", 0) == 1   # NEXT-3: c_a over every user (R10)
         self.u = [0] * self.U
         self.Q = []              # (call id, seq, is_cont) in delivery order
         self.e = None
@@ -123,7 +124,8 @@ class Sched:
         if self.mode == 1 and ovl and c["stage"] == 1:                   # l.20
             win = [x for x in self.log if x[2] == k and t - self.Wn < x[0] <= t]
             n_g, tau_g = len(win), sum(x[1] for x in win)
-            wa = [x for x in win if x[3] == c["app"]]
+            pool = [x for x in self.log if t - self.Wn < x[0] <= t] if self.app_global else win
+            wa = [x for x in pool if x[3] == c["app"]]
             n_a, tau_a = len(wa), sum(x[1] for x in wa)
             a = c["app"]
             if self.Trg and n_g > self.Trg:
@@ -264,6 +266,7 @@ def act(tr, ohat, cfg, overloaded=None, t_ns_override=None, limits=None):
     n = len(calls)
     Wn = cfg.get("window_ms", 60000) * 1_000_000
     heads_only = cfg.get("count_mode", 0) == 1
+    app_global = cfg.get("app_scope", 0) == 1
     tier_max = cfg.get("tier_max", 255)
     Trg, Ttg, Tra, Tta = limits
     tns = [(int(t_ns_override[i]) if t_ns_override is not None else calls[i]["t_ms"] * 1_000_000) for i in range(n)]
@@ -298,7 +301,10 @@ def act(tr, ohat, cfg, overloaded=None, t_ns_override=None, limits=None):
                and tns[i] - Wn < tns[x] and counted(x)]
         tau = lambda x: calls[x]["L_I"] + calls[x]["L_S"] + ohat(calls[x])
         n_g, tau_g = len(win), sum(tau(x) for x in win)
-        wa = [x for x in win if calls[x]["app"] == c["app"]]
+        pool = win
+        if app_global:           # every user's counted calls (R10)
+            pool = [x for x in range(n) if (tns[x], x) <= (tns[i], i) and tns[i] - Wn < tns[x] and counted(x)]
+        wa = [x for x in pool if calls[x]["app"] == c["app"]]
         n_a, tau_a = len(wa), sum(tau(x) for x in wa)
         a = c["app"]
         st = ADMIT

@@ -128,6 +128,68 @@ def test_act_vs_recount(seed):
     assert list(st) == ref
 
 
+@pytest.mark.parametrize("seed", range(200))
+def test_act_vs_recount_app_global(seed):
+    """NEXT-3 app-global counters (FS_SCOPE_APP_GLOBAL, R10) vs the O(n^2) recount."""
+    rng = np.random.default_rng(15000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=3, n_apps=A, max_inters=5, max_calls=9)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    prof = O.profile_from_host(A, J, cnt, si, ss, so)
+    n = tr["n_calls"]
+    cfg = dict(window_ms=int(rng.choice((1, 2, 4))), limits_from_profile=0, T_req_g=int(rng.choice((0, 2, 3))),
+               T_req_a=[int(rng.choice((0, 1, 2, 3))) for _ in range(A)], T_tok_g=int(rng.choice((0, 12))),
+               T_tok_a=[int(rng.choice((0, 9))) for _ in range(A)], count_mode=int(rng.integers(0, 2)),
+               tier_max=int(rng.choice((0, 255))), app_scope=1)
+    ovl = (rng.random(n) < 0.7).astype(np.uint8) if rng.random() < 0.8 else None
+    st, _ = O.act(tr, prof, cfg, overloaded=ovl)
+
+    def ohat(c):
+        j = S._slot(prof, c["app"], c["stage"])
+        return int(prof["sum_out"][c["app"]][j]) // int(prof["cnt"][c["app"]][j])
+
+    ref = S.act(tr, ohat, cfg, overloaded=ovl,
+                limits=(cfg["T_req_g"], cfg["T_tok_g"], cfg["T_req_a"], cfg["T_tok_a"]))
+    assert list(st) == ref
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_replay_vs_stepper_app_global(seed):
+    rng = np.random.default_rng(16000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(2, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    prof = O.profile_from_host(A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A, modes=(1,))
+    cfg["act"]["app_scope"] = 1
+    if _oversize(tr, prof, cfg):
+        return
+    o, s = O.replay(tr, prof, cfg)
+    eo, es = S.replay(tr, prof, cfg)
+    for k in ("status", "ovl", "arrive_ns", "admit_ns", "first_ns", "finish_ns", "order", "counters"):
+        assert list(o[k]) == list(eo[k]), (k, seed)
+    assert s["digest"] == es["digest"] and s["n_block"] == es["n_block"]
+
+
+def test_app_global_example():
+    """S:217 (c^r_a over the app's arrivals): user 0's head and then user 1's head of the same app
+    inside one window, T^r_a = 1, always overloaded -> user 1 is blocked (APP_REQ) with app-global
+    counters and admitted with per-(user, app) counters (Q2)."""
+    from paper_2411_15997_b200.tracegen import from_columns
+    rows = [dict(user=0, t_ms=0, app=0, inter=0, stage=1, ncalls=1, len_in=1, len_out=1),
+            dict(user=1, t_ms=1, app=0, inter=1, stage=1, ncalls=1, len_in=1, len_out=1)]
+    tr = from_columns(2, 1, rows)
+    prof = O.profile_from_host(1, 1, [[0, 1]], [[0, 1]], [[0, 0]], [[0, 1]])
+    cfg = dict(window_ms=60000, limits_from_profile=0, T_req_g=0, T_req_a=[1])
+    st, _ = O.act(tr, prof, dict(cfg, app_scope=1))
+    assert list(st) == [0, 3]
+    st, _ = O.act(tr, prof, cfg)
+    assert list(st) == [0, 0]
+    with pytest.raises(O.OracleError) as e:                      # R10: explicit limits only
+        O.act(tr, prof, dict(cfg, app_scope=1, limits_from_profile=1))
+    assert e.value.code == -1
+
+
 @pytest.mark.parametrize("seed", range(60))
 def test_step_vs_literal(seed):
     """Random step sequences: oracle Step vs the literal Sched of the stepper."""
