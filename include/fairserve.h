@@ -136,7 +136,10 @@ void fs_profile_partial_free(fs_profile_partial* part);
  * DROPPED iff their head is not admitted.  Result is the unique solution of the
  * causal recurrence. */
 enum { FS_COUNT_ALL_ARRIVALS = 0, FS_COUNT_HEADS_ONLY = 1 };
-enum { FS_SCOPE_USER_APP = 0 /* (Q2) */ };
+enum { FS_SCOPE_USER_APP = 0 /* (Q2) */,
+       FS_SCOPE_APP_GLOBAL = 1  /* NEXT-3 (R10): the app check counts every user's logged
+                                   calls of the app; explicit limits only (limits_from_profile = 0,
+                                   limit_mult_q8 = 0, else FS_E_INVAL); not for fs_wsc_step */ };
 enum {
   FS_ST_ADMIT = 0, FS_ST_BLOCK_USER_REQ = 1, FS_ST_BLOCK_USER_TOK = 2, FS_ST_BLOCK_APP_REQ = 3,
   FS_ST_BLOCK_APP_TOK = 4, FS_ST_DROPPED = 5, FS_ST_FILTERED = 6, FS_ST_NOT_ARRIVED = 7

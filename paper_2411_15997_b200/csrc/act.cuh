@@ -96,7 +96,7 @@ __global__ void k_gather_key(u64 n, const u32* perm, DTrace t, u32 by_app, u32* 
   u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   u32 i = perm[p];
-  key[p] = by_app ? t.user[i] * t.A + m_app(t.meta[i]) : t.user[i];
+  key[p] = by_app == 1 ? t.user[i] * t.A + m_app(t.meta[i]) : by_app == 2 ? m_app(t.meta[i]) : t.user[i];
 }
 
 struct ActOrder {

@@ -271,6 +271,7 @@ __global__ void k_replay_post(DTrace t, const u32* head_of, const u32* next_call
 static bool replay_cfg_ok(const fs_replay_cfg* c) {
   if (!c || c->mode > FS_MODE_FCFS) return false;
   if (c->mode == FS_MODE_RPM && (c->act.limits_from_profile || c->act.limit_mult_q8)) return false;   // R8
+  if (c->mode == FS_MODE_RPM && c->act.app_scope != FS_SCOPE_USER_APP) return false;
   return c->alpha < 256 && c->beta < 256 && c->gamma < 256 && c->prio_benign_q16 < (1u << 24) &&
          c->prio_abusive_q16 < (1u << 24) && c->max_batch >= 1 &&
          ((c->mode != FS_MODE_WI && c->mode != FS_MODE_RPM) || act_cfg_ok(&c->act));
@@ -327,6 +328,7 @@ static EngCfg eng_cfg(const fs_replay_cfg* c, const ScenTables& T, u32 s, u32 A,
   e.C = c->kv_capacity; e.Bmax = c->max_batch; e.theta = c->overload_permille;
   e.base = c->iter_base_ns; e.dec = c->decode_ns_per_req; e.pre = c->prefill_ns_per_tok;
   e.tier_max = c->tier_max; e.heads_only = c->act.count_mode == FS_COUNT_HEADS_ONLY;
+  e.app_global = c->mode == FS_MODE_WI && c->act.app_scope == FS_SCOPE_APP_GLOBAL;
   e.Wns = (i64)c->act.window_ms * 1000000;
   e.L = hl; e.ra = T.ra + (u64)s * A; e.ta = T.ta + (u64)s * A; e.W = T.W + (u64)s * AJ;
   e.inc = nullptr;
@@ -391,13 +393,14 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
     if (t.n) FS_LAUNCH(ctx, "replay_pre", k_replay_pre, div_up(t.n, B), B, 0, t, cfg->tier_max, o);
     if (o.admitted_per_app) cudaMemsetAsync(o.admitted_per_app, 0, t.A * 8, ctx->stream);
     // queued-continuation pool: same two-step capacity (n_inters is an exact bound)
+    const bool ag = wi && cfg->act.app_scope == FS_SCOPE_APP_GLOBAL;
+    const u32 all = (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull);        // exact log capacities
     EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget,
-                             cfg->mode >= FS_MODE_VTC, cfg->mode == FS_MODE_RPM ? (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull) : 0,
-                             t.A);
+                             cfg->mode >= FS_MODE_VTC, cfg->mode == FS_MODE_RPM ? all : 0, t.A, ag ? all : 0);
     unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
     if (S.failed) return FS_E_NOMEM;
     ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
-    auto rk = cfg->mode >= FS_MODE_VTC ? k_replay<true> : k_replay<false>;
+    auto rk = (cfg->mode >= FS_MODE_VTC || ag) ? k_replay<true> : k_replay<false>;
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
     FS_LAUNCH(ctx, "wsc_replay", rk, 1, 64, L.bytes_smem, a);
     cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
@@ -420,11 +423,12 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
                         fs_replay_summary* out, int32_t* codes) {
   if (!ctx || !tr || !P || !scen || !out || !codes || tr->n_apps == 0) return FS_E_INVAL;
   if (ns == 0) return FS_OK;
-  bool any_wi = false, any_dq = false, any_rpm = false;
+  bool any_wi = false, any_dq = false, any_rpm = false, any_ag = false;
   u32 Bmax = 1;
   for (u32 s = 0; s < ns; s++) {
     any_dq |= scen[s].mode >= FS_MODE_VTC;
     any_rpm |= scen[s].mode == FS_MODE_RPM;
+    any_ag |= scen[s].mode == FS_MODE_WI && scen[s].act.app_scope == FS_SCOPE_APP_GLOBAL;
     if (!replay_cfg_ok(&scen[s]) || scen[s].prio_q16) return FS_E_INVAL;
     if (scen[s].mode == FS_MODE_WI) {
       for (u32 q = 0; q < s; q++)          // one static head window per call
@@ -489,7 +493,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   cudaMemcpyAsync(dc, hc.data(), ns * sizeof(EngCfg), cudaMemcpyHostToDevice, ctx->stream);
   u32 p_cap = std::max<u32>(std::min<u32>(t.X, 1u << 16), 1);
   EngLayout L = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi,
-                           W.ring_slots, false, 0, any_dq, any_rpm ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0, t.A);
+                           W.ring_slots, false, 0, any_dq, any_rpm ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0, t.A,
+                           any_ag ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0);
   size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
@@ -499,12 +504,13 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   static const int lps = [] { const char* v = getenv("FS_SWEEP_LPS"); return v ? atoi(v) : 32; }();
   // scenarios of the FairServe modes only: the engine without the baseline-mode paths
   // (FS_SWEEP_LPS = 16 / 8, several replays per warp, measured slower: FS-mode engine only)
-  auto kern = any_dq ? (minb >= 6 ? k_sweep<6, 32, true> : minb == 5 ? k_sweep<5, 32, true> :
+  const bool base = any_dq || any_ag;
+  auto kern = base ? (minb >= 6 ? k_sweep<6, 32, true> : minb == 5 ? k_sweep<5, 32, true> :
                         minb == 4 ? k_sweep<4, 32, true> : k_sweep<3, 32, true>)
             : lps <= 8 ? k_sweep<4, 8, false> : lps == 16 ? k_sweep<4, 16, false>
             : (minb >= 6 ? k_sweep<6, 32, false> : minb == 5 ? k_sweep<5, 32, false> :
                minb == 4 ? k_sweep<4, 32, false> : k_sweep<3, 32, false>);
-  const u32 per_cta = any_dq ? 4 : 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
+  const u32 per_cta = base ? 4 : 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
   // the replays' state lives in global memory: give L1 every byte shared memory does not need
   static const int carve = [] { const char* v = getenv("FS_SWEEP_CARVE"); return v ? atoi(v) : -1; }();
   if (carve >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
@@ -575,6 +581,7 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
                                    fs_wsc_state** out) {
   if (!ctx || !tr || !P || !out || !replay_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
   if (cfg->mode == FS_MODE_RPM) return FS_E_INVAL;         // RPM needs the replay's time order (R8)
+  if (cfg->mode == FS_MODE_WI && cfg->act.app_scope == FS_SCOPE_APP_GLOBAL) return FS_E_INVAL;   // R10
   *out = nullptr;
   if (P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
   fs_wsc_state* st = new fs_wsc_state();

@@ -430,7 +430,8 @@ extern "C" void fs_profile_free(fs_profile* P) {
 
 // ------------------------------------------------------------------ ACT
 static bool act_cfg_ok(const fs_act_cfg* c) {
-  return c && c->app_scope == FS_SCOPE_USER_APP && c->count_mode <= 1;
+  if (!c || c->app_scope > FS_SCOPE_APP_GLOBAL || c->count_mode > 1) return false;
+  return c->app_scope == FS_SCOPE_USER_APP || (!c->limits_from_profile && !c->limit_mult_q8);   // R10
 }
 
 // device limit table for an ACT config (+ profile); returns false on bad input
@@ -451,11 +452,11 @@ static bool act_limits(fs_ctx* ctx, Scratch& S, const fs_profile* P, const fs_ac
 }
 
 // (user[, app], t_ns, id) order of all calls; never-arrived calls sort last in their segment
-static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, bool by_app, i64 W, ActOrder* ao) {
+static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, int kind, i64 W, ActOrder* ao) {
   u64 n = t.n;
   int B = 256;
   if (!tov) {
-    if (!build_order(ctx, S, t, by_app, &ao->o)) return false;
+    if (!build_order(ctx, S, t, kind, &ao->o)) return false;
   } else {
     unsigned long long* mx = S.zeros<unsigned long long>(1);
     u64* tk = S.alloc<u64>(n);
@@ -469,8 +470,8 @@ static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, 
     if (!radix_sort<u64>(ctx, S, tk, nullptr, n, bits_for(hmx + 1), &tks, &permt)) return false;
     u32* k2 = S.alloc<u32>(n);
     if (S.failed) return false;
-    FS_LAUNCH(ctx, "gather_key", k_gather_key, div_up(n, B), B, 0, n, permt, t, by_app ? 1u : 0u, k2);
-    ao->o.nseg = by_app ? (u64)t.U * t.A : t.U;
+    FS_LAUNCH(ctx, "gather_key", k_gather_key, div_up(n, B), B, 0, n, permt, t, (u32)kind, k2);
+    ao->o.nseg = kind == 1 ? (u64)t.U * t.A : kind == 2 ? (u64)t.A : t.U;
     if (!radix_sort<u32>(ctx, S, k2, permt, n, bits_for(ao->o.nseg ? ao->o.nseg - 1 : 0), &ao->o.key, &ao->o.perm))
       return false;
     ao->o.seg = S.alloc<u64>(ao->o.nseg + 1);
@@ -515,7 +516,9 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   if (rc) return rc;
   const i64 W = (i64)cfg->window_ms * 1000000;
   ActOrder ou, oua;
-  if (!act_order(ctx, S, t, tov, false, W, &ou) || !act_order(ctx, S, t, tov, true, W, &oua)) return FS_E_NOMEM;
+  // second order: per (user, app), or per app with app-global counters (R10)
+  const bool app_global = cfg->app_scope == FS_SCOPE_APP_GLOBAL;
+  if (!act_order(ctx, S, t, tov, 0, W, &ou) || !act_order(ctx, S, t, tov, app_global ? 2 : 1, W, &oua)) return FS_E_NOMEM;
   const u32 heads_only = cfg->count_mode == FS_COUNT_HEADS_ONLY;
   uint2* apk = S.alloc<uint2>(n);
   if (S.failed) return FS_E_NOMEM;
@@ -550,7 +553,7 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
     cudaMemcpyAsync(&hc, changed, 4, cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
     if (!hc || heads_only) break;
-    if (passes >= JACOBI_MAX) {
+    if (passes >= JACOBI_MAX && !app_global) {     // app-global windows couple users: global passes only
       cudaMemsetAsync(nlist, 0, 4, ctx->stream);
       FS_LAUNCH(ctx, "act_list", k_act_list, div_up(t.U, B), B, 0, t.U, uchg, ulist, nlist);
       u32 nw = 0;

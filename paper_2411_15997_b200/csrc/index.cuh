@@ -113,6 +113,10 @@ __global__ void k_key_user_app(DTrace t, u32* key) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < t.n) key[i] = t.user[i] * t.A + m_app(t.meta[i]);
 }
+__global__ void k_key_app(DTrace t, u32* key) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < t.n) key[i] = m_app(t.meta[i]);
+}
 
 struct Order {      // a stable (key, t, id) order of all calls
   u32* key;         // sorted keys (segment id per position)
@@ -121,18 +125,20 @@ struct Order {      // a stable (key, t, id) order of all calls
   u64 nseg;
 };
 
-// by_app = false: key = user (U segments); true: key = user * A + app (U*A segments).
-// The input order is (t_ms, id) so a stable sort yields (key, t, id).
-static bool build_order(fs_ctx* ctx, Scratch& S, const DTrace& t, bool by_app, Order* o) {
+// kind 0: key = user (U segments); 1: key = user * A + app (U*A segments); 2: key = app (A
+// segments, app-global windows, R10).  The input order is (t_ms, id) so a stable sort yields
+// (key, t, id).
+static bool build_order(fs_ctx* ctx, Scratch& S, const DTrace& t, int kind, Order* o) {
   u64 n = t.n;
   u32* k0 = S.alloc<u32>(n);
   if (S.failed) return false;
   int B = 256;
   if (n) {
-    if (by_app) FS_LAUNCH(ctx, "key_user_app", k_key_user_app, div_up(n, B), B, 0, t, k0);
+    if (kind == 1) FS_LAUNCH(ctx, "key_user_app", k_key_user_app, div_up(n, B), B, 0, t, k0);
+    else if (kind == 2) FS_LAUNCH(ctx, "key_app", k_key_app, div_up(n, B), B, 0, t, k0);
     else FS_LAUNCH(ctx, "key_user", k_key_user, div_up(n, B), B, 0, t, k0);
   }
-  o->nseg = by_app ? (u64)t.U * t.A : t.U;
+  o->nseg = kind == 1 ? (u64)t.U * t.A : kind == 2 ? (u64)t.A : t.U;
   if (!radix_sort<u32>(ctx, S, k0, nullptr, n, bits_for(o->nseg ? o->nseg - 1 : 0), &o->key, &o->perm)) return false;
   o->seg = S.alloc<u64>(o->nseg + 1);
   if (S.failed) return false;

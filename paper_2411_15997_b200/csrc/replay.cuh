@@ -48,7 +48,7 @@ struct EngCfg {                         // one scenario
   const u32* prio_q16;
   u64 C; u32 Bmax, theta;
   u64 base, dec, pre;
-  u32 tier_max, heads_only;
+  u32 tier_max, heads_only, app_global;  // app_global: FS_SCOPE_APP_GLOBAL app checks (R10)
   i64 Wns;
   DLimits L; const u32* ra; const u64* ta;
   const u64* W;                         // [A][J1] Q16 stage weights for (alpha, beta, gamma)
@@ -72,6 +72,8 @@ struct BEnt { u64 fi; u64 inc; u32 r, user, meta, link, think, rel; };   // batc
 struct PEnt { i64 t; u32 r, user, meta, pad; };                          // pending continuation (24 B)
 struct REnt { i64 t; u32 tau, app; };   // ACT ring entry: arrival, token load, app (16 B)
 struct RPEnt { i64 t; u32 user, app; }; // RPM window log entry (16 B)
+struct AGEnt { i64 t; u32 app, tau; };  // app-global window log entry (16 B)
+struct AGSum { u64 tau; u32 n, pad; };  // live logged calls of one app (all users)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
 
 struct EngState {
@@ -85,6 +87,7 @@ struct EngState {
   REnt* r;                              // ACT rings [ring slots] (CSR by user), one 16-B entry each
   u32* hseq;                            // VTC / RPM / FCFS: delivery seq of each head (uh position)
   RPEnt* rf; u32 rf_cap; u32* rapp;     // RPM: window log of every arrival (FIFO), live arrivals per app
+  AGEnt* ag; u32 ag_cap; AGSum* ags;    // app-global FS(W+I): window log of logged calls, per-app sums
   u64* W;                               // stage weights (smem copy or the scenario's table)
 };
 
@@ -129,6 +132,7 @@ struct EngineT {
   HEnt* hb; u32 hb_i, hb_n;              // HS_WARP: the group's shared-memory batch (LPS entries), next, count
   u32 hb_t, hb_r;                        // HS_WARP: (t_ms, id) of the next entry
   u32 rf_head, rf_len;                   // RPM window log: oldest entry, live entries
+  u32 ag_head, ag_len;                   // app-global window log
   u64 digest, n_adm;
   fs_replay_summary sum;
   int err_code; u64 err_idx;
@@ -190,7 +194,7 @@ struct EngineT {
     c_top = st.c_cap;                                      // eng_clear fills cfree[i] = i
     clock = 0; occ = 0; iter = 0; e = -1; seq = 0; hp = 0; digest = 0; n_adm = 0;
     static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
-    hb_i = hb_n = 0; rf_head = rf_len = 0;
+    hb_i = hb_n = 0; rf_head = rf_len = 0; ag_head = ag_len = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
   }
@@ -253,7 +257,7 @@ struct EngineT {
         u32 idx = h + q; if (idx >= cap) idx -= cap;
         REnt re = s.r[base + idx];
         n_g++; t_g += re.tau;
-        if (re.app == app) { n_a++; t_a += re.tau; }
+        if (re.app == app && !(BASE && c->app_global)) { n_a++; t_a += re.tau; }
       }
     }
     const DLimits& L = c->L;
@@ -272,6 +276,26 @@ struct EngineT {
     REnt re; re.t = tr; re.tau = tau; re.app = app;
     s.r[base + idx] = re;
     us.r_head = h; us.r_len = len + 1;
+    return true;
+  }
+
+  // app-global counters (R10): every logged call of every user in one FIFO (deliveries come in
+  // time order and share W), with live count / token load per app
+  __device__ __forceinline__ bool ag_log(i64 tr, u32 app, u32 tau, u32 r) {
+    const i64 lim = tr - c->Wns;
+    while (ag_len) {
+      AGEnt g = s.ag[ag_head];
+      if (g.t > lim) break;                              // half-open window (Q4)
+      s.ags[g.app].n--; s.ags[g.app].tau -= g.tau;
+      ag_head = ag_head + 1 == s.ag_cap ? 0 : ag_head + 1;
+      ag_len--;
+    }
+    if (ag_len == s.ag_cap) { err_code = ERR_NOMEM; err_idx = r; return false; }
+    u32 idx = ag_head + ag_len; if (idx >= s.ag_cap) idx -= s.ag_cap;
+    AGEnt g; g.t = tr; g.app = app; g.tau = tau;
+    s.ag[idx] = g;
+    ag_len++;
+    s.ags[app].n++; s.ags[app].tau += tau;
     return true;
   }
 
@@ -331,7 +355,10 @@ struct EngineT {
     int st = FS_ST_ADMIT;
     if (c->mode == FS_MODE_WI) {
       if (!static_heads && !ring_push(us, k, tr, h.B.y + h.B.w, m_app(m), r)) return -1;   // l.19
-      if (ovl) st = act_check(us, k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);                 // l.20-24
+      if (BASE && c->app_global) {                                                          // R10
+        if (!ag_log(tr, m_app(m), h.B.y + h.B.w, r)) return -1;
+        if (ovl) { const AGSum g = s.ags[m_app(m)]; st = act_check(us, k, m_app(m), tr, h.ng, h.tg, g.n, g.tau); }
+      } else if (ovl) st = act_check(us, k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);          // l.20-24
     } else if (BASE && c->mode == FS_MODE_RPM) {
       st = rpm_check(us, k, m_app(m), tr, r);
       if (st < 0) return -1;
@@ -369,6 +396,7 @@ struct EngineT {
     if (c->mode == FS_MODE_WI && !c->heads_only) {          // l.19 (continuations are never throttled)
       uint4 B = ldg4(&sh->recB[r]);
       if (!ring_push(us, k, tr, B.y + B.w, m_app(m), r)) return -1;
+      if (BASE && c->app_global && !ag_log(tr, m_app(m), B.y + B.w, r)) return -1;
     }
     if (BASE && c->mode == FS_MODE_RPM) {                   // RPM throttles continuations too (R8)
       int st = rpm_check(us, k, m_app(m), tr, r);
@@ -800,19 +828,21 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
 
 // ------------------------------------------------------------------ state layout
 enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_HPOS, L_CS, L_CF, L_BLK, L_RT, L_HSEQ, L_RF,
-       L_RAPP, L_N };
+       L_RAPP, L_AG, L_AGS, L_N };
 struct EngLayout {
   size_t bytes_smem = 0, bytes_glob = 0;
   size_t off[L_N];
   bool smem[L_N];
   u32 c_cap = 0;                        // continuation-slot pool capacity
   u32 rf_cap = 0, A = 0;                // RPM window log capacity, apps
+  u32 ag_cap = 0;                       // app-global window log capacity
 };
 
 // slots: capacity of the pool of queued-continuation slots (R5)
 // hseq: per-head delivery seqs (VTC / RPM / FCFS); rf_cap > 0: the RPM window log + per-app counts
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
-                            bool hring, size_t smem_budget, bool hseq = false, u32 rf_cap = 0, u32 A = 0) {
+                            bool hring, size_t smem_budget, bool hseq = false, u32 rf_cap = 0, u32 A = 0,
+                            u32 ag_cap = 0) {
   size_t sz[L_N];
   sz[L_HR] = hring ? (size_t)HRING * (sizeof(HEnt) + 8) + 64 : 0;
   sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
@@ -826,11 +856,13 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   sz[L_HSEQ] = hseq ? (size_t)(n_heads + 1) * 4 : 0;
   sz[L_RF] = (size_t)rf_cap * sizeof(RPEnt);
   sz[L_RAPP] = rf_cap ? (size_t)A * 4 : 0;
+  sz[L_AG] = (size_t)ag_cap * sizeof(AGEnt);
+  sz[L_AGS] = ag_cap ? (size_t)A * sizeof(AGSum) : 0;
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_RAPP, L_US, L_HK, L_HM, L_CS, L_CF};
+  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_RAPP, L_AGS, L_US, L_HK, L_HM, L_CS, L_CF};
   EngLayout L;
   L.c_cap = (u32)slots;
-  L.rf_cap = rf_cap; L.A = A;
+  L.rf_cap = rf_cap; L.A = A; L.ag_cap = ag_cap;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
     size_t b = (sz[k] + 15) / 16 * 16;
@@ -851,6 +883,7 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
   s->blocked = (u32*)P(L_BLK);
   s->r = (REnt*)P(L_RT); s->hpos = (uint2*)P(L_HPOS);
   s->hseq = (u32*)P(L_HSEQ); s->rf = (RPEnt*)P(L_RF); s->rf_cap = L.rf_cap; s->rapp = (u32*)P(L_RAPP);
+  s->ag = (AGEnt*)P(L_AG); s->ag_cap = L.ag_cap; s->ags = (AGSum*)P(L_AGS);
   if (hr) {
     unsigned char* base = (unsigned char*)P(L_HR);
     hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
@@ -872,6 +905,7 @@ __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u
   }
   for (u64 w = lane; w < sh.n_heads / 32 + 2; w += nl) s.blocked[w] = 0;
   if (s.rf_cap) for (u32 a = lane; a < sh.A; a += nl) s.rapp[a] = 0;
+  if (s.ag_cap) for (u32 a = lane; a < sh.A; a += nl) { AGSum z; z.tau = 0; z.n = 0; z.pad = 0; s.ags[a] = z; }
   for (u32 k = lane; k < s.c_cap; k += nl) s.cfree[k] = s.c_cap - 1 - k;   // pops hand out 0, 1, 2, ...
   if (s.W != W) for (u64 k = lane; k < AJ; k += nl) s.W[k] = W[k];
 }

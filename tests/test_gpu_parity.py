@@ -487,3 +487,71 @@ def test_metrics_tiny(F, ctx, seed):
         return
     go, _ = F.wsc_replay(ctx, F.Trace(tr), gp, cfg)
     _cmp_metrics(F, ctx, tr, go, eo, int(rng.choice((0, 1_000_000, 10**9))), f"tiny{seed}")
+
+
+# ------------------------------------------------------------------ NEXT-3 app-global counters
+@pytest.mark.parametrize("seed", range(60))
+def test_act_tiny_app_global(F, ctx, seed):
+    import torch
+    rng = np.random.default_rng(15000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=3, n_apps=A, max_inters=5, max_calls=9)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    n = tr["n_calls"]
+    cfg = dict(window_ms=int(rng.choice((1, 2, 4))), limits_from_profile=0, T_req_g=int(rng.choice((0, 2, 3))),
+               T_req_a=[int(rng.choice((0, 1, 2, 3))) for _ in range(A)], T_tok_g=int(rng.choice((0, 12))),
+               T_tok_a=[int(rng.choice((0, 9))) for _ in range(A)], count_mode=int(rng.integers(0, 2)),
+               tier_max=int(rng.choice((0, 255))), app_scope=1)
+    ovl = (rng.random(n) < 0.7).astype(np.uint8) if rng.random() < 0.8 else None
+    est, esum = O.act(tr, op, cfg, overloaded=ovl)
+    st, s = F.act_throttle(ctx, F.Trace(tr), gp, cfg,
+                           overloaded=None if ovl is None else torch.tensor(ovl, device="cuda"))
+    assert list(_np(st)) == list(est)
+    assert s["n_block"] == esum["n_block"]
+
+
+def test_act_c2_shape_app_global(F, ctx):
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=300, n_calls=200_000, seed=41))
+    op = O.profile(tr, dict(tier_max=0))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=0))
+    cfg = dict(window_ms=60000, limits_from_profile=0, T_req_g=12, T_req_a=[60] * tr["n_apps"],
+               T_tok_g=0, T_tok_a=[200000] * tr["n_apps"], app_scope=1)
+    est, esum = O.act(tr, op, cfg)
+    st, s = F.act_throttle(ctx, F.Trace(tr), gp, cfg)
+    g = _np(st)
+    bad = np.nonzero(g != est)[0]
+    assert len(bad) == 0, (bad[:10], g[bad[:10]], est[bad[:10]])
+    assert s["n_block"] == esum["n_block"] and sum(esum["n_block"]) > 0
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_replay_tiny_app_global(F, ctx, seed):
+    rng = np.random.default_rng(16000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(2, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A, modes=(1,))
+    cfg["act"]["app_scope"] = 1
+    cmp_replay(F, ctx, tr, gp, op, cfg, f"ag{seed}")
+
+
+def test_sweep_app_global(F, ctx):
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=100, n_calls=20_000, seed=61))
+    op = O.profile(tr, dict(tier_max=0))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=0))
+    base = dict(G.CONFIGS["c2"]["engine"], mode=1)
+    scen = []
+    for tm, lim, cm in [(15, 20, 0), (0, 10, 0), (7, 30, 1), (15, 5, 1)]:
+        scen.append(dict(base, tier_max=tm, overload_permille=0, act=dict(window_ms=60000, limits_from_profile=0, T_req_g=8,
+                                                     T_req_a=[lim] * tr["n_apps"], count_mode=cm, app_scope=1)))
+    scen.append(dict(base, act=dict(window_ms=60000, limits_from_profile=1)))
+    es, ecodes = O.sweep(tr, op, scen)
+    gs, gcodes = F.sweep(ctx, F.Trace(tr), gp, scen)
+    assert list(gcodes) == list(ecodes)
+    for a, b in zip(gs, es):
+        assert a == b
+    assert sum(es[0]["n_block"]) > 0
