@@ -115,6 +115,24 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def n_apps_of(wl):
+    from paper_2411_15997_b200 import tracegen as G
+    c = G.CONFIGS[wl]
+    return c.get("n_apps", len(c["apps"]) * len(c["app_scales"]))
+
+
+def workload_config(wl, n_calls, n_users, n_apps, scenarios, world):
+    """The `config` object of the JSON line (shared by both arms)."""
+    return {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive; profile + FS(W+I) replay + ACT",
+                         "c3": "C3: 10k users, 12 apps, 10M calls; profile + FS(W+I) replay + ACT",
+                         "c4": f"C4: app profile of {n_calls} calls sharded by user over {world} GPU(s) "
+                               f"(NCCL u64 SUM all-reduce rounds)",
+                         "c5": f"C5: profile + sweep of {scenarios} replays (throttle k x (alpha,beta,gamma) x "
+                               f"E_abusive x tier_max) of a 1M-call trace"}[wl],
+            "n_calls": n_calls, "n_users": n_users, "n_apps": n_apps, "scenarios_per_gpu": scenarios,
+            "parallelism": (f"user-hash shards x{world}" if wl == "c4" else f"independent problem per GPU x{world}")}
+
+
 def workload_cfg(name):
     from paper_2411_15997_b200 import tracegen as G
     c = G.CONFIGS[name]
@@ -280,16 +298,8 @@ def main():
         "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if wl == "c4" else "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive; profile + FS(W+I) replay + ACT",
-                                "c3": "C3: 10k users, 12 apps, 10M calls; profile + FS(W+I) replay + ACT",
-                                "c4": f"C4: app profile of {N * world} calls sharded by user over {world} GPU(s) "
-                                      f"(NCCL u64 SUM all-reduce rounds)",
-                                "c5": f"C5: profile + sweep of {S} replays (throttle k x (alpha,beta,gamma) x "
-                                      f"E_abusive x tier_max) of a 1M-call trace"}[wl],
-                   "n_calls": N, "n_users": tr["n_users"], "n_apps": tr["n_apps"], "scenarios_per_gpu": S,
-                   "parallelism": (f"user-hash shards x{world}" if wl == "c4" else
-                                   f"independent problem per GPU x{world}"),
-                   "l2": "flushed between timed steps (256 MB write, untimed)"},
+        "config": dict(workload_config(wl, N * world if wl == "c4" else N, tr["n_users"], tr["n_apps"], S, world),
+                       l2="flushed between timed steps (256 MB write, untimed)"),
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
                 "d2h_bytes_per_step": {"c4": 0}.get(wl, N if scen is None else 144 * S)},
         "gpu_launches": int(launches),
@@ -438,7 +448,8 @@ def reference(args, rank, world):
             "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": wl, "n_calls": n},
+            "config": workload_config(wl, G.CONFIGS[wl]["n_calls"], G.CONFIGS[wl]["n_users"], n_apps_of(wl),
+                                      args.scenarios if wl == "c5" else 0, 1),
             "cpu_baseline": {"value": v, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
