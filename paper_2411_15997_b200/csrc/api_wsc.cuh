@@ -471,7 +471,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
       if (k == combos.size()) combos.push_back(key);
       combo_of[s] = k;
     }
-    if ((u64)combos.size() * (t.n + 1) * 8 <= (2ull << 30)) {
+    static const int no_inc = [] { const char* v = getenv("FS_SWEEP_NO_INC"); return v ? atoi(v) : 0; }();
+    if (!no_inc && (u64)combos.size() * (t.n + 1) * 8 <= (2ull << 30)) {
       std::vector<u64*> tabs(combos.size());
       for (size_t k = 0; k < combos.size(); k++) tabs[k] = S.alloc<u64>(t.n + 1);
       if (S.failed) return FS_E_NOMEM;
