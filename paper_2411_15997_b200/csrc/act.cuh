@@ -205,10 +205,11 @@ struct ActUserJacobiArgs {
   const u32* meta; const uint8_t* ovl; const DLimits* L; const u32* ra; const u64* ta;
   uint8_t* status; u32* iters;
 };
-// segment-local exclusive scans of counted flags and token loads over [s, e)
-// (from position s on, continuing the prefix already stored at s)
+// exclusive scans of counted flags and token loads over [s, e), continuing from the carries;
+// returns the totals (block-uniform)
 __device__ void uj_scan(u64 s, u64 e, const uint2* pre, const uint8_t* status, u32* pc, u64* ptau,
-                        u32* shc, u64* sht, u32 carry_c, u64 carry_t) {
+                        u32* shc, u64* sht, u32* carry_c, u64* carry_t) {
+  u32 cc = *carry_c; u64 ct = *carry_t;
   for (u64 c0 = s; c0 < e; c0 += (u64)UJ_T * UJ_IPT) {
     u64 p0 = c0 + (u64)threadIdx.x * UJ_IPT;
     u32 fc[UJ_IPT]; u32 ft[UJ_IPT];
@@ -227,62 +228,91 @@ __device__ void uj_scan(u64 s, u64 e, const uint2* pre, const uint8_t* status, u
     u32 totc; u64 tott;
     u32 ec = block_excl_scan<u32>(lc, shc, &totc);
     u64 et = block_excl_scan<u64>(lt, sht, &tott);
-    ec += carry_c; et += carry_t;
+    ec += cc; et += ct;
 #pragma unroll
     for (int k = 0; k < UJ_IPT; k++) {
       u64 p = p0 + k;
       if (p < e) { pc[p] = ec; ptau[p] = et; }
       ec += fc[k]; et += ft[k];
     }
-    carry_c += totc; carry_t += tott;
+    cc += totc; ct += tott;
   }
+  *carry_c = cc; *carry_t = ct;
 }
+// Blocked Gauss-Seidel: the user's (t, id) order in chunks of UJ_CH positions; a chunk's decisions
+// depend only on itself and earlier (final) chunks, so each chunk is iterated (flags -> scans ->
+// decisions) until nothing changes, then frozen.  Prefixes are zero-based per user (u order) and
+// per (user, app) sub-segment (ua order, running carries per app); a chunk's calls of one app
+// occupy one contiguous ua range.
+static const int UJ_CH = UJ_T * UJ_IPT, UJ_AMAX = 256;
 __global__ void __launch_bounds__(UJ_T) k_act_user_jacobi(ActUserJacobiArgs a) {
   __shared__ u32 shc[32];
   __shared__ u64 sht[32];
   __shared__ int chg;
-  __shared__ unsigned long long fu, fa;   // first user / (user, app) position whose flag may change
+  __shared__ unsigned long long qmin[UJ_AMAX], qmax[UJ_AMAX];
+  __shared__ u32 acc[UJ_AMAX], nacc[UJ_AMAX];
+  __shared__ u64 act_[UJ_AMAX], nact[UJ_AMAX];
   const u32 u = a.users[blockIdx.x];
   const u64 s = a.seg_u[u], e = a.seg_u[u + 1];
-  const u64 sa = a.seg_ua[(u64)u * a.A], ea = a.seg_ua[(u64)u * a.A + a.A];
   const DLimits L = *a.L;
-  u32 it = 0;
-  u64 f = s, fq = sa;
-  // Positions before the first changed head keep their flags, prefixes and decisions (each
-  // depends on earlier positions only), so every pass restarts there.
-  for (;;) {
-    uj_scan(f, e, a.pre_u, a.status, a.pc_u, a.ptau_u, shc, sht, f > s ? a.pc_u[f] : 0u, f > s ? a.ptau_u[f] : 0ull);
-    uj_scan(fq, ea, a.pre_ua, a.status, a.pc_ua, a.ptau_ua, shc, sht, fq > sa ? a.pc_ua[fq] : 0u,
-            fq > sa ? a.ptau_ua[fq] : 0ull);
-    if (threadIdx.x == 0) { chg = 0; fu = ~0ull; fa = ~0ull; }
+  for (u32 k = threadIdx.x; k < a.A; k += UJ_T) { acc[k] = 0; act_[k] = 0; }
+  u32 ucc = 0; u64 uct = 0;                    // u-order carries at the chunk start
+  u32 it_max = 0;
+  __syncthreads();
+  for (u64 c0 = s; c0 < e; c0 += UJ_CH) {
+    const u64 c1 = c0 + UJ_CH < e ? c0 + UJ_CH : e;
+    for (u32 k = threadIdx.x; k < a.A; k += UJ_T) { qmin[k] = ~0ull; qmax[k] = 0; }
     __syncthreads();
-    for (u64 p = f + threadIdx.x; p < e; p += UJ_T) {          // Alg. 1 l.20-24 for the user's heads
-      uint2 v = a.pre_u[p];
-      if (v.x != ACT_HEAD) continue;                           // arrived, not filtered heads only
+    for (u64 p = c0 + threadIdx.x; p < c1; p += UJ_T) {
       u32 i = a.perm_u[p];
-      if (a.ovl && !a.ovl[i]) continue;
-      u64 q = a.pos_ua[i];
-      u64 lbu = a.lb_u[p], lba = a.lb_ua[q];
-      u64 n_g = (u64)a.pc_u[p] + 1 - a.pc_u[lbu], t_g = a.ptau_u[p] + v.y - a.ptau_u[lbu];
-      u64 n_a = (u64)a.pc_ua[q] + 1 - a.pc_ua[lba], t_a = a.ptau_ua[q] + v.y - a.ptau_ua[lba];
-      u32 app = m_app(a.meta[i]);
-      uint8_t st = FS_ST_ADMIT;
-      if (L.rg && n_g > L.rg) st = FS_ST_BLOCK_USER_REQ;
-      else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
-      else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
-      else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
-      if (st != a.status[i]) {
-        a.status[i] = st; chg = 1;
-        atomicMin(&fu, (unsigned long long)p); atomicMin(&fa, (unsigned long long)q);
-      }
+      u32 ap = m_app(a.meta[i]);
+      unsigned long long q = a.pos_ua[i];
+      atomicMin(&qmin[ap], q); atomicMax(&qmax[ap], q);
     }
     __syncthreads();
-    it++;
-    if (!chg) break;
-    f = fu; fq = fa;
+    u32 it = 0;
+    u32 cc_u; u64 ct_u;
+    for (;;) {
+      cc_u = ucc; ct_u = uct;
+      uj_scan(c0, c1, a.pre_u, a.status, a.pc_u, a.ptau_u, shc, sht, &cc_u, &ct_u);
+      for (u32 ap = 0; ap < a.A; ap++) {       // block-uniform loop over the chunk's apps
+        if (qmin[ap] == ~0ull) continue;
+        u32 c = acc[ap]; u64 tt = act_[ap];
+        uj_scan(qmin[ap], qmax[ap] + 1, a.pre_ua, a.status, a.pc_ua, a.ptau_ua, shc, sht, &c, &tt);
+        if (threadIdx.x == 0) { nacc[ap] = c; nact[ap] = tt; }
+      }
+      if (threadIdx.x == 0) chg = 0;
+      __syncthreads();
+      for (u64 p = c0 + threadIdx.x; p < c1; p += UJ_T) {       // Alg. 1 l.20-24 for the chunk's heads
+        uint2 v = a.pre_u[p];
+        if (v.x != ACT_HEAD) continue;                           // arrived, not filtered heads only
+        u32 i = a.perm_u[p];
+        if (a.ovl && !a.ovl[i]) continue;
+        u64 q = a.pos_ua[i];
+        u64 lbu = a.lb_u[p], lba = a.lb_ua[q];
+        u64 n_g = (u64)a.pc_u[p] + 1 - a.pc_u[lbu], t_g = a.ptau_u[p] + v.y - a.ptau_u[lbu];
+        u64 n_a = (u64)a.pc_ua[q] + 1 - a.pc_ua[lba], t_a = a.ptau_ua[q] + v.y - a.ptau_ua[lba];
+        u32 app = m_app(a.meta[i]);
+        uint8_t st = FS_ST_ADMIT;
+        if (L.rg && n_g > L.rg) st = FS_ST_BLOCK_USER_REQ;
+        else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
+        else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
+        else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
+        if (st != a.status[i]) { a.status[i] = st; chg = 1; }
+      }
+      __syncthreads();
+      it++;
+      if (!chg) break;
+      __syncthreads();
+    }
+    // the chunk is final (its last pass changed nothing): advance the carries past it
+    ucc = cc_u; uct = ct_u;
+    for (u32 ap = threadIdx.x; ap < a.A; ap += UJ_T)
+      if (qmin[ap] != ~0ull) { acc[ap] = nacc[ap]; act_[ap] = nact[ap]; }
     __syncthreads();
+    if (it > it_max) it_max = it;
   }
-  if (threadIdx.x == 0) atomicMax(a.iters, it);
+  if (threadIdx.x == 0) atomicMax(a.iters, it_max);
 }
 
 __global__ void k_act_list(u32 U, const u32* uchg, u32* list, u32* n) {
