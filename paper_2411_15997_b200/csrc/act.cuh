@@ -164,7 +164,39 @@ __global__ void k_act_flags(u64 n, const uint2* pre, const uint8_t* status, u32*
 struct ActDecideArgs {
   u64 n; const u32* meta; const uint8_t* ovl; const DLimits* L; const u32* ra; const u64* ta;
   ActOrder u, ua; uint8_t* status; u32* changed; const u32* user; u32* user_changed;
+  const uint4* hinfo;          // per user-order position of a checked head: {call, ua position, user, app}
 };
+// once per ACT call, per user-order position: the heads a pass must decide (arrived, not filtered,
+// overloaded) with their call id, (user, app)-order position, user and app -- so that each pass
+// walks the user order coalesced instead of scattering from call order into both orders
+__global__ void k_act_hinfo(u64 n, const uint2* pre_u, const u32* perm_u, const u32* pos_ua, const u32* meta,
+                            const u32* user, const uint8_t* ovl, uint4* hinfo) {
+  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  uint4 h = make_uint4(NONE32, 0, 0, 0);
+  if (pre_u[p].x == ACT_HEAD) {
+    u32 i = perm_u[p];
+    if (!ovl || ovl[i]) h = make_uint4(i, pos_ua[i], user[i], m_app(meta[i]));
+  }
+  hinfo[p] = h;
+}
+__global__ void k_act_decide_u(ActDecideArgs a) {
+  u64 pu = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pu >= a.n) return;
+  uint4 h = a.hinfo[pu];
+  if (h.x == NONE32) return;
+  u32 i = h.x, pa = h.y, app = h.w;
+  u64 lbu = a.u.lb[pu], lba = a.ua.lb[pa];
+  u64 n_g = a.u.pc[pu + 1] - a.u.pc[lbu], t_g = a.u.ptau[pu + 1] - a.u.ptau[lbu];
+  u64 n_a = a.ua.pc[pa + 1] - a.ua.pc[lba], t_a = a.ua.ptau[pa + 1] - a.ua.ptau[lba];
+  uint8_t st = FS_ST_ADMIT;
+  const DLimits& L = *a.L;
+  if (L.rg && n_g > L.rg) st = FS_ST_BLOCK_USER_REQ;
+  else if (L.tg && t_g > L.tg) st = FS_ST_BLOCK_USER_TOK;
+  else if (a.ra[app] && n_a > a.ra[app]) st = FS_ST_BLOCK_APP_REQ;
+  else if (a.ta[app] && t_a > a.ta[app]) st = FS_ST_BLOCK_APP_TOK;
+  if (st != a.status[i]) { a.status[i] = st; *a.changed = 1; a.user_changed[h.z] = 1; }
+}
 __global__ void k_act_decide(ActDecideArgs a) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;

@@ -528,6 +528,10 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
     if (S.failed) return FS_E_NOMEM;
     FS_LAUNCH(ctx, "act_pre", k_act_pre, div_up(n, B), B, 0, n, ao->o.perm, apk, ao->ts, ao->pre);
   }
+  uint4* hinfo = S.alloc<uint4>(n);
+  if (S.failed) return FS_E_NOMEM;
+  FS_LAUNCH(ctx, "act_hinfo", k_act_hinfo, div_up(n, B), B, 0, n, ou.pre, ou.o.perm, oua.pos, t.meta, t.user, overloaded,
+            hinfo);
   u32* changed = S.alloc<u32>(1);
   u32* uchg = S.alloc<u32>(t.U + 1);
   u32* ulist = S.alloc<u32>(t.U + 1);
@@ -546,8 +550,8 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
       excl_scan<u32>(ctx, S, ao->flag, ao->pc, n, ao->pc + n);
       excl_scan<u64>(ctx, S, ao->tau, ao->ptau, n, ao->ptau + n);
     }
-    ActDecideArgs da{n, t.meta, overloaded, LD.L, LD.ra, LD.ta, ou, oua, status, changed, t.user, uchg};
-    FS_LAUNCH(ctx, "act_decide", k_act_decide, div_up(n, B), B, 0, da);
+    ActDecideArgs da{n, t.meta, overloaded, LD.L, LD.ra, LD.ta, ou, oua, status, changed, t.user, uchg, hinfo};
+    FS_LAUNCH(ctx, "act_decide", k_act_decide_u, div_up(n, B), B, 0, da);
     passes++;
     u32 hc = 0;
     cudaMemcpyAsync(&hc, changed, 4, cudaMemcpyDeviceToHost, ctx->stream);
