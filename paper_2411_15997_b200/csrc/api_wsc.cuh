@@ -379,7 +379,9 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   eo.adm_app = o.admitted_per_app;
   if (eo.arrive && !eo.ovl) eo.arrive = nullptr;          // arrive/ovl are written together
   if (eo.admit && !eo.order) eo.admit = nullptr;
+  static const int rwarp = [] { const char* v = getenv("FS_REPLAY_WARP"); return v ? atoi(v) : 1; }();
   size_t budget = ctx->smem_optin ? ctx->smem_optin - 512 : 100 * 1024;
+  if (rwarp) budget -= sizeof(HEnt) * 32 + 64;             // the warp engine's static head batch
   fs_replay_summary* dsum = S.alloc<fs_replay_summary>(1);
   int* dcode = S.zeros<int>(1);
   u64* didx = S.zeros<u64>(1);
@@ -395,14 +397,15 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
     // queued-continuation pool: same two-step capacity (n_inters is an exact bound)
     const bool ag = wi && cfg->act.app_scope == FS_SCOPE_APP_GLOBAL;
     const u32 all = (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull);        // exact log capacities
-    EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, true, budget,
+    EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, !rwarp, budget,
                              cfg->mode >= FS_MODE_VTC, cfg->mode == FS_MODE_RPM ? all : 0, t.A, ag ? all : 0);
     unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
     if (S.failed) return FS_E_NOMEM;
     ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
-    auto rk = (cfg->mode >= FS_MODE_VTC || ag) ? k_replay<true> : k_replay<false>;
+    const bool base = cfg->mode >= FS_MODE_VTC || ag;
+    auto rk = rwarp ? (base ? k_replay_warp<true> : k_replay_warp<false>) : (base ? k_replay<true> : k_replay<false>);
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
-    FS_LAUNCH(ctx, "wsc_replay", rk, 1, 64, L.bytes_smem, a);
+    FS_LAUNCH(ctx, "wsc_replay", rk, 1, rwarp ? 32 : 64, L.bytes_smem, a);
     cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
     cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
     rc = finish(ctx, &S);

@@ -917,6 +917,30 @@ struct ReplayKArgs {
 
 // single replay: one CTA of two warps -- warp 0 lane 0 runs the serial engine,
 // warp 1 streams head arrivals into the shared ring
+// single replay, one warp: the 32 lanes run the engine in lockstep and refill the head batch
+// together (the sweep's engine; state in shared memory first)
+template <bool BASE>
+__global__ void __launch_bounds__(32) k_replay_warp(const __grid_constant__ ReplayKArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ HEnt hbs[32];
+  EngState st;
+  eng_bind(a.L, sm, a.gmem, a.p_cap, &st, nullptr);
+  u64 AJ = (u64)a.sh.A * a.sh.J1;
+  st.W = a.L.smem[L_W] ? st.W : (u64*)a.cfg.W;
+  eng_clear(st, a.sh, a.cfg.W, AJ, a.U, threadIdx.x, 32);
+  __syncwarp();
+  __threadfence_block();
+  EngineT<HS_WARP, 32, BASE> E;
+  E.init(&a.sh, &a.cfg, st, a.out, a.U);
+  E.hb = hbs;
+  E.run();
+  if (threadIdx.x == 0) {
+    *a.sum = E.sum;
+    *a.err_code = E.err_code ? E.err_code + 1 : 0;
+    *a.err_idx = E.err_idx;
+  }
+}
+
 template <bool BASE>
 __global__ void __launch_bounds__(64) k_replay(const __grid_constant__ ReplayKArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
