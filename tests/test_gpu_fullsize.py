@@ -90,3 +90,23 @@ def test_sweep_c5_full():
         assert s["n_arrived"] + s["n_dropped"] + s["n_filtered"] == tr["n_calls"]
         assert sum(s["n_block"]) <= int((heads & part).sum())
         assert s["u_min"] <= s["u_max"]
+
+
+def test_profile_c4_full():
+    """The 100M-call C4 profile (bench.py --workload c4 at one GPU) against the oracle's golden:
+    every table bit-exact (sha256), interpolated quantiles within 1e-6."""
+    path = os.path.join(GOLD, "full_c4.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = json.load(open(path))
+    from paper_2411_15997_b200 import build, fairserve as F
+    build.build()
+    ctx = F.Context(0)
+    tr = G.generate("c4")
+    assert tr["n_calls"] == g["n_calls"]
+    p = F.build_app_profiles(ctx, F.Trace(tr), g["profile_cfg"]).read()
+    for k, v in g["profile"].items():
+        assert p[k].tolist() == v, k
+    for k, v in g["profile_sha"].items():
+        assert h(p[k]) == v, k
+    np.testing.assert_allclose(p["interp_q"], np.array(g["interp_q"]), rtol=1e-6)

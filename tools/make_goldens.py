@@ -90,6 +90,29 @@ def run_c5(n_sample=12):
     print("c5 sample written", path, out["oracle_seconds"], flush=True)
 
 
+def run_c4():
+    """C4: the 100M-call profile (bench.py --workload c4 at one GPU builds exactly this trace)."""
+    t0 = time.time()
+    tr = G.generate("c4")
+    t1 = time.time()
+    pcfg = dict(tier_max=0, window_ms=60000, max_stage=64)
+    p = O.profile(tr, pcfg)
+    out = {
+        "citation": "written by tools/make_goldens.py from oracle/ only (SURVEY.md §8(c) O2); inputs: tracegen config c4",
+        "config": "c4", "n_calls": tr["n_calls"], "profile_cfg": pcfg,
+        "profile": {k: p[k].tolist() for k in ("T_req_a", "T_tok_a", "T_req_g", "T_tok_g", "nr_peak_r_a",
+                                                "nr_peak_t_a", "maxstage")},
+        "profile_sha": {k: h(p[k]) for k in ("cnt", "sum_in", "sum_sys", "sum_out", "hist", "nr_q", "peak_r_u",
+                                             "peak_t_u", "peak_r_ua", "peak_t_ua")},
+        "interp_q": p["interp_q"].tolist(),
+        "oracle_seconds": {"generate": t1 - t0, "profile": time.time() - t1},
+    }
+    path = os.path.join(ROOT, "tests", "golden", "full_c4.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("c4 written", path, out["oracle_seconds"], flush=True)
+
+
 if __name__ == "__main__":
     for nm in sys.argv[1:] or ["c2"]:
-        run_c5() if nm == "c5" else run(nm)
+        run_c5() if nm == "c5" else run_c4() if nm == "c4" else run(nm)
