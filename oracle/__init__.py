@@ -77,7 +77,8 @@ class _Trace(C.Structure):
 class _ProfileCfg(C.Structure):
     _fields_ = [("window_ms", C.c_uint32), ("max_stage", C.c_uint32), ("tier_max", C.c_uint32),
                 ("n_q", C.c_uint32), ("q_ppm", P32), ("limit_q_ppm", C.c_uint32),
-                ("limit_mult_q8", C.c_uint32), ("count_mode", C.c_uint32)]
+                ("limit_mult_q8", C.c_uint32), ("count_mode", C.c_uint32),
+                ("tau_w_in", C.c_uint32), ("tau_w_sys", C.c_uint32), ("tau_w_out", C.c_uint32)]
 
 
 class _ProfileOut(C.Structure):
@@ -100,7 +101,8 @@ class _ActCfg(C.Structure):
     _fields_ = [("window_ms", C.c_uint32), ("limits_from_profile", C.c_uint32),
                 ("limit_mult_q8", C.c_uint32), ("T_req_g", C.c_uint32), ("T_req_a", P32),
                 ("T_tok_g", C.c_uint64), ("T_tok_a", P64), ("count_mode", C.c_uint32),
-                ("app_scope", C.c_uint32), ("tier_max", C.c_uint32)]
+                ("app_scope", C.c_uint32), ("tier_max", C.c_uint32),
+                ("tau_w_in", C.c_uint32), ("tau_w_sys", C.c_uint32), ("tau_w_out", C.c_uint32)]
 
 
 class _ActSummary(C.Structure):
@@ -185,7 +187,7 @@ def profile(tr, cfg=None):
     nq = len(q)
     c = _ProfileCfg(cfg.get("window_ms", 60000), J, cfg.get("tier_max", 255), nq, _p(q, P32),
                     cfg.get("limit_q_ppm", 990000), cfg.get("limit_mult_q8", 256),
-                    cfg.get("count_mode", 0))
+                    cfg.get("count_mode", 0), *cfg.get("tau_weights", (0, 0, 0)))
     o = dict(cnt=np.zeros((A, J + 1), np.uint64), sum_in=np.zeros((A, J + 1), np.uint64),
              sum_sys=np.zeros((A, J + 1), np.uint64), sum_out=np.zeros((A, J + 1), np.uint64),
              ohat=np.zeros((A, J + 1), np.uint64), maxstage=np.zeros(A, np.uint32),
@@ -246,7 +248,7 @@ def _act_cfg(cfg, keep):
     return _ActCfg(cfg.get("window_ms", 60000), cfg.get("limits_from_profile", 1),
                    cfg.get("limit_mult_q8", 0), cfg.get("T_req_g", 0), _p(Ta, P32),
                    cfg.get("T_tok_g", 0), _p(Tt, P64), cfg.get("count_mode", 0),
-                   cfg.get("app_scope", 0), cfg.get("tier_max", 255))
+                   cfg.get("app_scope", 0), cfg.get("tier_max", 255), *cfg.get("tau_weights", (0, 0, 0)))
 
 
 def act(tr, prof, cfg=None, overloaded=None, t_ns_override=None):

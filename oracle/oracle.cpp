@@ -115,7 +115,16 @@ typedef struct {
   u32 window_ms, max_stage, tier_max, n_q;
   const u32* q_ppm;
   u32 limit_q_ppm, limit_mult_q8, count_mode;
+  u32 tau_w_in, tau_w_sys, tau_w_out;        // NEXT-3 weighted token load (R11); all 0 = (1, 1, 1)
 } or_profile_cfg;
+
+// token load of a call (Q8; weighted variant R11): w_in L_I + w_sys L_S + w_out O-hat(a, j')
+struct TauW { u64 wi, ws, wo; };
+static TauW tau_weights(u32 wi, u32 ws, u32 wo) {
+  if (!wi && !ws && !wo) return TauW{1, 1, 1};
+  return TauW{wi, ws, wo};
+}
+static bool tau_weights_ok(u32 wi, u32 ws, u32 wo) { return wi < 16 && ws < 16 && wo < 16; }
 
 typedef struct {          // every array caller-allocated; J = max_stage
   u64 *cnt, *sum_in, *sum_sys, *sum_out, *ohat;   // [A][J+1], index j in 1..J
@@ -169,7 +178,7 @@ static u64 limit_from(u64 nr, u32 k_q8) {   // T = max(1, ceil(k*NR)) in Q8; emp
 
 extern "C" int or_profile(const or_trace* t, const or_profile_cfg* cfg, or_profile_out* o, u64* bad_index) {
   if (!t || !cfg || !o || cfg->max_stage == 0 || cfg->max_stage > 255 ||
-      cfg->limit_q_ppm > 1000000) return E_INVAL;
+      cfg->limit_q_ppm > 1000000 || !tau_weights_ok(cfg->tau_w_in, cfg->tau_w_sys, cfg->tau_w_out)) return E_INVAL;
   for (u32 k = 0; k < cfg->n_q; k++) if (cfg->q_ppm[k] > 1000000) return E_INVAL;
   int rc = or_validate(t, bad_index, nullptr, nullptr);
   if (rc) return rc;
@@ -223,9 +232,10 @@ extern "C" int or_profile(const or_trace* t, const or_profile_cfg* cfg, or_profi
     if (cfg->count_mode == COUNT_HEADS && stage_of(t, i) != 1) continue;
     per_user[t->user[i]].push_back(i);
   }
+  const TauW tw = tau_weights(cfg->tau_w_in, cfg->tau_w_sys, cfg->tau_w_out);
   auto tau = [&](u64 x) -> u64 {
     u32 a = app_of(t, x), j = std::min(stage_of(t, x), J);
-    return (u64)t->len_in[x] + t->len_sys[x] + o->ohat[(u64)a * J1 + j];
+    return tw.wi * t->len_in[x] + tw.ws * t->len_sys[x] + tw.wo * o->ohat[(u64)a * J1 + j];
   };
   const i64 W = cfg->window_ms;
   for (u64 k = 0; k < (u64)U * A; k++) { o->peak_r_ua[k] = 0; o->peak_t_ua[k] = 0; }
@@ -292,6 +302,7 @@ typedef struct {
   u32 T_req_g; const u32* T_req_a;
   u64 T_tok_g; const u64* T_tok_a;
   u32 count_mode, app_scope, tier_max;
+  u32 tau_w_in, tau_w_sys, tau_w_out;        // R11; all 0 = (1, 1, 1)
 } or_act_cfg;
 
 struct Limits { u32 rg; u64 tg; std::vector<u32> ra; std::vector<u64> ta; bool tokens; };
@@ -350,7 +361,8 @@ typedef struct { u64 n_in, n_admit, n_block[4], n_dropped, n_filtered, n_inter_b
 extern "C" int or_act(const or_trace* t, const or_profile_view* p, const or_act_cfg* c,
            const uint8_t* overloaded, const i64* t_ns_override,
            uint8_t* status, or_act_summary* s, u64* bad_index) {
-  if (!t || !c || !status || c->app_scope > 1 || c->count_mode > 1) return E_INVAL;
+  if (!t || !c || !status || c->app_scope > 1 || c->count_mode > 1 ||
+      !tau_weights_ok(c->tau_w_in, c->tau_w_sys, c->tau_w_out)) return E_INVAL;
   // app-global counters (NEXT-3, R10): explicit limits only
   if (c->app_scope == 1 && (c->limits_from_profile || c->limit_mult_q8)) return E_INVAL;
   if (p && p->A != t->A) { *bad_index = 0; return E_PROFILE; }
@@ -362,12 +374,13 @@ extern "C" int or_act(const or_trace* t, const or_profile_view* p, const or_act_
   if (rc) return rc;
   if (L.tokens && !p) return E_INVAL;
   std::vector<u64> tau(t->n, 0);
+  const TauW tw = tau_weights(c->tau_w_in, c->tau_w_sys, c->tau_w_out);
   if (L.tokens)
     for (u64 i = 0; i < t->n; i++) {
       if (tier_of(t, i) > c->tier_max) continue;
       u64 k;
       if (!profile_slot(p, app_of(t, i), stage_of(t, i), &k)) { *bad_index = i; return E_PROFILE; }
-      tau[i] = (u64)t->len_in[i] + t->len_sys[i] + ohat_at(p, k);
+      tau[i] = tw.wi * t->len_in[i] + tw.ws * t->len_sys[i] + tw.wo * ohat_at(p, k);
     }
   auto tns = [&](u64 i) -> i64 { return t_ns_override ? t_ns_override[i] : (i64)t->t_ms[i] * 1000000; };
   // a continuation that arrives must come after its (arrived) head in (t, id) order
@@ -535,7 +548,8 @@ struct Sched {
     bool head = stage_of(t, r) == 1;
     u64 tau_r = 0;
     if (c->mode == 1) {
-      tau_r = prompt(r) + reserve(r);
+      const TauW tw = tau_weights(c->act.tau_w_in, c->act.tau_w_sys, c->act.tau_w_out);
+      tau_r = tw.wi * t->len_in[r] + tw.ws * t->len_sys[r] + tw.wo * reserve(r);
       if (c->act.count_mode == COUNT_ALL || head) {
         logs[k].push_back(std::make_tuple(tr, tau_r, a));                                        // l.19
         if (c->act.app_scope == 1) glog.push_back(std::make_tuple(tr, tau_r, a));
@@ -602,7 +616,8 @@ static int sched_init(Sched& S, const or_trace* t, const or_profile_view* p, con
   if (!t || !p || !c || c->max_batch == 0 || c->mode > 4 || c->alpha >= 256 || c->beta >= 256 ||
       c->gamma >= 256 || c->prio_benign_q16 >= (1u << 24) || c->prio_abusive_q16 >= (1u << 24))
     return E_INVAL;
-  if ((c->mode == 1 || c->mode == 3) && (c->act.app_scope > (c->mode == 1 ? 1u : 0u) || c->act.count_mode > 1))
+  if ((c->mode == 1 || c->mode == 3) && (c->act.app_scope > (c->mode == 1 ? 1u : 0u) || c->act.count_mode > 1 ||
+                                          !tau_weights_ok(c->act.tau_w_in, c->act.tau_w_sys, c->act.tau_w_out)))
     return E_INVAL;
   if (c->mode == 1 && c->act.app_scope == 1 && (c->act.limits_from_profile || c->act.limit_mult_q8))
     return E_INVAL;                                                  // app-global: explicit limits (R10)

@@ -66,6 +66,9 @@ class Sched:
         self.Wn = act.get("window_ms", 60000) * 1_000_000
         self.heads_only = act.get("count_mode", 0) == 1
         self.app_global = act.get("app_scope", 0) == 1   # NEXT-3: c_a over every user (R10)
+        self.tw = tuple(act.get("tau_weights", (0, 0, 0))) or (0, 0, 0)
+        if self.tw == (0, 0, 0):                         # R11: weighted token load
+            self.tw = (1, 1, 1)
         self.u = [0] * self.U
         self.Q = []              # (call id, seq, is_cont) in delivery order
         self.e = None
@@ -110,7 +113,7 @@ class Sched:
                     self.u[k] = max(self.u[k], self.u[self.e])           # l.13-15
             else:
                 self.u[k] = max(self.u[k], min(self.u[self.calls[q[0]]["user"]] for q in Q))  # l.16-18
-        tau = c["L_I"] + c["L_S"] + self.reserve(c)
+        tau = self.tw[0] * c["L_I"] + self.tw[1] * c["L_S"] + self.tw[2] * self.reserve(c)
         if self.mode == 1 and (not self.heads_only or c["stage"] == 1):
             self.log.append((t, tau, k, c["app"]))                     # l.19
         st = ADMIT
@@ -267,6 +270,8 @@ def act(tr, ohat, cfg, overloaded=None, t_ns_override=None, limits=None):
     Wn = cfg.get("window_ms", 60000) * 1_000_000
     heads_only = cfg.get("count_mode", 0) == 1
     app_global = cfg.get("app_scope", 0) == 1
+    tw = tuple(cfg.get("tau_weights", (0, 0, 0)))
+    tw = (1, 1, 1) if tw == (0, 0, 0) else tw
     tier_max = cfg.get("tier_max", 255)
     Trg, Ttg, Tra, Tta = limits
     tns = [(int(t_ns_override[i]) if t_ns_override is not None else calls[i]["t_ms"] * 1_000_000) for i in range(n)]
@@ -299,7 +304,7 @@ def act(tr, ohat, cfg, overloaded=None, t_ns_override=None, limits=None):
 
         win = [x for x in range(n) if calls[x]["user"] == c["user"] and (tns[x], x) <= (tns[i], i)
                and tns[i] - Wn < tns[x] and counted(x)]
-        tau = lambda x: calls[x]["L_I"] + calls[x]["L_S"] + ohat(calls[x])
+        tau = lambda x: tw[0] * calls[x]["L_I"] + tw[1] * calls[x]["L_S"] + tw[2] * ohat(calls[x])
         n_g, tau_g = len(win), sum(tau(x) for x in win)
         pool = win
         if app_global:           # every user's counted calls (R10)

@@ -171,6 +171,69 @@ def test_replay_vs_stepper_app_global(seed):
     assert s["digest"] == es["digest"] and s["n_block"] == es["n_block"]
 
 
+@pytest.mark.parametrize("seed", range(150))
+def test_act_vs_recount_tau_weighted(seed):
+    """NEXT-3 weighted token load (R11): tau = w_in L_I + w_sys L_S + w_out O-hat, vs the recount."""
+    rng = np.random.default_rng(17000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=2, n_apps=A, max_inters=5, max_calls=9)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    prof = O.profile_from_host(A, J, cnt, si, ss, so)
+    n = tr["n_calls"]
+    tw = tuple(int(x) for x in rng.integers(0, 4, size=3))
+    cfg = dict(window_ms=int(rng.choice((1, 2, 4))), limits_from_profile=0, T_req_g=int(rng.choice((0, 2))),
+               T_req_a=[int(rng.choice((0, 2))) for _ in range(A)], T_tok_g=int(rng.choice((0, 8, 20))),
+               T_tok_a=[int(rng.choice((0, 6, 15))) for _ in range(A)], count_mode=int(rng.integers(0, 2)),
+               tier_max=255, app_scope=int(rng.integers(0, 2)), tau_weights=tw)
+    ovl = (rng.random(n) < 0.7).astype(np.uint8)
+    st, _ = O.act(tr, prof, cfg, overloaded=ovl)
+
+    def ohat(c):
+        j = S._slot(prof, c["app"], c["stage"])
+        return int(prof["sum_out"][c["app"]][j]) // int(prof["cnt"][c["app"]][j])
+
+    ref = S.act(tr, ohat, cfg, overloaded=ovl,
+                limits=(cfg["T_req_g"], cfg["T_tok_g"], cfg["T_req_a"], cfg["T_tok_a"]))
+    assert list(st) == ref
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_replay_vs_stepper_tau_weighted(seed):
+    rng = np.random.default_rng(18000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(1, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    prof = O.profile_from_host(A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A, modes=(1,))
+    cfg["act"]["tau_weights"] = tuple(int(x) for x in rng.integers(0, 4, size=3))
+    cfg["act"]["app_scope"] = int(rng.integers(0, 2))
+    if _oversize(tr, prof, cfg):
+        return
+    o, s = O.replay(tr, prof, cfg)
+    eo, es = S.replay(tr, prof, cfg)
+    for k in ("status", "admit_ns", "order", "counters"):
+        assert list(o[k]) == list(eo[k]), (k, seed)
+    assert s["digest"] == es["digest"]
+
+
+def test_tau_weighted_example():
+    """R11 by hand: one call L_I = 10, L_S = 5, profiled output mean O-hat = 20; weights (2, 0, 1)
+    give tau = 40: T_tok_g = 39 blocks it (USER_TOK), 40 admits it; the profile's token peak of
+    the user is 40 too."""
+    from paper_2411_15997_b200.tracegen import from_columns
+    tr = from_columns(1, 1, [dict(user=0, t_ms=0, app=0, inter=0, stage=1, ncalls=1, len_in=10, len_sys=5,
+                                  len_out=20)])
+    prof = O.profile_from_host(1, 1, [[0, 1]], [[0, 10]], [[0, 5]], [[0, 20]])
+    base = dict(window_ms=60000, limits_from_profile=0, tau_weights=(2, 0, 1))
+    assert list(O.act(tr, prof, dict(base, T_tok_g=39))[0]) == [2]
+    assert list(O.act(tr, prof, dict(base, T_tok_g=40))[0]) == [0]
+    p = O.profile(tr, dict(tier_max=255, tau_weights=(2, 0, 1)))
+    assert int(p["peak_t_u"][0]) == 40
+    assert int(O.profile(tr, dict(tier_max=255))["peak_t_u"][0]) == 35
+    with pytest.raises(O.OracleError):
+        O.act(tr, prof, dict(base, tau_weights=(16, 0, 1)))
+
+
 def test_app_global_example():
     """S:217 (c^r_a over the app's arrivals): user 0's head and then user 1's head of the same app
     inside one window, T^r_a = 1, always overloaded -> user 1 is blocked (APP_REQ) with app-global
