@@ -82,6 +82,9 @@ typedef struct {
   uint32_t limit_q_ppm;     /* quantile for derived limits (990000) */
   uint32_t limit_mult_q8;   /* k in Q8 (256 = 1.0) */
   uint32_t count_mode;      /* FS_COUNT_ALL_ARRIVALS | FS_COUNT_HEADS_ONLY */
+  uint32_t tau_w_in, tau_w_sys, tau_w_out;   /* NEXT-3 (R11): token load tau = w_in L_I + w_sys L_S +
+                                                w_out O-hat for the window token peaks; all 0 = (1,1,1);
+                                                each < 16 (else FS_E_INVAL) */
 } fs_profile_cfg;
 int fs_build_app_profiles(fs_ctx* ctx, const fs_trace* trace, const fs_profile_cfg* cfg, fs_profile** out);
 /* explicit profile (tests, what-ifs): host arrays [n_apps][max_stage+1], index = stage (0 unused) */
@@ -152,6 +155,8 @@ typedef struct {
   uint32_t T_req_g; const uint32_t* T_req_a_h;   /* 0 = check disabled */
   uint64_t T_tok_g; const uint64_t* T_tok_a_h;   /* 0 = check disabled */
   uint32_t count_mode, app_scope, tier_max;
+  uint32_t tau_w_in, tau_w_sys, tau_w_out;       /* NEXT-3 (R11) weighted token load, as in fs_profile_cfg;
+                                                    fs_sweep: one set for all FS(W+I) scenarios */
 } fs_act_cfg;
 typedef struct {
   uint64_t n_in, n_admit, n_block[4], n_dropped, n_filtered, n_inter_blocked, n_not_arrived;

@@ -56,6 +56,7 @@ struct ActPrepArgs {
   DTrace t; u32 tier_max, J; const u32* maxstage; const u64* cnt; const u64* sum_out;
   const DLimits* L; const i64* t_override; const u32* head_of;
   DevErr* err; u64* tau; uint8_t* status;
+  TauW w;                                  // token load weights (R11)
 };
 // per call: tau (token load), initial status, ordering check of arrived continuations
 __global__ void k_act_prep(ActPrepArgs a) {
@@ -67,7 +68,7 @@ __global__ void k_act_prep(ActPrepArgs a) {
   if (!filt && a.L->tokens) {
     u64 k;
     if (!prof_slot(a.J, a.maxstage, a.cnt, m_app(m), m_stage(m), &k)) report(a.err, ERR_PROFILE, i);
-    else tau = (u64)a.t.len_in[i] + a.t.len_sys[i] + a.sum_out[k] / a.cnt[k];
+    else tau = (u64)a.w.wi * a.t.len_in[i] + (u64)a.w.ws * a.t.len_sys[i] + (u64)a.w.wo * (a.sum_out[k] / a.cnt[k]);
   }
   a.tau[i] = tau;
   if (a.t_override) {

@@ -23,16 +23,22 @@ __global__ void k_posmap(u64 n, const u32* list, u32* pos) {
   u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (p < n) pos[list[p]] = (u32)p;
 }
-// head token load tau = L_I + L_S + O-hat(app, stage 1) (0 if the profile has no slot)
+// head token load tau = w_in L_I + w_sys L_S + w_out O-hat(app, stage 1) (O-hat 0 if the profile
+// has no slot; weights (1, 1, 1) unless R11)
 __global__ void k_hw_gather(u64 n, const u32* list, DTrace t, u32 J, const u32* maxstage, const u64* cnt,
-                            const u64* ohat, u32* ts, u64* tau) {
+                            const u64* ohat, u32* ts, u64* tau, TauW w) {
   u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   u32 i = list[p], m = t.meta[i];
   u64 k, r = 0;
   if (prof_slot(J, maxstage, cnt, m_app(m), 1, &k)) r = ohat[k];
   ts[p] = t.t_ms[i];
-  tau[p] = (u64)t.len_in[i] + t.len_sys[i] + r;
+  tau[p] = (u64)w.wi * t.len_in[i] + (u64)w.ws * t.len_sys[i] + (u64)w.wo * r;
+}
+// weighted token load per call (R11) for the engine's window logs: w_in L_I + w_sys L_S + w_out R
+__global__ void k_tau_call(u64 n, const uint4* recB, const uint4* recC, TauW w, u32* tau) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tau[i] = w.wi * recC[i].z + w.ws * recC[i].w + w.wo * recB[i].w;
 }
 // static window over the heads of a segment: count and load of heads in (t - W, t], <= own position
 __global__ void k_hw_win(u64 n, const u32* list, const u32* key, const u64* seg, const u32* ts, const u64* ptau,
@@ -107,7 +113,7 @@ struct WscShared {
 
 // ring_cap: per-user ACT ring capacity cap (0 = exact: the user's continuation count)
 static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profile* P, u32 window_ms, bool windows,
-                       u64 ring_cap, WscShared* W) {
+                       u64 ring_cap, WscShared* W, TauW tw = TauW{1, 1, 1}) {
   u64 n = t.n;
   int B = 256;
   build_links(ctx, S, t, &W->L);
@@ -155,7 +161,7 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
     if (S.failed) return false;
     // per user
     FS_LAUNCH(ctx, "hw_gather", k_hw_gather, div_up(nh, B), B, 0, (u64)nh, W->uh_list, t, P->J, P->maxstage, P->cnt,
-              P->ohat, ts, tau);
+              P->ohat, ts, tau, tw);
     excl_scan<u64>(ctx, S, tau, ptau, nh, ptau + nh);
     FS_LAUNCH(ctx, "hw_win", k_hw_win, div_up(nh, B), B, 0, (u64)nh, W->uh_list, skeys, W->uh_off, ts, ptau, Wms,
               (const u32*)nullptr, W->hw_ng, W->hw_tg);
@@ -170,7 +176,7 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
     if (S.failed) return false;
     FS_LAUNCH(ctx, "seg_bounds", k_seg_bounds<u32>, div_up(nseg + 1, B), B, 0, k2s, (u64)nh, nseg, seg2);
     FS_LAUNCH(ctx, "hw_gather", k_hw_gather, div_up(nh, B), B, 0, (u64)nh, l2, t, P->J, P->maxstage, P->cnt, P->ohat,
-              ts, tau);
+              ts, tau, tw);
     excl_scan<u64>(ctx, S, tau, ptau, nh, ptau + nh);
     FS_LAUNCH(ctx, "hw_win", k_hw_win, div_up(nh, B), B, 0, (u64)nh, l2, k2s, seg2, ts, ptau, Wms, posmap, W->hw_na,
               W->hw_ta);
@@ -181,6 +187,13 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
   sh.hw_ng = W->hw_ng; sh.hw_tg = W->hw_tg; sh.hw_na = W->hw_na; sh.hw_ta = W->hw_ta;
   sh.utier = W->utier; sh.tier_calls = W->tier_calls; sh.r_off = W->r_off;
   sh.A = t.A; sh.J1 = P->J + 1;
+  sh.tau_w = nullptr;
+  if (!tau_w_unit(tw) && n) {
+    u32* tc = S.alloc<u32>(n);
+    if (S.failed) return false;
+    FS_LAUNCH(ctx, "tau_call", k_tau_call, div_up(n, B), B, 0, n, W->recB, W->recC, tw, tc);
+    sh.tau_w = tc;
+  }
   return true;
 }
 
@@ -353,7 +366,8 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   if (out) o = *out;
   const bool wi = cfg->mode == FS_MODE_WI;
   WscShared W;
-  if (!wsc_shared(ctx, S, t, P, cfg->act.window_ms, wi, 0, &W)) return FS_E_NOMEM;
+  if (!wsc_shared(ctx, S, t, P, cfg->act.window_ms, wi, 0, &W,
+                  tau_w(cfg->act.tau_w_in, cfg->act.tau_w_sys, cfg->act.tau_w_out))) return FS_E_NOMEM;
   int rc = finish(ctx, &S);
   if (rc) return rc;
   ScenTables T;
@@ -434,8 +448,11 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
     any_ag |= scen[s].mode == FS_MODE_WI && scen[s].act.app_scope == FS_SCOPE_APP_GLOBAL;
     if (!replay_cfg_ok(&scen[s]) || scen[s].prio_q16) return FS_E_INVAL;
     if (scen[s].mode == FS_MODE_WI) {
-      for (u32 q = 0; q < s; q++)          // one static head window per call
-        if (scen[q].mode == FS_MODE_WI && scen[q].act.window_ms != scen[s].act.window_ms) return FS_E_INVAL;
+      for (u32 q = 0; q < s; q++)          // one static head window and token load per call
+        if (scen[q].mode == FS_MODE_WI &&
+            (scen[q].act.window_ms != scen[s].act.window_ms || scen[q].act.tau_w_in != scen[s].act.tau_w_in ||
+             scen[q].act.tau_w_sys != scen[s].act.tau_w_sys || scen[q].act.tau_w_out != scen[s].act.tau_w_out))
+          return FS_E_INVAL;
       any_wi = true;
     }
     Bmax = std::max(Bmax, scen[s].max_batch);
@@ -445,9 +462,14 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   err_reset(ctx);
   DTrace t = dtrace(tr);
   u32 win = scen[0].act.window_ms;
-  for (u32 s = 0; s < ns; s++) if (scen[s].mode == FS_MODE_WI) { win = scen[s].act.window_ms; break; }
+  TauW tw{1, 1, 1};
+  for (u32 s = 0; s < ns; s++)
+    if (scen[s].mode == FS_MODE_WI) {
+      win = scen[s].act.window_ms; tw = tau_w(scen[s].act.tau_w_in, scen[s].act.tau_w_sys, scen[s].act.tau_w_out);
+      break;
+    }
   WscShared W;
-  if (!wsc_shared(ctx, S, t, P, win, any_wi, SWEEP_RING_CAP, &W)) return FS_E_NOMEM;
+  if (!wsc_shared(ctx, S, t, P, win, any_wi, SWEEP_RING_CAP, &W, tw)) return FS_E_NOMEM;
   int rc = finish(ctx, &S);
   if (rc) return rc;
   ScenTables T;
@@ -596,7 +618,8 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
   st->t = dtrace(tr);
   st->U = tr->n_users;
   // ring capacity per user = all its calls (heads and continuations are logged)
-  if (!wsc_shared(ctx, S, st->t, P, cfg->act.window_ms, false, 0, &st->W)) { delete st; return FS_E_NOMEM; }
+  if (!wsc_shared(ctx, S, st->t, P, cfg->act.window_ms, false, 0, &st->W,
+                  tau_w(cfg->act.tau_w_in, cfg->act.tau_w_sys, cfg->act.tau_w_out))) { delete st; return FS_E_NOMEM; }
   int rc = finish(ctx, &S);
   if (rc) { delete st; return rc; }
   if (!scen_tables(ctx, S, st->t, P, cfg, 1, &st->T)) { delete st; return FS_E_NOMEM; }

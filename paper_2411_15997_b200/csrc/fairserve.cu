@@ -135,7 +135,7 @@ extern "C" int fs_ctx_timing_read(fs_ctx* c, fs_kernel_time* out, int cap, int* 
 // ------------------------------------------------------------------ profiles
 static bool prof_cfg_ok(const fs_profile_cfg* c) {
   if (!c || c->max_stage == 0 || c->max_stage > 255 || c->limit_q_ppm > 1000000 || c->n_q > QMAX ||
-      (c->n_q && !c->q_ppm_h) || c->count_mode > 1)
+      (c->n_q && !c->q_ppm_h) || c->count_mode > 1 || !tau_w_ok(c->tau_w_in, c->tau_w_sys, c->tau_w_out))
     return false;
   for (u32 k = 0; k < c->n_q; k++) if (c->q_ppm_h[k] > 1000000) return false;
   return true;
@@ -289,7 +289,8 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
     cudaMemsetAsync(P->peak_t_ua, 0, (u64)U * A * 8, ctx->stream);
     uint2* wpk = pp->S->alloc<uint2>(pp->t.n + 1);
     if (pp->t.n && wpk) {
-      WinPackArgs wp{pp->t, J, pp->cfg.tier_max, pp->cfg.count_mode, P->ohat, wpk};
+      WinPackArgs wp{pp->t, J, pp->cfg.tier_max, pp->cfg.count_mode, P->ohat, wpk,
+                     tau_w(pp->cfg.tau_w_in, pp->cfg.tau_w_sys, pp->cfg.tau_w_out)};
       FS_LAUNCH(ctx, "win_pack", k_win_pack, div_up(pp->t.n, B), B, 0, wp);
     }
     prof_windows(pp, pp->ou, wpk, P->peak_r_u, P->peak_t_u);
@@ -430,7 +431,8 @@ extern "C" void fs_profile_free(fs_profile* P) {
 
 // ------------------------------------------------------------------ ACT
 static bool act_cfg_ok(const fs_act_cfg* c) {
-  if (!c || c->app_scope > FS_SCOPE_APP_GLOBAL || c->count_mode > 1) return false;
+  if (!c || c->app_scope > FS_SCOPE_APP_GLOBAL || c->count_mode > 1 ||
+      !tau_w_ok(c->tau_w_in, c->tau_w_sys, c->tau_w_out)) return false;
   return c->app_scope == FS_SCOPE_USER_APP || (!c->limits_from_profile && !c->limit_mult_q8);   // R10
 }
 
@@ -510,7 +512,8 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   u64* tau_call = S.alloc<u64>(n);
   if (S.failed) return FS_E_NOMEM;
   ActPrepArgs pa{t, cfg->tier_max, P ? P->J : 0, P ? P->maxstage : nullptr, P ? P->cnt : nullptr,
-                 P ? P->sum_out : nullptr, LD.L, tov, L.head_of, ctx->err, tau_call, status};
+                 P ? P->sum_out : nullptr, LD.L, tov, L.head_of, ctx->err, tau_call, status,
+                 tau_w(cfg->tau_w_in, cfg->tau_w_sys, cfg->tau_w_out)};
   FS_LAUNCH(ctx, "act_prep", k_act_prep, div_up(n, B), B, 0, pa);
   rc = finish(ctx, &S);
   if (rc) return rc;

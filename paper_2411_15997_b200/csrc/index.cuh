@@ -20,6 +20,12 @@ static inline DTrace dtrace(const fs_trace* t) {
   return d;
 }
 
+// token load weights (NEXT-3, R11): all 0 = (1, 1, 1)
+struct TauW { u32 wi, ws, wo; };
+static inline TauW tau_w(u32 wi, u32 ws, u32 wo) { return (wi | ws | wo) ? TauW{wi, ws, wo} : TauW{1, 1, 1}; }
+static inline bool tau_w_ok(u32 wi, u32 ws, u32 wo) { return wi < 16 && ws < 16 && wo < 16; }
+static inline bool tau_w_unit(const TauW& w) { return w.wi == 1 && w.ws == 1 && w.wo == 1; }
+
 __device__ __forceinline__ bool rec_range_ok(const DTrace& t, u64 i) {
   const u32 LMAX = 1u << 24;
   u32 m = t.meta[i], st = m_stage(m), nc = m_ncalls(m);

@@ -200,6 +200,7 @@ struct WinPackArgs {
   DTrace t; u32 J, tier_max, heads_only;
   const u64* ohat;                 // [A][J1]
   uint2* pk;                       // per call
+  TauW w;                          // token load weights (R11)
 };
 __global__ void k_win_pack(WinPackArgs a) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -207,8 +208,8 @@ __global__ void k_win_pack(WinPackArgs a) {
   u32 m = __ldg(&a.t.meta[i]);
   bool c = m_tier(m) <= a.tier_max && (!a.heads_only || m_stage(m) == 1);
   u32 v = 0;
-  if (c) v = 0x80000000u | (__ldg(&a.t.len_in[i]) + __ldg(&a.t.len_sys[i]) +
-                            (u32)a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)]);
+  if (c) v = 0x80000000u | (a.w.wi * __ldg(&a.t.len_in[i]) + a.w.ws * __ldg(&a.t.len_sys[i]) +
+                            a.w.wo * (u32)a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)]);
   a.pk[i] = make_uint2(__ldg(&a.t.t_ms[i]), v);
 }
 struct WinGatherArgs {

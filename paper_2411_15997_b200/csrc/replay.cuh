@@ -40,6 +40,7 @@ struct EngShared {                      // read-only, shared by every replay of 
   const u32* utier;                     // tier per user (0xFFFFFFFF = no calls)
   const u64* tier_calls;                // [256] calls per tier
   const u64* r_off;                     // [U+1] ACT continuation-ring offsets (CSR by user)
+  const u32* tau_w;                     // weighted token load per call (R11), NULL = prompt + reserve
   u32 A, J1;
 };
 
@@ -354,9 +355,10 @@ struct EngineT {
     bool was = lift(us);
     int st = FS_ST_ADMIT;
     if (c->mode == FS_MODE_WI) {
-      if (!static_heads && !ring_push(us, k, tr, h.B.y + h.B.w, m_app(m), r)) return -1;   // l.19
+      const u32 tau_h = sh->tau_w ? sh->tau_w[r] : h.B.y + h.B.w;                           // R11
+      if (!static_heads && !ring_push(us, k, tr, tau_h, m_app(m), r)) return -1;           // l.19
       if (BASE && c->app_global) {                                                          // R10
-        if (!ag_log(tr, m_app(m), h.B.y + h.B.w, r)) return -1;
+        if (!ag_log(tr, m_app(m), tau_h, r)) return -1;
         if (ovl) { const AGSum g = s.ags[m_app(m)]; st = act_check(us, k, m_app(m), tr, h.ng, h.tg, g.n, g.tau); }
       } else if (ovl) st = act_check(us, k, m_app(m), tr, h.ng, h.tg, h.na, h.ta);          // l.20-24
     } else if (BASE && c->mode == FS_MODE_RPM) {
@@ -395,8 +397,9 @@ struct EngineT {
     bool was = lift(us);
     if (c->mode == FS_MODE_WI && !c->heads_only) {          // l.19 (continuations are never throttled)
       uint4 B = ldg4(&sh->recB[r]);
-      if (!ring_push(us, k, tr, B.y + B.w, m_app(m), r)) return -1;
-      if (BASE && c->app_global && !ag_log(tr, m_app(m), B.y + B.w, r)) return -1;
+      const u32 tau_c = sh->tau_w ? sh->tau_w[r] : B.y + B.w;                               // R11
+      if (!ring_push(us, k, tr, tau_c, m_app(m), r)) return -1;
+      if (BASE && c->app_global && !ag_log(tr, m_app(m), tau_c, r)) return -1;
     }
     if (BASE && c->mode == FS_MODE_RPM) {                   // RPM throttles continuations too (R8)
       int st = rpm_check(us, k, m_app(m), tr, r);

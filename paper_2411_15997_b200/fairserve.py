@@ -83,7 +83,8 @@ class _Trace(C.Structure):
 class _ProfileCfg(C.Structure):
     _fields_ = [("window_ms", C.c_uint32), ("max_stage", C.c_uint32), ("tier_max", C.c_uint32),
                 ("n_q", C.c_uint32), ("q_ppm_h", P), ("limit_q_ppm", C.c_uint32),
-                ("limit_mult_q8", C.c_uint32), ("count_mode", C.c_uint32)]
+                ("limit_mult_q8", C.c_uint32), ("count_mode", C.c_uint32),
+                ("tau_w_in", C.c_uint32), ("tau_w_sys", C.c_uint32), ("tau_w_out", C.c_uint32)]
 
 
 class _ProfileDims(C.Structure):
@@ -102,7 +103,8 @@ class _ProfileHost(C.Structure):
 class _ActCfg(C.Structure):
     _fields_ = [("window_ms", C.c_uint32), ("limits_from_profile", C.c_uint32), ("limit_mult_q8", C.c_uint32),
                 ("T_req_g", C.c_uint32), ("T_req_a_h", P), ("T_tok_g", C.c_uint64), ("T_tok_a_h", P),
-                ("count_mode", C.c_uint32), ("app_scope", C.c_uint32), ("tier_max", C.c_uint32)]
+                ("count_mode", C.c_uint32), ("app_scope", C.c_uint32), ("tier_max", C.c_uint32),
+                ("tau_w_in", C.c_uint32), ("tau_w_sys", C.c_uint32), ("tau_w_out", C.c_uint32)]
 
 
 class _ActSummary(C.Structure):
@@ -257,7 +259,7 @@ def _profile_cfg(cfg, keep):
     keep.append(q)
     return _ProfileCfg(cfg.get("window_ms", 60000), cfg.get("max_stage", 64), cfg.get("tier_max", 255), len(q),
                        _hp(q), cfg.get("limit_q_ppm", 990000), cfg.get("limit_mult_q8", 256),
-                       cfg.get("count_mode", 0))
+                       cfg.get("count_mode", 0), *cfg.get("tau_weights", (0, 0, 0)))
 
 
 def build_app_profiles(ctx, trace, cfg=None):
@@ -320,7 +322,7 @@ def _act_cfg(cfg, keep):
     keep += [ra, ta]
     return _ActCfg(cfg.get("window_ms", 60000), cfg.get("limits_from_profile", 1), cfg.get("limit_mult_q8", 0),
                    cfg.get("T_req_g", 0), _hp(ra), cfg.get("T_tok_g", 0), _hp(ta), cfg.get("count_mode", 0),
-                   cfg.get("app_scope", 0), cfg.get("tier_max", 255))
+                   cfg.get("app_scope", 0), cfg.get("tier_max", 255), *cfg.get("tau_weights", (0, 0, 0)))
 
 
 def act_throttle(ctx, trace, profile, cfg=None, overloaded=None, t_ns_override=None, status=None):

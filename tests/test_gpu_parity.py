@@ -555,3 +555,61 @@ def test_sweep_app_global(F, ctx):
     for a, b in zip(gs, es):
         assert a == b
     assert sum(es[0]["n_block"]) > 0
+
+
+# ------------------------------------------------------------------ NEXT-3 weighted token load (R11)
+@pytest.mark.parametrize("seed", range(40))
+def test_act_tiny_tau_weighted(F, ctx, seed):
+    import torch
+    rng = np.random.default_rng(17000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=2, n_apps=A, max_inters=5, max_calls=9)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    n = tr["n_calls"]
+    cfg = dict(window_ms=int(rng.choice((1, 2, 4))), limits_from_profile=0, T_req_g=int(rng.choice((0, 2))),
+               T_req_a=[int(rng.choice((0, 2))) for _ in range(A)], T_tok_g=int(rng.choice((0, 8, 20))),
+               T_tok_a=[int(rng.choice((0, 6, 15))) for _ in range(A)], count_mode=int(rng.integers(0, 2)),
+               tier_max=255, app_scope=int(rng.integers(0, 2)),
+               tau_weights=tuple(int(x) for x in rng.integers(0, 4, size=3)))
+    ovl = (rng.random(n) < 0.7).astype(np.uint8)
+    est, _ = O.act(tr, op, cfg, overloaded=ovl)
+    st, _ = F.act_throttle(ctx, F.Trace(tr), gp, cfg, overloaded=torch.tensor(ovl, device="cuda"))
+    assert list(_np(st)) == list(est)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_replay_tiny_tau_weighted(F, ctx, seed):
+    rng = np.random.default_rng(18000 + seed)
+    A = int(rng.integers(1, 3))
+    tr = tiny_trace(rng, n_users=int(rng.integers(1, 4)), n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    cfg = tiny_replay_cfg(rng, A, modes=(1,))
+    cfg["act"]["tau_weights"] = tuple(int(x) for x in rng.integers(0, 4, size=3))
+    cfg["act"]["app_scope"] = int(rng.integers(0, 2))
+    cmp_replay(F, ctx, tr, gp, op, cfg, f"tw{seed}")
+
+
+def test_profile_and_sweep_tau_weighted(F, ctx):
+    """Weighted token peaks in the profile (and the limits derived from them), and a sweep whose
+    FS(W+I) scenarios share one weight set."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=100, n_calls=20_000, seed=61))
+    pcfg = dict(tier_max=0, tau_weights=(2, 1, 3))
+    op = O.profile(tr, pcfg)
+    gpp = F.build_app_profiles(ctx, F.Trace(tr), pcfg)
+    gpr = gpp.read()
+    for k in ("peak_t_u", "peak_t_ua", "T_tok_a", "T_tok_g", "peak_r_u", "T_req_a"):
+        assert (gpr[k] == op[k]).all(), k
+    base = dict(G.CONFIGS["c2"]["engine"], mode=1, overload_permille=0)
+    scen = [dict(base, tier_max=tm, act=dict(window_ms=60000, limits_from_profile=1, tau_weights=(2, 1, 3)))
+            for tm in (15, 0, 7)]
+    scen.append(dict(base, mode=0))
+    es, ecodes = O.sweep(tr, op, scen)
+    gs, gcodes = F.sweep(ctx, F.Trace(tr), gpp, scen)
+    assert list(gcodes) == list(ecodes)
+    for a, b in zip(gs, es):
+        assert a == b
+    assert sum(es[0]["n_block"]) > 0
