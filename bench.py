@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--calls", type=int, default=0, help="c4: total calls (default 100M)")
-    ap.add_argument("--scenarios", type=int, default=4096, help="c5: scenarios per GPU")
+    ap.add_argument("--scenarios", type=int, default=4096, help="c5: scenarios per GPU (the whole grid with --sweep-split)")
+    ap.add_argument("--sweep-split", action="store_true",
+                    help="c5 at N>1: one grid split over the ranks (LPT, all_gather of summaries; strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timings", action="store_true", help="print per-kernel timings to stderr")
     return ap.parse_args()
@@ -121,7 +123,7 @@ def n_apps_of(wl):
     return c.get("n_apps", len(c["apps"]) * len(c["app_scales"]))
 
 
-def workload_config(wl, n_calls, n_users, n_apps, scenarios, world):
+def workload_config(wl, n_calls, n_users, n_apps, scenarios, world, split=False):
     """The `config` object of the JSON line (shared by both arms)."""
     return {"workload": {"c2": "C2: 1k users, 6 apps, 1M calls, 5% abusive; profile + FS(W+I) replay + ACT",
                          "c3": "C3: 10k users, 12 apps, 10M calls; profile + FS(W+I) replay + ACT",
@@ -130,7 +132,9 @@ def workload_config(wl, n_calls, n_users, n_apps, scenarios, world):
                          "c5": f"C5: profile + sweep of {scenarios} replays (throttle k x (alpha,beta,gamma) x "
                                f"E_abusive x tier_max) of a 1M-call trace"}[wl],
             "n_calls": n_calls, "n_users": n_users, "n_apps": n_apps, "scenarios_per_gpu": scenarios,
-            "parallelism": (f"user-hash shards x{world}" if wl == "c4" else f"independent problem per GPU x{world}")}
+            "parallelism": (f"user-hash shards x{world}" if wl == "c4" else
+                            f"one {scenarios}-scenario grid split over {world} GPUs (LPT, NCCL all_gather)" if split else
+                            f"independent problem per GPU x{world}")}
 
 
 def workload_cfg(name):
@@ -197,7 +201,8 @@ def main():
         pcfg = dict(tier_max=0, window_ms=60000, max_stage=64)
     else:
         # weak scaling: every rank gets its own independent problem (rank 0 = the BASELINE config)
-        tr = G.generate(wl, seed=G.CONFIGS[wl]["seed"] + rank)
+        split = wl == "c5" and args.sweep_split and world > 1
+        tr = G.generate(wl, seed=G.CONFIGS[wl]["seed"] + (0 if split else rank))
     N = tr["n_calls"]
     T = F.Trace(tr)                                                # inputs resident in HBM before timing
     host = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int32)).pin_memory() for k in F.FIELDS}
@@ -213,6 +218,8 @@ def main():
             return F.build_app_profiles(ctx, trace, pcfg)
         prof = F.build_app_profiles(ctx, trace, pcfg)                 # A1-A5
         if scen is not None:
+            if split:                                                    # A9 over the ranks + A10 gather
+                return F.sweep_dist(ctx, trace, prof, scen, tr["meta"])
             return F.sweep(ctx, trace, prof, scen)                       # A9 (A6-A7 inside every replay)
         o, s = F.wsc_replay(ctx, trace, prof, eng, out=outs)            # A7
         return F.act_throttle(ctx, trace, prof, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"],
@@ -278,6 +285,8 @@ def main():
     ms_max, e2e_step_ms = float(t[0]), float(t[1])
     units_per_rank = N * (len(scen) if scen is not None else 1)
     total_units = units_per_rank * world               # c4: the ranks' shards sum to the one trace
+    if wl == "c5" and args.sweep_split and world > 1:
+        total_units = units_per_rank                   # one grid over all ranks
     value = total_units * args.steps / (ms_max / 1e3)
     e2e_value = total_units / (e2e_step_ms / 1e3)
     if args.timings and rank == 0:
@@ -296,9 +305,10 @@ def main():
         "metric": "trace requests throttled+scheduled/sec",
         "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong" if wl == "c4" else "weak",
+        "scaling": "strong" if wl == "c4" or (wl == "c5" and args.sweep_split and world > 1) else "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": dict(workload_config(wl, N * world if wl == "c4" else N, tr["n_users"], tr["n_apps"], S, world),
+        "config": dict(workload_config(wl, N * world if wl == "c4" else N, tr["n_users"], tr["n_apps"], S, world,
+                                       split=wl == "c5" and args.sweep_split and world > 1),
                        l2="flushed between timed steps (256 MB write, untimed)"),
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
                 "d2h_bytes_per_step": {"c4": 0}.get(wl, N if scen is None else 144 * S)},

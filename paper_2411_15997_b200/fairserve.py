@@ -429,6 +429,77 @@ def sweep(ctx, trace, profile, scenarios):
     return [_summary(s) for s in outs], codes
 
 
+def scenario_costs(tr_meta, scenarios):
+    """Estimated replay cost of each scenario: its participating calls (tier <= tier_max)."""
+    tiers = np.asarray(tr_meta) >> 24
+    cnt = np.bincount(tiers.astype(np.int64), minlength=256).astype(np.int64)
+    cum = np.cumsum(cnt)
+    return [int(cum[min(int(sc.get("tier_max", 255)), 255)]) for sc in scenarios]
+
+
+def lpt_split(costs, world):
+    """Longest-processing-time assignment of scenarios to ranks: scenarios by
+    decreasing cost (ties by index) each go to the least-loaded rank (ties: lowest rank).
+    Returns one sorted index list per rank."""
+    load = [0] * world
+    parts = [[] for _ in range(world)]
+    for i in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        r = min(range(world), key=lambda r: (load[r], r))
+        parts[r].append(i)
+        load[r] += costs[i]
+    return [sorted(p) for p in parts]
+
+
+N_SUMMARY_WORDS = 18       # fs_replay_summary as u64 words (n_block counts 4)
+
+
+def _summary_words(s, code):
+    w = [s["n_arrived"], *s["n_block"], s["n_dropped"], s["n_filtered"], s["n_admitted"], s["n_finished"],
+         s["n_iterations"], s["n_ovl_arrivals"], s["makespan_ns"], s["sum_wait_ns"], s["max_wait_ns"],
+         s["sum_ttft_ns"], s["u_min"], s["u_max"], s["digest"]]
+    return [int(x) for x in w], int(code)
+
+
+def _words_summary(w):
+    w = [int(x) & ((1 << 64) - 1) for x in w]
+    keys = ["n_arrived", "n_dropped", "n_filtered", "n_admitted", "n_finished", "n_iterations", "n_ovl_arrivals",
+            "makespan_ns", "sum_wait_ns", "max_wait_ns", "sum_ttft_ns", "u_min", "u_max", "digest"]
+    d = {"n_arrived": w[0], "n_block": w[1:5]}
+    d.update({k: w[5 + i] for i, k in enumerate(keys[1:])})
+    if d["makespan_ns"] >= 1 << 63:
+        d["makespan_ns"] -= 1 << 64
+    return d
+
+
+def sweep_dist(ctx, trace, profile, scenarios, trace_meta, group=None, sweep_fn=None):
+    """One scenario grid sharded over the ranks (strong scaling): an LPT slice per rank runs
+    through fs_sweep, then one all_gather of the fixed-size summaries (NCCL on GPUs) gives
+    every rank the whole grid's results in grid order.  No collective inside the replays."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    parts = lpt_split(scenario_costs(trace_meta, scenarios), world)
+    mine = parts[rank]
+    fn = sweep_fn or (lambda sc: sweep(ctx, trace, profile, sc))
+    sums, codes = fn([scenarios[i] for i in mine]) if mine else ([], np.zeros(0, np.int32))
+    L = max(len(p) for p in parts)
+    buf = torch.zeros((L, N_SUMMARY_WORDS + 1), dtype=torch.int64, device=ctx.device)
+    for j, (sm, cd) in enumerate(zip(sums, codes)):
+        w, c = _summary_words(sm, cd)
+        buf[j, :N_SUMMARY_WORDS] = torch.tensor(np.array(w, dtype=np.uint64).view(np.int64))
+        buf[j, N_SUMMARY_WORDS] = c
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    res = [None] * len(scenarios)
+    rc = np.zeros(len(scenarios), np.int32)
+    for r in range(world):
+        g = out[r].cpu().numpy()
+        for j, i in enumerate(parts[r]):
+            res[i] = _words_summary(g[j, :N_SUMMARY_WORDS].view(np.uint64))
+            rc[i] = int(g[j, N_SUMMARY_WORDS])
+    return res, rc
+
+
 METRIC_FIELDS = ["requests_total", "requests_served", "requests_blocked", "requests_dropped",
                  "interactions_total", "interactions_completed", "interactions_blocked_at_head",
                  "interactions_aborted_midway", "wasted_tokens", "prompt_tokens", "decode_tokens", "abuser_tokens",

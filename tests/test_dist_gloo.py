@@ -182,3 +182,40 @@ def _max_reduce(rank, world):
 def test_bench_max_over_ranks_gloo():
     res = _run("_max_reduce", 2)
     assert res[0] == res[1] == [101.0, 14.0]
+
+
+def _sweep_split(rank, world):
+    """sweep_dist: LPT slices per rank, one all_gather of the summaries -> every rank holds the
+    whole grid's results in grid order (the sweep itself is faked: summary = f(scenario))."""
+    from paper_2411_15997_b200 import fairserve as F
+
+    class Ctx:
+        device = torch.device("cpu")
+
+    rng = np.random.default_rng(3)
+    meta = (rng.integers(0, 16, size=5000) << 24).astype(np.uint32)
+    scen = [dict(tier_max=int(t), key=i) for i, t in enumerate(rng.integers(0, 16, size=37))]
+
+    def fake(sc):
+        out = []
+        for s in sc:
+            k = s["key"]
+            out.append(dict(n_arrived=k, n_block=[k, 1, 2, 3], n_dropped=k + 1, n_filtered=s["tier_max"],
+                            n_admitted=2 * k, n_finished=2 * k, n_iterations=3 * k, n_ovl_arrivals=4,
+                            makespan_ns=10**12 + k, sum_wait_ns=5, max_wait_ns=6, sum_ttft_ns=7, u_min=8,
+                            u_max=(1 << 64) - 1 - k, digest=(1 << 63) + k))
+        return out, np.array([k % 3 for k in (s["key"] for s in sc)], np.int32)
+
+    res, codes = F.sweep_dist(Ctx(), None, None, scen, meta, sweep_fn=fake)
+    want, wcodes = fake(scen)
+    assert res == want and list(codes) == list(wcodes)
+    parts = F.lpt_split(F.scenario_costs(meta, scen), world)
+    assert sorted(i for p in parts for i in p) == list(range(len(scen)))
+    loads = [sum(F.scenario_costs(meta, scen)[i] for i in p) for p in parts]
+    assert max(loads) - min(loads) <= max(F.scenario_costs(meta, scen))      # LPT balance bound
+    return len(parts[rank])
+
+
+def test_sweep_dist_gloo():
+    res = _run("_sweep_split", 2)
+    assert sum(res) == 37
