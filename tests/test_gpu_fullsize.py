@@ -110,3 +110,28 @@ def test_profile_c4_full():
     for k, v in g["profile_sha"].items():
         assert h(p[k]) == v, k
     np.testing.assert_allclose(p["interp_q"], np.array(g["interp_q"]), rtol=1e-6)
+
+
+def test_metrics_c2_full():
+    """fs_replay_metrics over the full C2 FS(W+I) replay (the bench's configuration) against the
+    oracle's §5 metrics (tests/golden/full_c2_metrics.json): every count exact, Jain within 1e-12."""
+    path = os.path.join(GOLD, "full_c2_metrics.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    g = json.load(open(path))
+    from paper_2411_15997_b200 import build, fairserve as F
+    build.build()
+    ctx = F.Context(0)
+    tr = G.generate("c2")
+    assert tr["n_calls"] == g["n_calls"]
+    T = F.Trace(tr)
+    prof = F.build_app_profiles(ctx, T, g["profile_cfg"])
+    o, _ = F.wsc_replay(ctx, T, prof, g["engine"])
+    for thr, want in g["metrics"].items():
+        got, per = F.replay_metrics(ctx, T, o, int(thr))
+        for a, b in [(got, want["global"])] + list(zip(per, want["per_app"])):
+            for k, v in b.items():
+                if k == "jain":
+                    assert a[k] == pytest.approx(v, rel=1e-12), (thr, k)
+                else:
+                    assert a[k] == v, (thr, k, a[k], v)

@@ -90,6 +90,30 @@ def run_c5(n_sample=12):
     print("c5 sample written", path, out["oracle_seconds"], flush=True)
 
 
+def run_c2_metrics():
+    """§5 metrics (oracle/metrics.py) of the full C2 FS(W+I) replay of the bench's configuration,
+    global and per app, at three delay thresholds."""
+    from oracle import metrics as M
+    c = G.CONFIGS["c2"]
+    tr = G.generate("c2")
+    pcfg = dict(tier_max=c["profile"]["tier_max"], window_ms=60000, max_stage=64)
+    p = O.profile(tr, pcfg)
+    act = dict(window_ms=60000, limits_from_profile=1, limit_mult_q8=0, count_mode=0)
+    eng = dict(c["engine"], mode=1, tier_max=255, alpha=1, beta=2, gamma=1, act=act)
+    o, _ = O.replay(tr, p, eng)
+    res = {}
+    for thr in (0, 5_000_000, 1_000_000_000):
+        g, per = M.replay_metrics(tr, o, thr)
+        res[str(thr)] = {"global": g, "per_app": per}
+    out = {"citation": "written by tools/make_goldens.py from oracle/ only (oracle/metrics.py, DESIGN.md R9); "
+                       "inputs: tracegen config c2, the bench's FS(W+I) replay",
+           "config": "c2", "n_calls": tr["n_calls"], "profile_cfg": pcfg, "engine": eng, "metrics": res}
+    path = os.path.join(ROOT, "tests", "golden", "full_c2_metrics.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print("c2 metrics written", path, flush=True)
+
+
 def run_c4():
     """C4: the 100M-call profile (bench.py --workload c4 at one GPU builds exactly this trace)."""
     t0 = time.time()
@@ -115,4 +139,4 @@ def run_c4():
 
 if __name__ == "__main__":
     for nm in sys.argv[1:] or ["c2"]:
-        run_c5() if nm == "c5" else run_c4() if nm == "c4" else run(nm)
+        {"c5": run_c5, "c4": run_c4, "c2m": run_c2_metrics}.get(nm, lambda: run(nm))()
