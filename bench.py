@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--sweep-split", action="store_true",
                     help="c5 at N>1: one grid split over the ranks (LPT, all_gather of summaries; strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gen", default="cpu", choices=["cpu", "gpu"],
+                    help="c4: trace from tracegen.py (cpu) or fs_generate_trace on the device (gpu)")
     ap.add_argument("--timings", action="store_true", help="print per-kernel timings to stderr")
     return ap.parse_args()
 
@@ -195,7 +197,14 @@ def main():
         c4 = G.CONFIGS["c4"]
         total = args.calls or c4["n_calls"]
         Ur = c4["n_users"] // world
-        tr = G.generate(dict(c4, n_calls=total // world, n_users=Ur, seed=c4["seed"] + rank))
+        c4r = dict(c4, n_calls=total // world, n_users=Ur, seed=c4["seed"] + rank)
+        if args.gen == "gpu":                       # NEXT-4 device generator (untimed setup)
+            Tg = F.generate_trace(ctx, c4r)
+            tr = {k: Tg.t[k].cpu().numpy().view(np.uint32) for k in F.FIELDS}
+            tr.update(n_calls=Tg.n, n_users=Tg.U, n_apps=Tg.A, n_inters=Tg.X)
+            del Tg
+        else:
+            tr = G.generate(c4r)
         tr["user"] = (tr["user"] + np.uint32(rank * Ur)).astype(np.uint32)
         tr["n_users"] = Ur * world
         pcfg = dict(tier_max=0, window_ms=60000, max_stage=64)

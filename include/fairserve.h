@@ -263,6 +263,27 @@ int fs_replay_metrics(fs_ctx* ctx, const fs_trace* trace, const uint8_t* status,
                       const int64_t* admit_ns, const int64_t* first_ns, int64_t delay_threshold_ns,
                       fs_metrics* global_h, fs_metrics* per_app_h);
 
+/* ------------------------------------------------------------------ device trace generator (NEXT-4)
+ * fs_generate_trace: a Copilot-shaped synthetic trace of exactly n_calls calls, generated on the
+ * device with a counter-based generator (DESIGN.md §4's recipe, a different sample than
+ * tracegen.py): per-user tier / home app (Zipf 1.1) / second app / lognormal rate weight (x20 if
+ * abusive), calls per interaction from the graph-size table or {1: 80 %, 3: 20 %}
+ * (c1_sizes), diurnal head times (abusive: ON/OFF bursts), lognormal lengths, Exp(500 ms) think,
+ * recorded continuation time = previous + 50 + L_O + think.  Output: the eight SoA arrays (DEVICE,
+ * caller-owned, n_calls each) sorted by (t_ms, interaction, stage), interaction ids dense in head
+ * order; *n_inters_h = number of interactions.  app_means_h: HOST [n_apps][3] mean L_I, L_S, L_O.
+ * Errors: FS_E_INVAL (bad sizes, n_calls >= 2^32, n_apps > 255), FS_E_NOMEM, FS_E_CUDA. */
+typedef struct {
+  uint64_t seed, n_calls;
+  uint32_t n_users, n_apps, duration_ms, c1_sizes;
+  double abusive_frac;
+  const double* app_means_h;
+  uint32_t in_cap, sys_cap, out_cap;
+} fs_gen_cfg;
+int fs_generate_trace(fs_ctx* ctx, const fs_gen_cfg* cfg, uint32_t* user, uint32_t* t_ms, uint32_t* len_in,
+                      uint32_t* len_sys, uint32_t* len_out, uint32_t* think_ms, uint32_t* inter, uint32_t* meta,
+                      uint32_t* n_inters_h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -598,3 +598,4 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
 
 #include "api_wsc.cuh"
 #include "metrics.cuh"
+#include "tracegen.cuh"

@@ -56,6 +56,7 @@ def lib():
             "fs_wsc_state_read": [V, V, V, PI32], "fs_wsc_state_free": [V],
             "fs_sweep": [V, V, V, V, U32, V, V],
             "fs_replay_metrics": [V, V, V, V, V, V, I64, V, V],
+            "fs_generate_trace": [V, V, V, V, V, V, V, V, V, V, PU32],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -216,6 +217,31 @@ class Trace:
         """H2D copy of pinned host tensors (the end-to-end path)."""
         t = {k: host[k].to(device, non_blocking=True) for k in FIELDS}
         return cls(meta, tensors=t)
+
+
+class _GenCfg(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("n_calls", C.c_uint64), ("n_users", C.c_uint32), ("n_apps", C.c_uint32),
+                ("duration_ms", C.c_uint32), ("c1_sizes", C.c_uint32), ("abusive_frac", C.c_double),
+                ("app_means_h", P), ("in_cap", C.c_uint32), ("sys_cap", C.c_uint32), ("out_cap", C.c_uint32)]
+
+
+def generate_trace(ctx, cfg_or_name, n_calls=None, seed=None):
+    """fs_generate_trace: a synthetic trace of the tracegen config's shape generated on the device
+    (NEXT-4); returns a device-resident Trace (no host copy)."""
+    from . import tracegen as G
+    cfg = dict(G.CONFIGS[cfg_or_name]) if isinstance(cfg_or_name, str) else dict(cfg_or_name)
+    n = int(n_calls if n_calls is not None else cfg["n_calls"])
+    names, means = G._app_table(cfg)
+    means = np.ascontiguousarray(means, dtype=np.float64)
+    abf = cfg.get("abusive_frac", cfg.get("n_abusive", 1) / cfg["n_users"])
+    c = _GenCfg(int(seed if seed is not None else cfg["seed"]), n, int(cfg["n_users"]), len(names),
+                int(cfg["duration_ms"]), 1 if cfg.get("m_dist") == "c1" else 0, float(abf), means.ctypes.data,
+                int(cfg["in_cap"]), int(cfg["sys_cap"]), int(cfg["out_cap"]))
+    t = {k: torch.empty(max(n, 1), dtype=torch.int32, device=ctx.device) for k in FIELDS}
+    nx = C.c_uint32(0)
+    ctx._check(lib().fs_generate_trace(ctx.h, _a(c), *[P(t[k].data_ptr()) for k in FIELDS], C.byref(nx)))
+    meta = dict(n_calls=n, n_users=int(cfg["n_users"]), n_apps=len(names), n_inters=int(nx.value))
+    return Trace(meta, tensors=t)
 
 
 class Profile:
