@@ -142,7 +142,7 @@ def workload_config(wl, n_calls, n_users, n_apps, scenarios, world, split=False)
 def workload_cfg(name):
     from paper_2411_15997_b200 import tracegen as G
     c = G.CONFIGS[name]
-    eng = dict(c["engine"], mode=1, tier_max=255, alpha=1, beta=2, gamma=1,
+    eng = dict(c["engine"] or {}, mode=1, tier_max=255, alpha=1, beta=2, gamma=1,
                act=dict(window_ms=60000, limits_from_profile=1, limit_mult_q8=0, count_mode=0))
     pcfg = dict(tier_max=c["profile"]["tier_max"], window_ms=60000, max_stage=64)
     return c, eng, pcfg
@@ -166,7 +166,8 @@ def sweep_scenarios(eng, total):
 
 
 # ALGORITHMIC bytes per call of the kernels that touch every call once per launch
-ALGO_BYTES = {"prof_stream": 16, "win_gather": 36, "act_flags": 42, "pack_records": 84}
+ALGO_BYTES = {"prof_stream": 16, "win_gather": 24, "act_flags": 21, "pack_records": 84,
+              "radix_scatter": 16}   # radix pass: 4 B key + 4 B value read, the same written
 
 
 def main():
@@ -439,6 +440,9 @@ def reference(args, rank, world):
     if wl == "c3":
         tr = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
         desc = "C3-shaped 1M-call / 1k-user sample per step"
+    elif wl == "c4":
+        tr = G.generate(dict(G.CONFIGS["c4"], n_calls=2_000_000, n_users=2000, seed=4))
+        desc = "C4-shaped 2M-call / 2k-user sample per step: profile"
     else:
         tr = G.generate("c2")
         desc = "full C2 step" if wl == "c2" else "C5 trace: profile + 2 of the grid's scenario replays per step"
@@ -449,6 +453,8 @@ def reference(args, rank, world):
 
     def step():
         p = O.profile(tr, pcfg)
+        if wl == "c4":
+            return
         if wl == "c5":
             O.sweep(tr, p, picks)
             return
@@ -465,7 +471,8 @@ def reference(args, rank, world):
     v = n * args.steps / dt
     line = {"impl": "reference", "metric": "trace requests throttled+scheduled/sec", "value": v,
             "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "strong" if wl == "c4" else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": workload_config(wl, G.CONFIGS[wl]["n_calls"], G.CONFIGS[wl]["n_users"], n_apps_of(wl),
                                       args.scenarios if wl == "c5" else 0, 1),
