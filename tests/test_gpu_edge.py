@@ -112,3 +112,60 @@ def test_error_codes(F, ctx, case):
     e, g = _both(F, ctx, tr, prof, cfg)
     assert e[0] == "err" and g[0] == "err", (e, g)
     assert g[1:] == e[1:], (case, e, g)
+
+
+# ------------------------------------------------------------------ edge cases of the NEXT rows
+@pytest.mark.parametrize("mode", [2, 3, 4])
+def test_baseline_modes_empty_and_single(F, ctx, mode):
+    cfg = dict(ENG, mode=mode)
+    tr = G.from_columns(3, 2, [])
+    tr["n_inters"] = 0
+    e, g = _both(F, ctx, tr, PROF1, cfg)
+    assert g[1] == e[1] and g[1]["n_arrived"] == 0
+    tr = G.from_columns(1, 2, [_row()])
+    e, g = _both(F, ctx, tr, PROF1, cfg)
+    assert g[1] == e[1] and g[1]["n_admitted"] == 1
+
+
+def test_rpm_blocks_the_second_call_of_a_user(F, ctx):
+    """RPM with T_req_g = 1: a user's second call inside the window is blocked whatever its
+    stage (here a continuation: the interaction is aborted midway)."""
+    rows = [_row(inter=0, ncalls=3), _row(inter=0, stage=2, ncalls=3, t_ms=1), _row(inter=0, stage=3, ncalls=3, t_ms=2)]
+    tr = G.from_columns(1, 2, rows)
+    cfg = dict(ENG, mode=3, act=dict(window_ms=60000, limits_from_profile=0, T_req_g=1, T_req_a=[0, 0]))
+    prof = (2, 3, [[0, 1, 1, 1], [0, 1, 1, 1]], [[0, 10, 10, 10]] * 2, [[0, 0, 0, 0]] * 2, [[0, 3, 3, 3]] * 2)
+    e, g = _both(F, ctx, tr, prof, cfg)
+    assert g[1] == e[1]
+    assert list(g[0]["status"].cpu().numpy()) == list(e[0]["status"]) == [0, 1, 5]
+
+
+def test_metrics_empty_and_single(F, ctx):
+    from oracle import metrics as M
+    tr = G.from_columns(3, 2, [])
+    tr["n_inters"] = 0
+    T = F.Trace(tr)
+    out = F.replay_outputs(ctx, T)
+    g, per = F.replay_metrics(ctx, T, out, 0)
+    assert g["requests_total"] == 0 and g["ttft_n"] == 0 and g["jain"] == 0.0 and len(per) == 2
+    tr = G.from_columns(1, 2, [_row()])
+    e, _ = O.replay(tr, O.profile_from_host(*PROF1), ENG)
+    go, _ = F.wsc_replay(ctx, F.Trace(tr), F.profile_from_host(ctx, *PROF1), ENG)
+    g, _ = F.replay_metrics(ctx, F.Trace(tr), go, 0)
+    eg, _ = M.replay_metrics(tr, e, 0)
+    assert g == eg and g["users_served"] == 1 and g["jain"] == 1.0
+
+
+def test_generate_tiny(F, ctx):
+    T = F.generate_trace(ctx, "c1", n_calls=1, seed=3)
+    assert T.n == 1 and T.X == 1
+    assert int((T.t["meta"][0].item() >> 8) & 255) == 1          # the one call is a head
+
+
+def test_sweep_empty_grid_and_bad_config(F, ctx):
+    tr = G.from_columns(1, 2, [_row()])
+    gp = F.profile_from_host(ctx, *PROF1)
+    sums, codes = F.sweep(ctx, F.Trace(tr), gp, [])
+    assert sums == [] and len(codes) == 0
+    with pytest.raises(F.FsError) as e:                        # RPM takes explicit limits only (R8)
+        F.sweep(ctx, F.Trace(tr), gp, [dict(ENG, mode=3, act=dict(window_ms=10, limits_from_profile=1))])
+    assert e.value.code == -1
