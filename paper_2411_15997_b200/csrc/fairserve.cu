@@ -159,6 +159,38 @@ static void prof_stream(fs_ctx* ctx, const DTrace& t, u32 J, u32 tier_max, u64* 
   if (t.n) FS_LAUNCH(ctx, "prof_stream", k_prof_stream, grid, 1024, smem, a);
 }
 
+// limits (Q8) from the dense peaks: radix select of every set's nearest-rank quantile at once
+static void prof_limits(fs_profile_partial* pp) {
+  fs_ctx* ctx = pp->ctx;
+  fs_profile* P = pp->P;
+  const u32 A = P->A, U = pp->t.U, NS = 2 * (A + 1);
+  LimSel* sel = pp->S->zeros<LimSel>(NS);
+  u32* hist = pp->S->zeros<u32>((size_t)NS * 256);
+  if (pp->S->failed) return;
+  LimArgs la{A, U, pp->cfg.limit_q_ppm, pp->cfg.limit_mult_q8, P->peak_r_u, P->peak_t_u, P->peak_r_ua, P->peak_t_ua,
+             sel, hist};
+  const u64 tot = (u64)U * A + U;
+  const int grid = (int)std::max<u64>(1, std::min<u64>(div_up(tot ? tot : 1, 256), (u64)ctx->sm_count * 4));
+  if (tot) FS_LAUNCH(ctx, "lim_count", k_lim_count, grid, 256, 0, la);
+  FS_LAUNCH(ctx, "lim_init", k_lim_init, div_up(NS, 128), 128, 0, la);
+  std::vector<LimSel> hs(NS);
+  cudaMemcpyAsync(hs.data(), sel, NS * sizeof(LimSel), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  u64 mx = 0;
+  for (const LimSel& l : hs) mx = std::max(mx, l.maxv);
+  const int top = std::max(0, (bits_for(mx) + 7) / 8 - 1);
+  size_t smem = (size_t)NS * 256 * 4;
+  const int priv = smem + 1024 <= ctx->smem_optin;     // block-private histograms when they fit
+  if (!priv) smem = 0;
+  else cudaFuncSetAttribute(k_lim_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int d = top; d >= 0 && tot; d--) {
+    FS_LAUNCH(ctx, "lim_hist", k_lim_hist, grid, 256, smem, la, d, top, priv);
+    FS_LAUNCH(ctx, "lim_select", k_lim_select, div_up(NS, 4), 128, 0, la);
+  }
+  FS_LAUNCH(ctx, "lim_final", k_lim_final, div_up(NS, 128), 128, 0, la, P->nr_peak_r_a, P->nr_peak_t_a,
+            P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g, P->T_tok_g);
+}
+
 static void prof_windows(fs_profile_partial* pp, const Order& o, const uint2* pk, u32* peak_r, u64* peak_t) {
   fs_ctx* ctx = pp->ctx;
   Scratch& S = *pp->S;
@@ -316,9 +348,7 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
         FS_LAUNCH(ctx, "unpack", k_unpack_u64_u32, div_up((u64)U * A, B), B, 0, pk + 2 * U, P->peak_r_ua, (u64)U * A);
         cudaMemcpyAsync(P->peak_t_ua, pk + 2 * U + (u64)U * A, (u64)U * A * 8, cudaMemcpyDeviceToDevice, ctx->stream);
       }
-      FS_LAUNCH(ctx, "limits", k_limits, dim3(A + 1, 2), 256, 0, A, U, pp->cfg.limit_q_ppm, pp->cfg.limit_mult_q8,
-                P->peak_r_u, P->peak_t_u, P->peak_r_ua, P->peak_t_ua, P->nr_peak_r_a, P->nr_peak_t_a,
-                P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g, P->T_tok_g);
+      prof_limits(pp);
       pp->peaks_done = true;
     }
     u64 w = prof_q_next(pp, buf);

@@ -419,66 +419,118 @@ __global__ void k_q_final(u32 A, u32 nq, const u32* qppm, const u64* hist, const
 // {peak_u[u] : u present}; metric 0 = request peaks, 1 = token peaks.  Exact
 // nearest rank by MSD radix select (8-bit digits over u64), then
 // T = max(1, ceil(k * NR)) in Q8, 0 for an empty set.
-__global__ void k_limits(u32 A, u32 U, u32 qppm, u32 kq8, const u32* pr_u, const u64* pt_u, const u32* pr_ua,
-                         const u64* pt_ua, u32* nr_r_a, u64* nr_t_a, u32* nr_r_g, u64* nr_t_g, u32* T_r_a,
-                         u64* T_t_a, u32* T_r_g, u64* T_t_g) {
-  __shared__ u32 h[256];
-  __shared__ u64 prefix, krank, cnt;
-  __shared__ int digit_sh;
-  u32 set = blockIdx.x, metric = blockIdx.y;
-  auto present = [&](u32 u) -> bool { return set < A ? pr_ua[(u64)u * A + set] > 0 : pr_u[u] > 0; };
-  auto value = [&](u32 u) -> u64 {
-    if (set < A) return metric ? pt_ua[(u64)u * A + set] : (u64)pr_ua[(u64)u * A + set];
-    return metric ? pt_u[u] : (u64)pr_u[u];
-  };
-  if (threadIdx.x == 0) cnt = 0;
+// Limits (Q8): per set (every app's per-(user, app) peaks, and the users' peaks) and metric
+// (requests, tokens), the nearest-rank q quantile NR_q of the present peaks (request peak > 0),
+// then T = max(1, ceil(k NR_q)).  Exact radix select over all 2 (A + 1) sets at once: every pass
+// streams the peak arrays coalesced (element (u, a) feeds set a) into per-set 256-bin digit
+// histograms (block-private in shared memory, one global atomic per non-zero bin per block),
+// then one warp per set picks the digit holding its rank.  Passes start at the highest non-zero
+// digit of any set.
+struct LimSel { u64 n, krank, prefix, maxv; };
+struct LimArgs {
+  u32 A, U, qppm, kq8;
+  const u32* pr_u; const u64* pt_u; const u32* pr_ua; const u64* pt_ua;
+  LimSel* sel;                 // [2][A + 1]
+  u32* hist;                   // [2][A + 1][256]
+};
+__device__ __forceinline__ void lim_item(const LimArgs& a, u64 i, u32* set_out, bool* present, u64* vr, u64* vt) {
+  const u64 UA = (u64)a.U * a.A;
+  if (i < UA) { *set_out = (u32)(i % a.A); u32 r = a.pr_ua[i]; *present = r > 0; *vr = r; *vt = a.pt_ua[i]; }
+  else { u64 u = i - UA; *set_out = a.A; u32 r = a.pr_u[u]; *present = r > 0; *vr = r; *vt = a.pt_u[u]; }
+}
+__global__ void k_lim_count(LimArgs a) {      // n and max per (metric, set): block-private, then global
+  __shared__ unsigned long long cn[256], mr[256], mt[256];   // per set (A + 1 <= 256)
+  for (u32 k = threadIdx.x; k <= a.A; k += blockDim.x) { cn[k] = 0; mr[k] = 0; mt[k] = 0; }
   __syncthreads();
-  u32 c = 0;
-  for (u32 u = threadIdx.x; u < U; u += blockDim.x) c += present(u);
-  atomicAdd((unsigned long long*)&cnt, (unsigned long long)c);
-  __syncthreads();
-  u64 n = cnt;
-  u64 result = 0;
-  if (n > 0) {
-    if (threadIdx.x == 0) {
-      u64 k = ((u128)qppm * n + 999999) / 1000000;
-      if (k < 1) k = 1;
-      if (k > n) k = n;
-      krank = k - 1;
-      prefix = 0;
-    }
-    __syncthreads();
-    for (int d = 7; d >= 0; d--) {
-      for (u32 k = threadIdx.x; k < 256; k += blockDim.x) h[k] = 0;
-      __syncthreads();
-      int sh = 8 * d;
-      u64 pre = prefix;
-      for (u32 u = threadIdx.x; u < U; u += blockDim.x) {
-        if (!present(u)) continue;
-        u64 v = value(u);
-        if (d < 7 && (v >> (sh + 8)) != pre) continue;
-        atomicAdd(&h[(v >> sh) & 255], 1u);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        u64 cum = 0; int b = 0;
-        for (; b < 256; b++) { if (cum + h[b] > krank) break; cum += h[b]; }
-        krank -= cum;
-        prefix = (pre << 8) | (u64)b;
-        digit_sh = b;
-      }
-      __syncthreads();
-    }
-    result = prefix;
+  const u64 tot = (u64)a.U * a.A + a.U;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (u64)gridDim.x * blockDim.x) {
+    u32 st; bool pr; u64 vr, vt;
+    lim_item(a, i, &st, &pr, &vr, &vt);
+    if (!pr) continue;
+    atomicAdd(&cn[st], 1ull);
+    atomicMax(&mr[st], (unsigned long long)vr);
+    atomicMax(&mt[st], (unsigned long long)vt);
   }
-  if (threadIdx.x == 0) {
-    u64 T = 0;
-    if (result) { u128 v = ((u128)kq8 * result + 255) >> 8; T = v < 1 ? 1 : (u64)v; }
-    if (set < A) {
-      if (metric) { nr_t_a[set] = result; T_t_a[set] = T; } else { nr_r_a[set] = (u32)result; T_r_a[set] = (u32)T; }
-    } else {
-      if (metric) { *nr_t_g = result; *T_t_g = T; } else { *nr_r_g = (u32)result; *T_r_g = (u32)T; }
+  __syncthreads();
+  for (u32 k = threadIdx.x; k <= a.A; k += blockDim.x) {
+    if (!cn[k]) continue;
+    atomicAdd((unsigned long long*)&a.sel[k].n, cn[k]);
+    atomicAdd((unsigned long long*)&a.sel[a.A + 1 + k].n, cn[k]);
+    atomicMax((unsigned long long*)&a.sel[k].maxv, mr[k]);
+    atomicMax((unsigned long long*)&a.sel[a.A + 1 + k].maxv, mt[k]);
+  }
+}
+__global__ void k_lim_init(LimArgs a) {
+  u32 s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= 2 * (a.A + 1)) return;
+  LimSel& l = a.sel[s];
+  u64 k = l.n ? ((u128)a.qppm * l.n + 999999) / 1000000 : 0;
+  if (l.n && k < 1) k = 1;
+  if (k > l.n) k = l.n;
+  l.krank = k ? k - 1 : 0;
+  l.prefix = 0;
+}
+__global__ void k_lim_hist(LimArgs a, int d, int top, int priv) {
+  extern __shared__ u32 lh[];                  // [2 (A + 1)][256] when priv (else global atomics)
+  const u32 NS = 2 * (a.A + 1);
+  u32* hh = priv ? lh : a.hist;
+  if (priv) for (u32 k = threadIdx.x; k < NS * 256; k += blockDim.x) lh[k] = 0;
+  __syncthreads();
+  const u64 tot = (u64)a.U * a.A + a.U;
+  const int sh = 8 * d;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (u64)gridDim.x * blockDim.x) {
+    u32 st; bool pr; u64 vr, vt;
+    lim_item(a, i, &st, &pr, &vr, &vt);
+    if (!pr) continue;
+    for (u32 mt = 0; mt < 2; mt++) {
+      u32 s = mt * (a.A + 1) + st;
+      u64 v = mt ? vt : vr;
+      if (d < top && (v >> (sh + 8)) != a.sel[s].prefix) continue;
+      atomicAdd(&hh[s * 256 + ((v >> sh) & 255)], 1u);
     }
+  }
+  __syncthreads();
+  if (priv)
+    for (u32 k = threadIdx.x; k < NS * 256; k += blockDim.x)
+      if (lh[k]) atomicAdd(&a.hist[k], lh[k]);
+}
+__global__ void k_lim_select(LimArgs a) {      // one warp per (metric, set): the digit holding krank
+  u32 s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (s >= 2 * (a.A + 1)) return;
+  LimSel& l = a.sel[s];
+  u32* h = a.hist + (u64)s * 256;
+  u32 c[8]; u64 loc = 0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) { c[k] = h[lane * 8 + k]; loc += c[k]; }
+  u64 inc = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(FULL_MASK, inc, o); if ((int)lane >= o) inc += y; }
+  u64 ex = inc - loc, kr = l.krank;
+  bool mine = l.n && ex <= kr && kr < inc;
+  u32 who = __ballot_sync(FULL_MASK, mine);
+  if (mine) {
+    u64 cum = ex; int b = lane * 8;
+    for (int k = 0; k < 8; k++) { if (cum + c[k] > kr) { b = lane * 8 + k; break; } cum += c[k]; }
+    l.krank = kr - cum;
+    l.prefix = (l.prefix << 8) | (u64)b;
+  }
+  (void)who;
+  __syncwarp();
+  for (int k = 0; k < 8; k++) h[lane * 8 + k] = 0;             // ready for the next digit
+}
+__global__ void k_lim_final(LimArgs a, u32* nr_r_a, u64* nr_t_a, u32* nr_r_g, u64* nr_t_g, u32* T_r_a, u64* T_t_a,
+                            u32* T_r_g, u64* T_t_g) {
+  u32 s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= 2 * (a.A + 1)) return;
+  const LimSel& l = a.sel[s];
+  u32 metric = s / (a.A + 1), set = s % (a.A + 1);
+  u64 result = l.n ? l.prefix : 0;
+  u64 T = 0;
+  if (result) { u128 v = ((u128)a.kq8 * result + 255) >> 8; T = v < 1 ? 1 : (u64)v; }
+  if (set < a.A) {
+    if (metric) { nr_t_a[set] = result; T_t_a[set] = T; } else { nr_r_a[set] = (u32)result; T_r_a[set] = (u32)T; }
+  } else {
+    if (metric) { *nr_t_g = result; *T_t_g = T; } else { *nr_r_g = (u32)result; *T_r_g = (u32)T; }
   }
 }
 
