@@ -215,10 +215,7 @@ __global__ void k_radix_hist(const K* keys, u64 n, int shift, u32* tile_hist, in
 #pragma unroll 4
   for (int r = 0; r < RS_R; r++) {
     u64 i = base + (u64)r * RS_T + threadIdx.x;
-    bool ok = i < n;
-    u32 d = ok ? (u32)((keys[i] >> shift) & 255) : 0u;
-    u32 peers = digit_peers(d, ok);
-    if (ok && (threadIdx.x & 31) == (u32)(__ffs(peers) - 1)) atomicAdd(&h[d], (u32)__popc(peers));
+    if (i < n) atomicAdd(&h[(u32)((keys[i] >> shift) & 255)], 1u);   // shared atomics (measured faster than ranking)
   }
   __syncthreads();
   tile_hist[(u64)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
