@@ -237,7 +237,7 @@ extern "C" int fs_profile_local(fs_ctx* ctx, const fs_trace* tr, const fs_profil
   pp->qppm.assign(cfg->q_ppm_h, cfg->q_ppm_h + cfg->n_q);
   pp->cfg.q_ppm_h = pp->qppm.data();
   const u32 A = tr->n_apps, J = cfg->max_stage, U = tr->n_users, nq = cfg->n_q;
-  pp->P = profile_alloc(A, J, U, nq);
+  pp->P = profile_alloc(A, J, U, nq, ctx->stream);
   if (!pp->P) { delete pp; return FS_E_NOMEM; }
   pp->P->q_ppm = pp->qppm;
   err_reset(ctx);
@@ -407,7 +407,7 @@ extern "C" int fs_profile_from_host(fs_ctx* ctx, uint32_t A, uint32_t J, const u
                                     const uint64_t* s_sys, const uint64_t* s_out, const uint32_t* T_req_a,
                                     uint32_t T_req_g, const uint64_t* T_tok_a, uint64_t T_tok_g, fs_profile** out) {
   if (!ctx || !out || !cnt || !s_in || !s_sys || !s_out || A == 0 || A > 255 || J == 0 || J > 255) return FS_E_INVAL;
-  fs_profile* P = profile_alloc(A, J, 0, 0);
+  fs_profile* P = profile_alloc(A, J, 0, 0, ctx->stream);
   if (!P) return FS_E_NOMEM;
   u64 AJ = (u64)A * (J + 1);
   cudaStream_t s = ctx->stream;
@@ -455,7 +455,7 @@ extern "C" int fs_profile_read(fs_ctx* ctx, const fs_profile* P, fs_profile_host
 
 extern "C" void fs_profile_free(fs_profile* P) {
   if (!P) return;
-  cudaFree(P->block);
+  cudaFreeAsync(P->block, P->stream);       // the creating context's stream (torch's current stream)
   delete P;
 }
 
