@@ -263,19 +263,26 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter(const K* kin, const u32*
   K* skey = (K*)sbuf;
   u32* sval = (u32*)sbuf;
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < 8 * 257; i += RS_T) (&wcnt[0][0])[i] = 0;
-  __syncthreads();
   const u64 tile0 = (u64)blockIdx.x * RS_TILE;
   u64 base = tile0 + (u64)w * (RS_R * 32);
   K key[RS_R];
   u32 val[RS_R], rank[RS_R];
-  u32 lt = lanemask_lt();
+  // every global load of the tile in flight before the ranking (it fences the warp each round)
+  const u32 gb = dbase[threadIdx.x] + tile_off[(u64)threadIdx.x * ntiles + blockIdx.x];
 #pragma unroll
   for (int r = 0; r < RS_R; r++) {
     u64 i = base + (u64)r * 32 + lane;
     bool ok = i < n;
     key[r] = ok ? kin[i] : (K)0;
     val[r] = ok ? (vin ? vin[i] : (u32)i) : 0u;
+  }
+  for (int i = threadIdx.x; i < 8 * 257; i += RS_T) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  u32 lt = lanemask_lt();
+#pragma unroll
+  for (int r = 0; r < RS_R; r++) {
+    u64 i = base + (u64)r * 32 + lane;
+    bool ok = i < n;
     u32 d = ok ? (u32)((key[r] >> shift) & 255) : 256u;
     u32 vm = __ballot_sync(FULL_MASK, ok);
     u32 peers = digit_peers(d & 255u, ok);
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(RS_T) k_radix_scatter(const K* kin, const u32*
     for (int ww = 0; ww < 8; ww++) { u32 c = wcnt[ww][d]; wcnt[ww][d] = s; s += c; }
     u32 ex = block_excl_scan<u32>(s, sh_scan, nullptr);   // digit start inside the tile
     dstart[d] = ex;
-    gbase[d] = dbase[d] + tile_off[(u64)d * ntiles + blockIdx.x];
+    gbase[d] = gb;
   }
   __syncthreads();
 #pragma unroll
