@@ -33,14 +33,19 @@ __device__ __forceinline__ bool rec_range_ok(const DTrace& t, u64 i) {
          t.len_in[i] < LMAX && t.len_sys[i] < LMAX && t.len_out[i] < LMAX && t.len_out[i] != 0;
 }
 
-// pass 1: range, time order, head of each interaction (min index with stage 1)
-__global__ void k_val_range(DTrace t, DevErr* err, u32* head_of_inter) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= t.n) return;
-  if (!rec_range_ok(t, i)) { report(err, ERR_RANGE, i); return; }
+// pass 1: range, time order, head of each interaction (min index with stage 1); the range
+// verdicts go to a bitset (rok) so the later passes do not re-read the length fields
+__global__ void k_val_range(DTrace t, DevErr* err, u32* head_of_inter, u32* rok) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;      // blockDim is a multiple of 32
+  const bool in = i < t.n, ok = in && rec_range_ok(t, i);
+  const u32 bits = __ballot_sync(FULL_MASK, ok);
+  if (in && (threadIdx.x & 31) == 0) rok[i >> 5] = bits;
+  if (!in) return;
+  if (!ok) { report(err, ERR_RANGE, i); return; }
   if (i > 0 && t.t_ms[i] < t.t_ms[i - 1]) report(err, ERR_ORDER, i);
   if (m_stage(t.meta[i]) == 1) atomicMin(&head_of_inter[t.inter[i]], (u32)i);
 }
+__device__ __forceinline__ bool range_ok(const u32* rok, u64 i) { return (rok[i >> 5] >> (i & 31)) & 1u; }
 
 __global__ void k_val_nslots(DTrace t, const u32* head_of_inter, u64* nslots) {
   u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x;
@@ -49,29 +54,47 @@ __global__ void k_val_nslots(DTrace t, const u32* head_of_inter, u64* nslots) {
   nslots[x] = h == NONE32 ? 0 : m_ncalls(t.meta[h]);
 }
 
-__device__ __forceinline__ bool head_consistent(const DTrace& t, u64 i, u32 h) {
-  if (h == NONE32) return false;
-  u32 mi = t.meta[i], mh = t.meta[h];
-  return t.user[i] == t.user[h] && m_app(mi) == m_app(mh) && m_ncalls(mi) == m_ncalls(mh);
+// per interaction, packed so the per-call checks take one 16-B gather instead of four (head,
+// its user and meta, the slot offset): w = slot offset (< 255 X < 2^40) | app << 40 | ncalls << 48
+struct IRec { u32 h, user; u64 w; };
+__device__ __forceinline__ u64 ir_off(const IRec& e) { return e.w & ((1ull << 40) - 1); }
+
+__global__ void k_val_irec(DTrace t, const u32* head_of_inter, const u64* off, IRec* ir) {
+  u64 x = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= t.X) return;
+  IRec e;
+  e.h = head_of_inter[x]; e.user = 0; e.w = 0;
+  if (e.h != NONE32) {
+    u32 mh = t.meta[e.h];
+    e.user = t.user[e.h];
+    e.w = off[x] | (u64)m_app(mh) << 40 | (u64)m_ncalls(mh) << 48;
+  }
+  ir[x] = e;
 }
 
-__global__ void k_val_slots(DTrace t, DevErr* err, const u32* head_of_inter, const u64* off, u32* slot) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= t.n || !rec_range_ok(t, i)) return;
-  u32 x = t.inter[i];
-  u32 h = head_of_inter[x];
-  if (!head_consistent(t, i, h)) { report(err, ERR_ORDER, i); return; }
-  atomicMin(&slot[off[x] + m_stage(t.meta[i]) - 1], (u32)i);
+// call i belongs to the interaction of head e.h: same user, app and call count
+__device__ __forceinline__ bool head_consistent(const DTrace& t, u64 i, const IRec& e) {
+  if (e.h == NONE32) return false;
+  u32 mi = t.meta[i];
+  return t.user[i] == e.user && m_app(mi) == (u32)(e.w >> 40 & 255u) && m_ncalls(mi) == (u32)(e.w >> 48 & 255u);
 }
 
-__global__ void k_val_links(DTrace t, DevErr* err, const u32* head_of_inter, const u64* off, const u32* slot,
-                            u32* head_of, u32* next_call) {
+__global__ void k_val_slots(DTrace t, DevErr* err, const u32* rok, const IRec* ir, u32* slot) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= t.n || !rec_range_ok(t, i)) return;
-  u32 x = t.inter[i];
-  if (!head_consistent(t, i, head_of_inter[x])) return;
+  if (i >= t.n || !range_ok(rok, i)) return;
+  const IRec e = ir[t.inter[i]];
+  if (!head_consistent(t, i, e)) { report(err, ERR_ORDER, i); return; }
+  atomicMin(&slot[ir_off(e) + m_stage(t.meta[i]) - 1], (u32)i);
+}
+
+__global__ void k_val_links(DTrace t, DevErr* err, const u32* rok, const IRec* ir, const u32* slot, u32* head_of,
+                            u32* next_call) {
+  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= t.n || !range_ok(rok, i)) return;
+  const IRec e = ir[t.inter[i]];
+  if (!head_consistent(t, i, e)) return;
   u32 m = t.meta[i], s = m_stage(m), nc = m_ncalls(m);
-  u64 o = off[x];
+  u64 o = ir_off(e);
   bool bad = slot[o + s - 1] != (u32)i;
   if (s > 1) { u32 p = slot[o + s - 2]; if (p == NONE32 || p > (u32)i) bad = true; }
   u32 nx = NONE32;
@@ -89,12 +112,14 @@ static bool build_links(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
   L->head_of = S.alloc<u32>(n);
   L->next_call = S.alloc<u32>(n);
   u32* hoi = S.alloc<u32>(t.X + 1);
-  u64* nsl = S.alloc<u64>(t.X + 1);
+  IRec* ir = S.alloc<IRec>(t.X + 1);
+  u64* nsl = (u64*)ir;                   // slot counts, dead once scanned: the records reuse them
   u64* off = S.alloc<u64>(t.X + 1);
+  u32* rok = S.alloc<u32>(n / 32 + 1);
   if (S.failed) return false;
   cudaMemsetAsync(hoi, 0xFF, (t.X + 1) * 4, ctx->stream);
   int B = 256;
-  if (n) FS_LAUNCH(ctx, "val_range", k_val_range, div_up(n, B), B, 0, t, ctx->err, hoi);
+  if (n) FS_LAUNCH(ctx, "val_range", k_val_range, div_up(n, B), B, 0, t, ctx->err, hoi, rok);
   if (t.X) FS_LAUNCH(ctx, "val_nslots", k_val_nslots, div_up(t.X, B), B, 0, t, hoi, nsl);
   excl_scan<u64>(ctx, S, nsl, off, t.X, off + t.X);
   u64 total = 0;
@@ -103,9 +128,10 @@ static bool build_links(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
   u32* slot = S.alloc<u32>(total + 1);
   if (S.failed) return false;
   cudaMemsetAsync(slot, 0xFF, (total + 1) * 4, ctx->stream);
+  if (t.X) FS_LAUNCH(ctx, "val_irec", k_val_irec, div_up(t.X, B), B, 0, t, hoi, off, ir);
   if (n) {
-    FS_LAUNCH(ctx, "val_slots", k_val_slots, div_up(n, B), B, 0, t, ctx->err, hoi, off, slot);
-    FS_LAUNCH(ctx, "val_links", k_val_links, div_up(n, B), B, 0, t, ctx->err, hoi, off, slot, L->head_of, L->next_call);
+    FS_LAUNCH(ctx, "val_slots", k_val_slots, div_up(n, B), B, 0, t, ctx->err, rok, ir, slot);
+    FS_LAUNCH(ctx, "val_links", k_val_links, div_up(n, B), B, 0, t, ctx->err, rok, ir, slot, L->head_of, L->next_call);
   }
   return true;
 }
