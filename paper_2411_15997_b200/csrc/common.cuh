@@ -164,17 +164,35 @@ __global__ void k_scan_blocks(T* bsum, int nb, T* grand) {
   if (threadIdx.x == 0 && grand) *grand = carry;
 }
 
+// the tile moves through shared memory: coalesced (striped) global loads and stores, blocked
+// per-thread runs for the scan (a pad word per 16 items keeps both views conflict-free)
+__device__ __forceinline__ u32 scan_pad(u32 k) { return k + (k >> 4); }
 template <class T>
-__global__ void k_scan_apply(const T* in, T* out, u64 n, const T* bsum) {
+__global__ void __launch_bounds__(SCAN_T) k_scan_apply(const T* in, T* out, u64 n, const T* bsum) {
   __shared__ T sh[32];
-  u64 base = (u64)blockIdx.x * SCAN_TILE + (u64)threadIdx.x * SCAN_IPT;
+  __shared__ T tile[SCAN_TILE + SCAN_TILE / 16];
+  const u64 base = (u64)blockIdx.x * SCAN_TILE;
+#pragma unroll
+  for (int r = 0; r < SCAN_IPT; r++) {
+    u32 k = r * SCAN_T + threadIdx.x;
+    u64 i = base + k;
+    tile[scan_pad(k)] = i < n ? in[i] : (T)0;
+  }
+  __syncthreads();
   T v[SCAN_IPT];
   T s = 0;
 #pragma unroll
-  for (int r = 0; r < SCAN_IPT; r++) { u64 i = base + r; v[r] = i < n ? in[i] : (T)0; s += v[r]; }
-  T ex = block_excl_scan<T>(s, sh, nullptr) + bsum[blockIdx.x];
+  for (int r = 0; r < SCAN_IPT; r++) { v[r] = tile[scan_pad(threadIdx.x * SCAN_IPT + r)]; s += v[r]; }
+  T ex = block_excl_scan<T>(s, sh, nullptr) + bsum[blockIdx.x];   // ends with a barrier
 #pragma unroll
-  for (int r = 0; r < SCAN_IPT; r++) { u64 i = base + r; if (i < n) out[i] = ex; ex += v[r]; }
+  for (int r = 0; r < SCAN_IPT; r++) { tile[scan_pad(threadIdx.x * SCAN_IPT + r)] = ex; ex += v[r]; }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < SCAN_IPT; r++) {
+    u32 k = r * SCAN_T + threadIdx.x;
+    u64 i = base + k;
+    if (i < n) out[i] = tile[scan_pad(k)];
+  }
 }
 
 // exclusive scan of n items; out[n] (if total_dev) receives the total
