@@ -261,6 +261,7 @@ def main():
     # end to end through the public API with host buffers: H2D of the trace, the step, D2H of the results
     e2e_steps = 1 if scen is not None else max(1, min(args.steps, 3))
     e2e_ms = 0.0
+    d2h_c4 = 0
     d2h = torch.empty(N, dtype=torch.uint8).pin_memory()
     for _ in range(e2e_steps):
         flush.zero_()
@@ -270,7 +271,8 @@ def main():
         T2 = F.Trace.from_host_tensors(tr, host)
         res = step(T2)                                    # the sweep returns its summaries in host memory
         if wl == "c4":
-            res.read()                                    # D2H of the profile tables
+            got = res.read()                              # D2H of the profile tables
+            d2h_c4 = sum(v.nbytes for v in got.values() if hasattr(v, "nbytes"))
         elif scen is None:
             d2h.copy_(status, non_blocking=True)
         b.record(stream)
@@ -321,7 +323,7 @@ def main():
                                        split=wl == "c5" and args.sweep_split and world > 1),
                        l2="flushed between timed steps (256 MB write, untimed)"),
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
-                "d2h_bytes_per_step": {"c4": 0}.get(wl, N if scen is None else 144 * S)},
+                "d2h_bytes_per_step": d2h_c4 if wl == "c4" else (N if scen is None else 144 * S)},
         "gpu_launches": int(launches),
         "roofline": roof,
         "stage_ms": {k: v[1] / args.steps for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])[:8]},
