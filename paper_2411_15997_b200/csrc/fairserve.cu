@@ -146,7 +146,7 @@ static void prof_stream(fs_ctx* ctx, const DTrace& t, u32 J, u32 tier_max, u64* 
   const u32 A = t.A, J1 = J + 1;
   size_t sums = (size_t)4 * A * J1 * 8;
   size_t budget = ctx->smem_optin ? ctx->smem_optin - 1024 : 200 * 1024;
-  size_t per_app = (size_t)NF * NBINS * 4;
+  size_t per_app = (size_t)HB_APP * 4;
   u32 na = (u32)std::min<size_t>(A, (budget - sums) / per_app);
   if (na == 0) na = 1;
   u32 chunks = (A + na - 1) / na;

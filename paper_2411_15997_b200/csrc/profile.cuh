@@ -99,14 +99,21 @@ struct ProfStreamArgs {
   u64 *cnt, *s_in, *s_sys, *s_out, *hist;
 };
 
+// shared-memory bins per app: only the bins a validated field can reach (L < 2^24: bins < 176;
+// L_I + L_S + L_O < 3 * 2^24: < 192; m < 256: < 48), so all apps' bins and the sums fit at once
+// (one pass over the trace; the full 240-bin rows took two passes at 34 apps)
+__host__ __device__ __forceinline__ u32 hb_off(u32 f) { return f < 4 ? 176 * f : 720; }
+__host__ __device__ __forceinline__ u32 hb_cap(u32 f) { return f < 3 ? 176 : f == 3 ? 192 : 48; }
+static const u32 HB_APP = 768;
+
 __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const u32 J1 = a.J + 1, A = a.t.A;
   const u32 a0 = blockIdx.y * a.na_chunk, na = min(a.na_chunk, A - a0);
   const bool do_sums = blockIdx.y == 0;
   u64* ssum = (u64*)sm;                              // [4][A*J1] (only chunk 0)
-  u32* shist = (u32*)(sm + (do_sums ? (size_t)4 * A * J1 * 8 : 0));   // [na][5][240]
-  const u32 nsum = do_sums ? 4 * A * J1 : 0, nh = na * NF * NBINS;
+  u32* shist = (u32*)(sm + (do_sums ? (size_t)4 * A * J1 * 8 : 0));   // [na][HB_APP]
+  const u32 nsum = do_sums ? 4 * A * J1 : 0, nh = na * HB_APP;
   for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) ssum[k] = 0;
   for (u32 k = threadIdx.x; k < nh; k += blockDim.x) shist[k] = 0;
   __syncthreads();
@@ -133,12 +140,12 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
       }
     }
     if (!ok || app < a0 || app >= a0 + na) return;
-    u32* hb = shist + (app - a0) * NF * NBINS;
-    atomicAdd(&hb[loglin_bin(Li)], 1u);
-    atomicAdd(&hb[NBINS + loglin_bin(Ls)], 1u);
-    atomicAdd(&hb[2 * NBINS + loglin_bin(Lo)], 1u);
-    atomicAdd(&hb[3 * NBINS + loglin_bin(Li + Ls + Lo)], 1u);
-    if (st == 1) atomicAdd(&hb[4 * NBINS + loglin_bin(m_ncalls(m))], 1u);
+    u32* hb = shist + (app - a0) * HB_APP;              // (clamped: an out-of-range trace fails validation)
+    atomicAdd(&hb[min(loglin_bin(Li), 175u)], 1u);
+    atomicAdd(&hb[176 + min(loglin_bin(Ls), 175u)], 1u);
+    atomicAdd(&hb[352 + min(loglin_bin(Lo), 175u)], 1u);
+    atomicAdd(&hb[528 + min(loglin_bin(Li + Ls + Lo), 191u)], 1u);
+    if (st == 1) atomicAdd(&hb[720 + min(loglin_bin(m_ncalls(m)), 47u)], 1u);
   };
   const u64 stride = (u64)gridDim.x * blockDim.x;
   const u64 n4 = a.vec ? n / 4 : 0;                    // uint4 loads: 4 calls per thread per array
@@ -171,7 +178,9 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   }
   for (u32 k = threadIdx.x; k < nh; k += blockDim.x) {
     u32 v = shist[k];
-    if (v) atomicAdd((unsigned long long*)&a.hist[(u64)a0 * NF * NBINS + k], (unsigned long long)v);
+    if (!v) continue;
+    u32 ap = k / HB_APP, r = k % HB_APP, f = r < 720 ? min(r / 176, 3u) : 4, bin = r - hb_off(f);
+    atomicAdd((unsigned long long*)&a.hist[((u64)(a0 + ap) * NF + f) * NBINS + bin], (unsigned long long)v);
   }
 }
 
