@@ -166,7 +166,7 @@ def sweep_scenarios(eng, total):
 
 
 # ALGORITHMIC bytes per call of the kernels that touch every call once per launch
-ALGO_BYTES = {"prof_stream": 16, "win_gather": 28, "act_flags": 21, "pack_records": 84,
+ALGO_BYTES = {"prof_stream": 16, "win_scan": 28, "act_flags": 21, "pack_records": 84,
               "radix_scatter": 16}   # radix pass: 4 B key + 4 B value read, the same written
 
 

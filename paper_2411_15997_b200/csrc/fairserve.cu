@@ -198,17 +198,17 @@ static void prof_windows(fs_profile_partial* pp, const Order& o, const uint2* pk
   u64 n = t.n;
   if (!n) return;
   u32* ts = S.alloc<u32>(n);
-  u64* tau = S.alloc<u64>(n + 1);
-  u32* flag = S.alloc<u32>(n + 1);
   u64* ptau = S.alloc<u64>(n + 1);
   u32* pc = S.alloc<u32>(n + 1);
+  const u32 nt = div_up(n, WS_TILE);
+  u64* lt = S.alloc<u64>(2 * (size_t)nt);
+  u32* lc = S.alloc<u32>(3 * (size_t)nt + 1);                // agg, inc, stat, ticket
   if (S.failed) return;
+  cudaMemsetAsync(lc + 2 * (size_t)nt, 0, ((size_t)nt + 1) * 4, ctx->stream);
   int B = 256;
-  WinGatherArgs g{n, o.perm, pk, ts, tau, flag};
-  FS_LAUNCH(ctx, "win_gather", k_win_gather, div_up(n, B), B, 0, g);
-  excl_scan<u64>(ctx, S, tau, ptau, n, ptau + n);
-  excl_scan<u32>(ctx, S, flag, pc, n, pc + n);
-  WinPeakArgs w{n, o.key, o.seg, ts, ptau, pc, flag, (i64)pp->cfg.window_ms, peak_r, peak_t};
+  WinScanArgs g{n, o.perm, pk, ts, ptau, pc, lt, lt + nt, lc, lc + nt, lc + 2 * (size_t)nt, lc + 3 * (size_t)nt};
+  FS_LAUNCH(ctx, "win_scan", k_win_scan, nt, WS_T, 0, g);
+  WinPeakArgs w{n, o.key, o.seg, ts, ptau, pc, nullptr, (i64)pp->cfg.window_ms, peak_r, peak_t};
   FS_LAUNCH(ctx, "win_peaks", k_win_peaks, div_up(n, B), B, 0, w);
 }
 

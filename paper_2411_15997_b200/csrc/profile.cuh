@@ -223,17 +223,104 @@ __global__ void k_win_pack(WinPackArgs a) {
                             a.w.wo * (u32)a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)]);
   a.pk[i] = make_uint2(__ldg(&a.t.t_ms[i]), v);
 }
-struct WinGatherArgs {
+
+// gather + both window prefix sums in one pass (single-pass scan, decoupled look-back): per
+// position p of the order, ts[p] = t of call perm[p], ptau[p] = sum of tau over positions < p,
+// pc[p] = number of counted positions < p (ptau[n], pc[n] = totals).  No per-position tau / flag
+// arrays: the scan consumes the gathered values from shared memory.
+static const int WS_T = 256, WS_IPT = 16, WS_TILE = WS_T * WS_IPT;
+struct WinScanArgs {
   u64 n; const u32* perm; const uint2* pk;
-  u32* ts; u64* tau; u32* flag;    // per position
+  u32* ts; u64* ptau; u32* pc;
+  u64* agg_t; u64* inc_t; u32* agg_c; u32* inc_c; u32* stat; u32* ticket;   // per tile (stat zeroed)
 };
-__global__ void k_win_gather(WinGatherArgs a) {
-  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.n) return;
-  uint2 v = a.pk[__ldg(&a.perm[p])];
-  a.ts[p] = v.x;
-  a.tau[p] = v.y & 0x7FFFFFFFu;
-  a.flag[p] = v.y >> 31;
+__global__ void __launch_bounds__(WS_T) k_win_scan(WinScanArgs a) {
+  __shared__ uint2 tile[WS_TILE + WS_TILE / 16];
+  __shared__ u64 sht[32];
+  __shared__ u32 shc[32];
+  __shared__ u32 s_tile;
+  __shared__ u64 s_pt;
+  __shared__ u32 s_pc;
+  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);   // tiles start in ticket order
+  __syncthreads();
+  const u32 tid = s_tile;
+  const u64 base = (u64)tid * WS_TILE;
+#pragma unroll
+  for (int r = 0; r < WS_IPT; r++) {                         // striped: coalesced perm and ts
+    u32 k = r * WS_T + threadIdx.x;
+    u64 i = base + k;
+    uint2 v = make_uint2(0, 0);
+    if (i < a.n) { v = a.pk[__ldg(&a.perm[i])]; a.ts[i] = v.x; }
+    tile[scan_pad(k)] = make_uint2(v.y & 0x7FFFFFFFu, v.y >> 31);
+  }
+  __syncthreads();
+  u32 tv[WS_IPT], cv[WS_IPT];
+  u64 st = 0; u32 sc = 0;
+#pragma unroll
+  for (int r = 0; r < WS_IPT; r++) {
+    uint2 e = tile[scan_pad(threadIdx.x * WS_IPT + r)];
+    tv[r] = e.x; cv[r] = e.y; st += e.x; sc += e.y;
+  }
+  u64 tot_t; u32 tot_c;
+  u64 ex_t = block_excl_scan<u64>(st, sht, &tot_t);
+  u32 ex_c = block_excl_scan<u32>(sc, shc, &tot_c);
+  if (threadIdx.x < 32) {                                    // warp 0: look back 32 tiles at a time
+    const int lane = threadIdx.x;
+    u64 pt = 0; u32 pcn = 0;
+    if (tid > 0) {
+      if (lane == 0) {
+        a.agg_t[tid] = tot_t; a.agg_c[tid] = tot_c;
+        __threadfence();
+        atomicExch(&a.stat[tid], 1u);
+      }
+      for (long long j0 = (long long)tid - 1;; j0 -= 32) {
+        const long long j = j0 - lane;                         // lane 0 = nearest predecessor
+        u32 f = 2;
+        if (j >= 0) while ((f = *(volatile u32*)&a.stat[j]) == 0) {}
+        __threadfence();
+        const u32 incm = __ballot_sync(FULL_MASK, f == 2);   // j < 0 counts as an inclusive 0
+        const int L = incm ? __ffs(incm) - 1 : 32;
+        u64 vt = 0; u32 vc = 0;
+        if (j >= 0 && lane < L) { vt = *(volatile u64*)&a.agg_t[j]; vc = *(volatile u32*)&a.agg_c[j]; }
+        else if (j >= 0 && lane == L) { vt = *(volatile u64*)&a.inc_t[j]; vc = *(volatile u32*)&a.inc_c[j]; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) { vt += __shfl_xor_sync(FULL_MASK, vt, o); vc += __shfl_xor_sync(FULL_MASK, vc, o); }
+        pt += vt; pcn += vc;
+        if (incm) break;
+      }
+    }
+    if (lane == 0) {
+      a.inc_t[tid] = pt + tot_t; a.inc_c[tid] = pcn + tot_c;
+      __threadfence();
+      atomicExch(&a.stat[tid], 2u);
+      s_pt = pt; s_pc = pcn;
+      if (base + WS_TILE >= a.n) { a.ptau[a.n] = pt + tot_t; a.pc[a.n] = pcn + tot_c; }   // last tile
+    }
+  }
+  __syncthreads();
+  u64 rt = s_pt + ex_t;
+  u32 rc = s_pc + ex_c;
+  u64* t64 = (u64*)tile;                                       // 8 B per element: same padded slots
+#pragma unroll
+  for (int r = 0; r < WS_IPT; r++) { t64[scan_pad(threadIdx.x * WS_IPT + r)] = rt; rt += tv[r]; }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < WS_IPT; r++) {
+    u32 k = r * WS_T + threadIdx.x;
+    u64 i = base + k;
+    if (i < a.n) a.ptau[i] = t64[scan_pad(k)];
+  }
+  __syncthreads();
+  u32* t32 = (u32*)tile;
+#pragma unroll
+  for (int r = 0; r < WS_IPT; r++) { t32[scan_pad(threadIdx.x * WS_IPT + r)] = rc; rc += cv[r]; }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < WS_IPT; r++) {
+    u32 k = r * WS_T + threadIdx.x;
+    u64 i = base + k;
+    if (i < a.n) a.pc[i] = t32[scan_pad(k)];
+  }
 }
 
 __device__ __forceinline__ void atomic_max_u64(u64* p, u64 v) { atomicMax((unsigned long long*)p, (unsigned long long)v); }
@@ -248,7 +335,7 @@ __global__ void k_win_peaks(WinPeakArgs a) {
   bool ok = p < a.n;
   u32 k = ok ? a.key[p] : NONE32;
   u32 nr = 0; u64 nt = 0;
-  if (ok && a.flag[p]) {
+  if (ok && (a.flag ? a.flag[p] != 0 : a.pc[p + 1] != a.pc[p])) {
     u64 s = a.seg[k];
     u64 lb = window_lb<u32>(a.ts, s, p, (i64)a.ts[p] - a.W);
     nr = a.pc[p + 1] - a.pc[lb];

@@ -18,6 +18,6 @@ ncu --metrics smsp__inst_executed.sum,sm__cycles_elapsed.max,gpu__time_duration.
     --clock-control none -k regex:'^k_replay$' --csv --log-file gpurun_out/${TAG}_replay.csv \
     python tools/prof_replay.py c2 0 1 > gpurun_out/${TAG}_replay.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,dram__throughput.avg.pct_of_peak_sustained_elapsed \
-    --clock-control none -k regex:'k_prof_stream|k_radix_scatter|k_win_gather|k_win_peaks|k_act_flags|k_act_decide|k_act_walk|k_q_count|k_pack_records|k_val_' \
+    --clock-control none -k regex:'k_prof_stream|k_radix_scatter|k_win_scan|k_win_peaks|k_act_flags|k_act_decide|k_act_walk|k_q_count|k_pack_records|k_val_' \
     --csv --log-file gpurun_out/${TAG}_hbm.csv python tools/prof_stages.py c3 > gpurun_out/${TAG}_hbm.log 2>&1
 echo done
