@@ -394,9 +394,15 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
                 "ns_per_call": per_s / N * 1e9, "hbm_stages": stages}
     b = ALGO_BYTES.get(name, 0) * N
     gbs = b / per_s / 1e9 if b else None
+    traffic = None
+    if name == "win_scan" and args.workload == "c4" and N == 100_000_000:
+        # one ncu launch of the same kernel at this size (profiles/r01_c4_winscan.csv)
+        prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_c4_winscan.csv"))
+        if prof.get("dram__bytes_read.sum") is not None:
+            traffic = prof["dram__bytes_read.sum"] + prof.get("dram__bytes_write.sum", 0.0)
     return {"bound": "hbm", "kernel": name, "ms_per_launch": per_s * 1e3, "achieved": gbs,
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"] if gbs else None,
-            "traffic": None, "peak_source": src, "hbm_stages": stages}
+            "traffic": traffic, "algorithmic_bytes_per_launch": b, "peak_source": src, "hbm_stages": stages}
 
 
 def cpu_baseline(workload, tr):
