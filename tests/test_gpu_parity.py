@@ -141,6 +141,17 @@ def test_profile_parity(F, ctx, case):
     _cmp_profile(gpr, O.profile(tr, cfg), 5)
 
 
+@pytest.mark.parametrize("n", [1, 31, 4095, 4096, 4097, 12289])
+def test_profile_tile_boundaries(F, ctx, n):
+    """Sizes around the 4096-item tiles of the single-pass window scan and the device-wide scan
+    (one tile, exact tiles, one item over, several tiles + a ragged tail)."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=50, n_calls=n, seed=31 + n))
+    assert tr["n_calls"] == n
+    cfg = dict(tier_max=255, window_ms=20_000)
+    gpr = F.build_app_profiles(ctx, F.Trace(tr), cfg).read()
+    _cmp_profile(gpr, O.profile(tr, cfg), 5)
+
+
 def test_profile_c2_full(F, ctx):
     tr = G.generate("c2")
     cfg = dict(tier_max=0)
