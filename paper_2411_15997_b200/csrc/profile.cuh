@@ -341,8 +341,18 @@ __global__ void k_win_peaks(WinPeakArgs a) {
     nr = a.pc[p + 1] - a.pc[lb];
     nt = a.ptau[p + 1] - a.ptau[lb];
   }
-  // warp segmented max over runs of equal keys (positions are sorted by key)
   int lane = threadIdx.x & 31;
+  // most warps lie inside one segment (one key): plain warp max, one lane's atomics
+  if (__reduce_min_sync(FULL_MASK, k) == __reduce_max_sync(FULL_MASK, k)) {
+    if (k == NONE32) return;
+    const u32 mr = __reduce_max_sync(FULL_MASK, nr);
+    const u32 hi = __reduce_max_sync(FULL_MASK, (u32)(nt >> 32));
+    const u32 lo = __reduce_max_sync(FULL_MASK, (u32)(nt >> 32) == hi ? (u32)nt : 0u);
+    const u64 mt = (u64)hi << 32 | lo;
+    if (lane == 0 && (mr || mt)) { atomicMax(&a.peak_r[k], mr); atomic_max_u64(&a.peak_t[k], mt); }
+    return;
+  }
+  // else a warp segmented max over runs of equal keys (positions are sorted by key)
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     u32 ko = __shfl_up_sync(FULL_MASK, k, o);
