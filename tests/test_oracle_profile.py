@@ -113,3 +113,15 @@ def test_validation_errors():
     h = multi[0]
     bad["meta"][h] = (bad["meta"][h] & ~np.uint32(255 << 8)) | np.uint32(2 << 8)   # head relabelled stage 2
     assert O.validate(bad)[0] == -3
+
+
+def test_reachable_histogram_bins():
+    """The CUDA stream pass keeps only the bins a validated field can reach (profile.cuh
+    hb_off: 176 per length field, 192 for L_I + L_S + L_O, 48 for m): lengths < 2^24 (FS_E_RANGE
+    beyond), their sum < 3 * 2^24, m <= 255 (8-bit field).  Pinned against the
+    oracle's log-linear binning (monotone in the value, so the largest value gives the largest bin)."""
+    assert O.bin_of(2**24 - 1) == 175
+    assert O.bin_of(3 * (2**24 - 1)) <= 191
+    assert O.bin_of(255) == 47
+    vals = [0, 1, 7, 8, 9, 15, 16, 255, 256, 2**20, 2**24 - 1]
+    assert [O.bin_of(v) for v in vals] == sorted(O.bin_of(v) for v in vals)
