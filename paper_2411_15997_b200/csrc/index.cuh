@@ -137,10 +137,6 @@ static bool build_links(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
 }
 
 // ------------------------------------------------------------------ (t, id)-ordered index
-__global__ void k_key_user(DTrace t, u32* key) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < t.n) key[i] = t.user[i];
-}
 __global__ void k_key_user_app(DTrace t, u32* key) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < t.n) key[i] = t.user[i] * t.A + m_app(t.meta[i]);
@@ -162,13 +158,14 @@ struct Order {      // a stable (key, t, id) order of all calls
 // (key, t, id).
 static bool build_order(fs_ctx* ctx, Scratch& S, const DTrace& t, int kind, Order* o) {
   u64 n = t.n;
-  u32* k0 = S.alloc<u32>(n);
-  if (S.failed) return false;
   int B = 256;
-  if (n) {
-    if (kind == 1) FS_LAUNCH(ctx, "key_user_app", k_key_user_app, div_up(n, B), B, 0, t, k0);
-    else if (kind == 2) FS_LAUNCH(ctx, "key_app", k_key_app, div_up(n, B), B, 0, t, k0);
-    else FS_LAUNCH(ctx, "key_user", k_key_user, div_up(n, B), B, 0, t, k0);
+  const u32* k0 = t.user;                  // the user order sorts the trace's user field as is
+  if (kind != 0) {
+    u32* kk = S.alloc<u32>(n);
+    if (S.failed) return false;
+    if (n && kind == 1) FS_LAUNCH(ctx, "key_user_app", k_key_user_app, div_up(n, B), B, 0, t, kk);
+    else if (n) FS_LAUNCH(ctx, "key_app", k_key_app, div_up(n, B), B, 0, t, kk);
+    k0 = kk;
   }
   o->nseg = kind == 1 ? (u64)t.U * t.A : kind == 2 ? (u64)t.A : t.U;
   if (!radix_sort<u32>(ctx, S, k0, nullptr, n, bits_for(o->nseg ? o->nseg - 1 : 0), &o->key, &o->perm)) return false;
