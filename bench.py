@@ -41,10 +41,12 @@ def parse():
     ap.add_argument("--workload", default="c5", choices=["c2", "c3", "c4", "c5"])
     ap.add_argument("--calls", type=int, default=0, help="c4: total calls (default 100M)")
     ap.add_argument("--scenarios", type=int, default=4096, help="c5: scenarios per GPU (the whole grid with --sweep-split)")
-    ap.add_argument("--sweep-split", action="store_true",
-                    help="c5 at N>1: one grid split over the ranks (LPT, all_gather of summaries; strong scaling)")
+    ap.add_argument("--sweep-split", default="auto", choices=["auto", "on", "off"],
+                    help="c5 at N>1: one grid split over the ranks (LPT, all_gather of summaries; strong "
+                         "scaling, the default) or an independent grid per rank (off: weak scaling)")
+    ap.add_argument("--no-hbm", action="store_true", help="skip the full-size HBM lines (C4 profile, C3/C2 ACT)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--gen", default="cpu", choices=["cpu", "gpu"],
+    ap.add_argument("--gen", default="gpu", choices=["cpu", "gpu"],
                     help="c4: trace from tracegen.py (cpu) or fs_generate_trace on the device (gpu)")
     ap.add_argument("--timings", action="store_true", help="print per-kernel timings to stderr")
     return ap.parse_args()
@@ -170,6 +172,71 @@ ALGO_BYTES = {"prof_stream": 16, "win_scan": 28, "act_flags": 21, "pack_records"
               "radix_scatter": 16}   # radix pass: 4 B key + 4 B value read, the same written
 
 
+def participating(meta, scen):
+    """Participating calls of each scenario (tier <= tier_max): the units of requests/s (SURVEY
+    §8(d): calls in the (filtered) trace).  Filtered users' calls never arrive (Q35)."""
+    from paper_2411_15997_b200.fairserve import scenario_costs
+    return scenario_costs(meta, scen)
+
+
+def stratified_sample(scen):
+    """One scenario per abuse mix (tier_max 0..15): the middle one of the grid's scenarios with
+    that tier_max (throttle k, weights and E vary across the sample)."""
+    out = []
+    for tm in range(16):
+        c = [s for s in scen if s["tier_max"] == tm]
+        if c:
+            out.append(c[len(c) // 2])
+    return out
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def shard_device_trace(F, T, rank, world):
+    """Rank's user-hash shard of a device-resident trace (sm64(user) mod world, the split of
+    tracegen.shard_by_user), keeping (t_ms, id) order; interaction ids renumbered densely in
+    id order.  Input plumbing on the device (untimed); none of the method's arithmetic."""
+    import torch
+    u = T.t["user"].long() & 0xFFFFFFFF
+    M = (1 << 64) - 1
+
+    def c64(v):                                  # u64 constant as a wrapped int64
+        return v - (1 << 64) if v >= 1 << 63 else v
+
+    def shr(x, k):                               # logical right shift of u64 bits held in int64
+        return (x >> k) & ((1 << (64 - k)) - 1)
+    x = u + c64(0x9E3779B97F4A7C15)
+    x = (x ^ shr(x, 30)) * c64(0xBF58476D1CE4E5B9)
+    x = (x ^ shr(x, 27)) * c64(0x94D049BB133111EB)
+    x = x ^ shr(x, 31)
+    # unsigned mod: (hi * 2^32 + lo) mod w
+    hi, lo = shr(x, 32), x & 0xFFFFFFFF
+    h = ((hi % world) * ((1 << 32) % world) + lo % world) % world
+    keep = torch.nonzero(h == rank).squeeze(1)
+    t = {k: T.t[k].index_select(0, keep).contiguous() for k in F.FIELDS}
+    uniq, inv = torch.unique(t["inter"].long() & 0xFFFFFFFF, return_inverse=True)
+    t["inter"] = inv.to(torch.int32).contiguous()
+    del M
+    meta = dict(n_calls=int(keep.numel()), n_users=T.U, n_apps=T.A, n_inters=int(uniq.numel()))
+    return F.Trace(meta, tensors=t)
+
+
+def profile_sha(prof):
+    """sha256 over the finalised profile's tables (the G-invariance check of the sharded C4 line)."""
+    import hashlib
+    r = prof.read()
+    h = hashlib.sha256()
+    for k in sorted(x for x in r if hasattr(r[x], "tobytes")):
+        h.update(k.encode())
+        h.update(np.ascontiguousarray(r[k]).tobytes())
+    return h.hexdigest()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -191,34 +258,35 @@ def main():
     ctx = F.Context(local)
     stream = torch.cuda.current_stream()
     wl = args.workload
+    split = wl == "c5" and world > 1 and args.sweep_split != "off"
     c, eng, pcfg = workload_cfg("c2" if wl in ("c5", "c4") else wl)
+    c4_sha = None
     if wl == "c4":
-        # C4: one 100M-call profile sharded by user over the ranks (strong scaling): rank r
-        # holds users [r U/G, (r+1) U/G) with its share of the calls; NCCL SUM all-reduce rounds
+        # C4: ONE 100M-call trace (the same seed on every rank) sharded by user hash over the
+        # ranks (strong scaling); NCCL SUM all-reduce rounds; every G finalises the
+        # identical profile (config.profile_sha)
         c4 = G.CONFIGS["c4"]
         total = args.calls or c4["n_calls"]
-        Ur = c4["n_users"] // world
-        c4r = dict(c4, n_calls=total // world, n_users=Ur, seed=c4["seed"] + rank)
+        c4r = dict(c4, n_calls=total)
         if args.gen == "gpu":                       # NEXT-4 device generator (untimed setup)
-            Tg = F.generate_trace(ctx, c4r)
-            tr = {k: Tg.t[k].cpu().numpy().view(np.uint32) for k in F.FIELDS}
-            tr.update(n_calls=Tg.n, n_users=Tg.U, n_apps=Tg.A, n_inters=Tg.X)
-            del Tg
+            Tfull = F.generate_trace(ctx, c4r)
         else:
-            tr = G.generate(c4r)
-        tr["user"] = (tr["user"] + np.uint32(rank * Ur)).astype(np.uint32)
-        tr["n_users"] = Ur * world
+            Tfull = F.Trace(G.generate(c4r))
+        T = shard_device_trace(F, Tfull, rank, world) if world > 1 else Tfull
+        del Tfull
+        tr = {k: T.t[k].cpu().numpy().view(np.uint32) for k in F.FIELDS}
+        tr.update(n_calls=T.n, n_users=T.U, n_apps=T.A, n_inters=T.X)
         pcfg = dict(tier_max=0, window_ms=60000, max_stage=64)
     else:
-        # weak scaling: every rank gets its own independent problem (rank 0 = the BASELINE config)
-        split = wl == "c5" and args.sweep_split and world > 1
+        # c5 at N > 1 (default): one grid split over the ranks (strong scaling); --sweep-split off or
+        # c2/c3: every rank gets its own independent problem (weak scaling; rank 0 = the BASELINE config)
         tr = G.generate(wl, seed=G.CONFIGS[wl]["seed"] + (0 if split else rank))
+        T = F.Trace(tr)                                            # inputs resident in HBM before timing
     N = tr["n_calls"]
-    T = F.Trace(tr)                                                # inputs resident in HBM before timing
     host = {k: torch.from_numpy(np.ascontiguousarray(tr[k]).view(np.int32)).pin_memory() for k in F.FIELDS}
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device="cuda")   # > 126 MB L2
     scen = sweep_scenarios(eng, args.scenarios) if wl == "c5" else None
-    outs = F.replay_outputs(ctx, T) if wl != "c4" else None
+    outs = F.replay_outputs(ctx, T) if wl not in ("c4",) else None
     status = torch.empty(N, dtype=torch.uint8, device="cuda")
 
     def step(trace):
@@ -244,13 +312,14 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    last = None
     with Clocks(local) as clk:
         for _ in range(args.steps):
             flush.zero_()                                  # L2 flush between timed steps (not timed)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            step(T)
+            last = step(T)
             b.record(stream)
             evs.append((a, b))
         torch.cuda.synchronize()
@@ -258,6 +327,11 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in evs)
     kt = ctx.timings()
     launches = sum(v[0] for v in kt.values())
+    if wl == "c4":
+        c4_sha = profile_sha(last)
+    sweep_codes_ok = None
+    if scen is not None:
+        sweep_codes_ok = bool((np.asarray(last[1]) == 0).all())
     # end to end through the public API with host buffers: H2D of the trace, the step, D2H of the results
     e2e_steps = 1 if scen is not None else max(1, min(args.steps, 3))
     e2e_ms = 0.0
@@ -278,6 +352,7 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         e2e_ms += a.elapsed_time(b)
+        del T2
     # one single replay of the C2 configuration on this trace (BASELINE configs[1]), for context
     single = None
     if scen is not None and rank == 0:
@@ -295,15 +370,23 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, e2e_step_ms = float(t[0]), float(t[1])
-    units_per_rank = N * (len(scen) if scen is not None else 1)
-    total_units = units_per_rank * world               # c4: the ranks' shards sum to the one trace
-    if wl == "c5" and args.sweep_split and world > 1:
-        total_units = units_per_rank                   # one grid over all ranks
+    # requests/s counts the calls in the (filtered) trace: a sweep scenario's units
+    # are its participating calls (tier <= tier_max); filtered users' calls never arrive
+    units_per_rank = sum(participating(tr["meta"], scen)) if scen is not None else N
+    calls_replayed_per_rank = N * len(scen) if scen is not None else N
+    grids = 1 if split else world
+    total_units = units_per_rank * grids               # c4: the ranks' shards sum to the one trace
+    if wl == "c4":
+        total_units = units_per_rank * world
     value = total_units * args.steps / (ms_max / 1e3)
     e2e_value = total_units / (e2e_step_ms / 1e3)
     if args.timings and rank == 0:
         for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1]):
             sys.stderr.write(f"{k:28s} launches={v[0]:7d} total_ms={v[1]:10.3f} per_step_ms={v[1] / args.steps:9.3f}\n")
+    hbm = None
+    if rank == 0 and world == 1 and wl == "c5" and not args.no_hbm:
+        del host
+        hbm = hbm_lines(ctx, F, G, T, outs, eng, flush)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -313,15 +396,21 @@ def main():
     dom_name, (dom_launches, dom_ms) = max(kt.items(), key=lambda kv: kv[1][1])
     roof = roofline(dom_name, dom_launches, dom_ms, N, peaks, peak_src, args, kt)
     S = len(scen) if scen is not None else 0
+    cfg = dict(workload_config(wl, N * world if wl == "c4" else N, tr["n_users"], tr["n_apps"], S, world,
+                               split=split),
+               l2="flushed between timed steps (256 MB write, untimed)")
+    if scen is not None:
+        cfg.update(participating_calls_per_grid=units_per_rank, replayed_calls_per_grid=calls_replayed_per_rank,
+                   all_scenario_codes_ok=sweep_codes_ok)
+    if wl == "c4":
+        cfg.update(profile_sha=c4_sha, trace="fs_generate_trace (device)" if args.gen == "gpu" else "tracegen.py")
     line = {
         "metric": "trace requests throttled+scheduled/sec",
         "value": value, "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong" if wl == "c4" or (wl == "c5" and args.sweep_split and world > 1) else "weak",
+        "scaling": "strong" if wl == "c4" or split else "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": dict(workload_config(wl, N * world if wl == "c4" else N, tr["n_users"], tr["n_apps"], S, world,
-                                       split=wl == "c5" and args.sweep_split and world > 1),
-                       l2="flushed between timed steps (256 MB write, untimed)"),
+        "config": cfg,
         "e2e": {"value": e2e_value, "unit": "requests/s", "h2d_bytes_per_step": 32 * N,
                 "d2h_bytes_per_step": d2h_c4 if wl == "c4" else (N if scen is None else 144 * S)},
         "gpu_launches": int(launches),
@@ -329,8 +418,12 @@ def main():
         "stage_ms": {k: v[1] / args.steps for k, v in sorted(kt.items(), key=lambda kv: -kv[1][1])[:8]},
         "clocks": clk.summary(),
     }
+    if scen is not None:
+        line["replayed_calls_per_s"] = calls_replayed_per_rank * grids * args.steps / (ms_max / 1e3)
     if single:
         line["single_replay"] = single
+    if hbm:
+        line["hbm"] = hbm
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(wl, tr)
     print(json.dumps(line), flush=True)
@@ -339,6 +432,121 @@ def main():
         dist.destroy_process_group()
 
 
+# algorithmic bytes per call of the HBM-bound stages
+PROFILE_ALGO_B = 56          # one read of user, t, meta, L_I, L_S, L_O (24 B) + per order 16 B (perm + (t, tau))
+ACT_ALGO_B = 30              # user, t, meta, L_I, L_S, inter, overload (25 B) + perm (4 B) + status (1 B):
+                             # one pass; the fixed-point passes the implementation adds are not credited
+
+
+def _time_calls(ctx, fn, flush, stream, reps):
+    """mean device ms of `reps` L2-flushed calls after one warm-up, and the library's per-kernel times"""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    ctx.timing_reset()
+    ctx.set_timing(True)
+    tot = 0.0
+    for _ in range(reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    ctx.set_timing(False)
+    return tot / reps, ctx.timings()
+
+
+def _stage_line(name, ms, n, algo_b, peaks, kt, reps, ncu):
+    gbs = algo_b * n / (ms / 1e3) / 1e9
+    kern = []
+    for k, (l, t) in sorted(kt.items(), key=lambda kv: -kv[1][1])[:12]:
+        e = {"kernel": k, "ms": t / reps, "launches": l / reps}
+        if ncu and k in ncu:
+            e["ncu_dram_bytes_per_call"] = ncu[k]
+        kern.append(e)
+    return {"workload": name, "calls": n, "ms": ms, "calls_per_s": n / (ms / 1e3),
+            "algorithmic_bytes_per_call": algo_b, "achieved_gbs": gbs, "peak_gbs": peaks["hbm_gbs"],
+            "frac": gbs / peaks["hbm_gbs"], "kernels": kern}
+
+
+def ncu_bytes_per_call(path, n):
+    """{kernel: DRAM bytes (read + write) per call per launch} from a committed ncu --csv capture."""
+    import csv
+    out = {}
+    try:
+        rows = [r for r in csv.reader(open(path)) if r and not r[0].startswith("==")]
+    except OSError:
+        return out
+    hdr = rows[0]
+    ix = {h: i for i, h in enumerate(hdr)}
+    acc = {}
+    for r in rows[1:]:
+        try:
+            nm = r[ix["Kernel Name"]].split("(")[0].split("<")[0].replace("k_", "", 1)
+            if r[ix["Metric Name"]] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                v = float(r[ix["Metric Value"]].replace(",", ""))
+                unit = r[ix["Metric Unit"]]
+                v *= {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+                acc.setdefault((nm, r[ix["ID"]]), 0.0)
+                acc[(nm, r[ix["ID"]])] += v
+        except (KeyError, ValueError, IndexError):
+            pass
+    per = {}
+    for (nm, _), v in acc.items():
+        per.setdefault(nm, []).append(v)
+    for nm, vs in per.items():
+        out[nm] = sum(vs) / len(vs) / n
+    return out
+
+
+def hbm_lines(ctx, F, G, T5, outs, eng, flush):
+    """The HBM half of the metric at full size (north_star: profile + ACT >= 50 % of HBM peak),
+    in the default run: (1) the 100M-call C4 profile on a device-generated trace, (2) ACT on a
+    device-generated 10M-call C3 trace with overload always on (the heavy worst-case screening
+    path), (3) ACT on the C2/C5 trace with the single replay's recorded arrivals and overload
+    flags.  Generation is untimed; each stage is the median-free mean of `reps` L2-flushed runs."""
+    import torch
+    stream = torch.cuda.current_stream()
+    peaks, _ = load_peaks()
+    res = {}
+    reps = 3
+    T4 = F.generate_trace(ctx, "c4")
+    p4 = dict(tier_max=0, window_ms=60000, max_stage=64)
+    ms, kt = _time_calls(ctx, lambda: F.build_app_profiles(ctx, T4, p4), flush, stream, reps)
+    res["c4_profile"] = _stage_line("C4 fs_build_app_profiles, 100M calls (device-generated), tier_max 0",
+                                    ms, T4.n, PROFILE_ALGO_B, peaks, kt, reps,
+                                    ncu_bytes_per_call(os.path.join(ROOT, "profiles", "r02_c4_dram.csv"), T4.n))
+    del T4
+    torch.cuda.synchronize()
+    T3 = F.generate_trace(ctx, "c3")
+    _, e3, p3 = workload_cfg("c3")
+    prof3 = F.build_app_profiles(ctx, T3, p3)
+    st3 = torch.empty(T3.n, dtype=torch.uint8, device="cuda")
+    summ = {}
+    ms, kt = _time_calls(ctx, lambda: summ.update(F.act_throttle(ctx, T3, prof3, e3["act"], status=st3)[1]),
+                         flush, stream, reps)
+    res["c3_act_overload_always"] = _stage_line(
+        "C3 fs_act_throttle, 10M calls (device-generated), overload always", ms, T3.n, ACT_ALGO_B, peaks, kt, reps,
+        ncu_bytes_per_call(os.path.join(ROOT, "profiles", "r02_c3_act_dram.csv"), T3.n))
+    res["c3_act_overload_always"]["summary"] = summ
+    del T3, prof3, st3
+    # ACT on the C2 trace with the single replay's recorded arrival times and overload flags
+    _, e2, p2 = workload_cfg("c2")
+    prof2 = F.build_app_profiles(ctx, T5, p2)
+    st2 = torch.empty(T5.n, dtype=torch.uint8, device="cuda")
+    summ = {}
+    ms, kt = _time_calls(ctx, lambda: summ.update(F.act_throttle(ctx, T5, prof2, e2["act"], overloaded=outs["ovl"],
+                                                                 t_ns_override=outs["arrive_ns"], status=st2)[1]),
+                         flush, stream, reps)
+    res["c2_act_replay_flags"] = _stage_line(
+        "C2 fs_act_throttle, 1M calls, the replay's arrival times + overload flags", ms, T5.n, ACT_ALGO_B, peaks,
+        kt, reps, None)
+    res["c2_act_replay_flags"]["summary"] = summ
+    res["c2_act_replay_flags"]["equals_replay_status"] = bool(torch.equal(st2, outs["status"]))
+    return res
 
 
 def ncu_csv(path):
@@ -405,13 +613,23 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
             "traffic": traffic, "algorithmic_bytes_per_launch": b, "peak_source": src, "hbm_stages": stages}
 
 
+def oracle_sweep_parallel(O, tr, p, scen, P):
+    """the oracle's replays (oracle/, single-threaded C++ each) run side by side on P host threads
+    (ctypes releases the GIL; the oracle keeps no global state): the P-core CPU baseline of
+    BASELINE.md §5"""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(P) as ex:
+        return list(ex.map(lambda s: O.sweep(tr, p, [s]), sorted(scen, key=lambda s: -s["tier_max"])))
+
+
 def cpu_baseline(workload, tr):
     """The oracle as it stands (oracle/, single-threaded C++) on a bounded sample of the
-    same workload, timed on this host."""
+    same workload, timed on this host; the sweep's sample runs on all host cores."""
     import oracle as O
     from paper_2411_15997_b200 import tracegen as G
     c, eng, pcfg = workload_cfg("c2" if workload == "c5" else workload)
     sample, desc = tr, "full trace"
+    cores = 1
     if workload == "c3":
         sample = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
         desc = "C3-shaped 1M-call / 1k-user sample: profile + FS(W+I) replay + ACT"
@@ -424,18 +642,30 @@ def cpu_baseline(workload, tr):
     if workload == "c4":
         pass
     elif workload == "c5":
-        scen = sweep_scenarios(eng, 4096)
-        picks = [scen[0], scen[len(scen) // 2]]
-        O.sweep(sample, p, picks)
-        n *= len(picks)
-        desc = "C5 trace: profile + 2 of the grid's scenario replays"
+        picks = stratified_sample(sweep_scenarios(eng, 4096))
+        cores = min(host_cores(), len(picks))
+        oracle_sweep_parallel(O, sample, p, picks, cores)
+        n = sum(participating(sample["meta"], picks))
+        desc = (f"C5 trace: profile + {len(picks)} of the grid's replays (one per tier_max 0..15, "
+                f"stratified) on {cores} host threads; units = participating calls")
     else:
         o, _ = O.replay(sample, p, eng)
         O.act(sample, p, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
         if workload == "c2":
             desc = "full C2 step: profile + FS(W+I) replay + ACT"
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt}
+    return {"value": n / dt, "unit": "requests/s", "cores": cores, "kind": "oracle", "sample": desc, "seconds": dt,
+            "cpu": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def reference(args, rank, world):
@@ -445,6 +675,7 @@ def reference(args, rank, world):
     from paper_2411_15997_b200 import tracegen as G
     wl = args.workload
     c, eng, pcfg = workload_cfg("c2" if wl == "c5" else wl)
+    cores = 1
     if wl == "c3":
         tr = G.generate(dict(G.CONFIGS["c3"], n_users=1000, n_calls=1_000_000, seed=3))
         desc = "C3-shaped 1M-call / 1k-user sample per step"
@@ -453,18 +684,20 @@ def reference(args, rank, world):
         desc = "C4-shaped 2M-call / 2k-user sample per step: profile"
     else:
         tr = G.generate("c2")
-        desc = "full C2 step" if wl == "c2" else "C5 trace: profile + 2 of the grid's scenario replays per step"
+        desc = "full C2 step"
     O.build()
-
-    scen = sweep_scenarios(eng, 4096)
-    picks = [scen[0], scen[len(scen) // 2]]
+    picks = stratified_sample(sweep_scenarios(eng, 4096))
+    if wl == "c5":
+        cores = min(host_cores(), len(picks))
+        desc = (f"C5 trace per step: profile + {len(picks)} of the grid's replays (one per tier_max 0..15, "
+                f"stratified) on {cores} host threads; units = participating calls")
 
     def step():
         p = O.profile(tr, pcfg)
         if wl == "c4":
             return
         if wl == "c5":
-            O.sweep(tr, p, picks)
+            oracle_sweep_parallel(O, tr, p, picks, cores)
             return
         o, _ = O.replay(tr, p, eng)
         O.act(tr, p, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
@@ -475,16 +708,18 @@ def reference(args, rank, world):
     for _ in range(args.steps):
         step()
     dt = time.perf_counter() - t0
-    n = tr["n_calls"] * (2 if wl == "c5" else 1)
+    n = sum(participating(tr["meta"], picks)) if wl == "c5" else tr["n_calls"]
     v = n * args.steps / dt
+    split = wl == "c5" and world > 1 and args.sweep_split != "off"
     line = {"impl": "reference", "metric": "trace requests throttled+scheduled/sec", "value": v,
             "unit": "requests/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "strong" if wl == "c4" else "weak",
+            "scaling": "strong" if wl == "c4" or split else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": workload_config(wl, G.CONFIGS[wl]["n_calls"], G.CONFIGS[wl]["n_users"], n_apps_of(wl),
-                                      args.scenarios if wl == "c5" else 0, 1),
-            "cpu_baseline": {"value": v, "unit": "requests/s", "cores": 1, "kind": "oracle", "sample": desc},
+                                      args.scenarios if wl == "c5" else 0, world, split=split),
+            "cpu_baseline": {"value": v, "unit": "requests/s", "cores": cores, "kind": "oracle", "sample": desc,
+                             "cpu": cpu_model()},
             "e2e": {"value": v, "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -49,6 +49,18 @@ int fs_ctx_error_detail(const fs_ctx* ctx, uint64_t* first_bad_index_h, char* ms
  * enable=1 starts accumulating; fs_ctx_timing_read returns up to cap entries. */
 typedef struct { char name[40]; uint64_t launches; double total_ms; } fs_kernel_time;
 int fs_ctx_set_timing(fs_ctx* ctx, int enable);
+/* Device memory for the library's scratch and its opaque objects (SURVEY §8(b) conventions):
+ * with an allocator installed, every device allocation the library makes after this call
+ * (scratch of each call, fs_profile / fs_profile_partial / fs_wsc_state storage) comes from
+ * alloc(bytes, user) and goes back through free_(ptr, user) -- e.g. torch's caching allocator
+ * on the ctx stream.  alloc returns NULL on failure (the call then returns FS_E_NOMEM).  Both
+ * NULL restores the default (cudaMallocAsync / cudaFreeAsync on the ctx stream).  Objects keep
+ * the allocator they were created with; it must outlive them.  Frees are issued after the
+ * call's work is enqueued on the ctx stream (stream-ordered reuse, as torch's allocator does).
+ * Returns FS_E_INVAL if exactly one of alloc / free_ is NULL. */
+typedef void* (*fs_alloc_fn)(size_t bytes, void* user);
+typedef void (*fs_free_fn)(void* ptr, void* user);
+int fs_ctx_set_allocator(fs_ctx* ctx, fs_alloc_fn alloc, fs_free_fn free_, void* user);
 int fs_ctx_timing_read(fs_ctx* ctx, fs_kernel_time* out_h, int cap, int* n_h);
 int fs_ctx_timing_reset(fs_ctx* ctx);
 
@@ -217,7 +229,16 @@ typedef struct {
 int fs_wsc_replay(fs_ctx* ctx, const fs_trace* trace, const fs_profile* profile, const fs_replay_cfg* cfg,
                   const fs_replay_out* out, fs_replay_summary* sum_h);
 
-/* fs_wsc_step: one iteration boundary of Alg. 1 on a persistent device state:
+/* fs_wsc_state_create: the persistent scheduler state of the online form of Alg. 1 --
+ * the policy's two hooks, arrival on the monitoring stream and pick/finish on the execution
+ * stream (SPEC hooks S:147-150) -- for one trace (call ids index its records), one
+ * profile (Eq. 2 weights; limits) and one config.  Holds the counters u_i
+ * (all 0), the per-user FIFOs and Q (empty), e = NONE (Alg. 1 l.13-15) and the ACT
+ * window logs (Alg. 1 l.19).  Errors: FS_E_INVAL (bad config, RPM or app-global scope:
+ * their windows need ordered arrivals, R8/R10), FS_E_PROFILE, FS_E_NOMEM; trace errors as
+ * fs_wsc_replay.  After a failed fs_wsc_step the state is poisoned and later steps return
+ * FS_E_PROTOCOL.
+ * fs_wsc_step: one iteration boundary of Alg. 1 on a persistent device state:
  * apply finishes (l.44-48), deliver arrivals in the given order (l.11-25, overload
  * from occ_tokens), then the admission round (l.28-39) with occ_tokens/batch_size.
  * finished/arrived/arrived_ns/arrival_status/admitted are DEVICE arrays; admitted
@@ -232,9 +253,16 @@ int fs_wsc_step(fs_ctx* ctx, fs_wsc_state* st, int64_t now_ns, int64_t occ_token
 int fs_wsc_state_read(fs_ctx* ctx, const fs_wsc_state* st, uint64_t* counters_h, int32_t* last_exit_h);
 void fs_wsc_state_free(fs_wsc_state* st);
 
-/* fs_sweep: n_scen independent replays of one trace (thresholds x weights x abuse
- * mixes); scen_h host array of configs (prio_q16 must be NULL); out_h host array of
- * summaries; codes_h host array of per-scenario fs_status. */
+/* fs_sweep: n_scen independent fs_wsc_replay runs (Alg. 1 whole) of one trace
+ * over a grid of the paper's knobs -- throttle thresholds (the limits T "based on the analysis
+ * of historical data", scaled by act.limit_mult_q8), WSC token weights (alpha, beta,
+ * gamma of Eq. 2) and priorities E (Eq. 3), and abuse mixes (tier_max: which
+ * abusive users exist) -- the north star's "many independent replays over thresholds,
+ * weights and abusive-user mixes".  scen_h: host array of n_scen configs (prio_q16 must be
+ * NULL; FS(W+I) scenarios share one window and token-load weight set).  out_h: host array of
+ * n_scen summaries, each bit-identical to fs_wsc_replay's for that config.  codes_h: host
+ * array of per-scenario fs_status (a scenario's data error does not stop the others).
+ * Returns FS_E_INVAL for bad arguments, else the first trace-level error, else FS_OK. */
 int fs_sweep(fs_ctx* ctx, const fs_trace* trace, const fs_profile* profile, const fs_replay_cfg* scen_h,
              uint32_t n_scen, fs_replay_summary* out_h, int32_t* codes_h);
 

@@ -592,6 +592,7 @@ struct fs_wsc_state {
   i64* scal;
   u32 p_cap, U;
   DTrace t;
+  bool poisoned = false;                  // a failed step may leave the heaps mid-update
   ~fs_wsc_state() { delete S; }
 };
 
@@ -663,6 +664,7 @@ extern "C" int fs_wsc_step(fs_ctx* ctx, fs_wsc_state* st, int64_t now_ns, int64_
   (void)now_ns;
   if (!ctx || !st || !n_admitted || (nfin && !fin) || (narr && (!arr || !arr_t || !arr_status)) || !admitted)
     return FS_E_INVAL;
+  if (st->poisoned) return FS_E_PROTOCOL;
   Scratch S(ctx);
   err_reset(ctx);
   int* dcode = S.zeros<int>(1);
@@ -677,8 +679,12 @@ extern "C" int fs_wsc_step(fs_ctx* ctx, fs_wsc_state* st, int64_t now_ns, int64_
   cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
   cudaMemcpyAsync(&hidx, didx, 8, cudaMemcpyDeviceToHost, ctx->stream);
   int rc = finish(ctx, &S);
-  if (rc) return rc;
-  if (hcode) { ctx->bad_index = hidx; return ERR_TO_FS[hcode - 1]; }
+  if (rc) { st->poisoned = true; return rc; }
+  if (hcode) {
+    st->poisoned = true;
+    ctx->bad_index = hidx;
+    return hcode == STEP_E_INVAL ? FS_E_INVAL : ERR_TO_FS[hcode - 1];
+  }
   return FS_OK;
 }
 

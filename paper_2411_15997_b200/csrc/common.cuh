@@ -44,7 +44,26 @@ struct fs_ctx {
   std::vector<TimerRec> pending;
   std::vector<TimeAcc> acc;
   std::vector<cudaEvent_t> pool;
+  fs_alloc_fn ualloc = nullptr;   // fs_ctx_set_allocator (e.g. torch's caching allocator), else
+  fs_free_fn ufree = nullptr;     // cudaMallocAsync / cudaFreeAsync on the ctx stream
+  void* uuser = nullptr;
 };
+
+// Device memory through the context's allocator.  An object records the allocator it was
+// created with (DevAlloc) so it can be freed after the context changed allocators.
+struct DevAlloc {
+  fs_free_fn ufree = nullptr; void* uuser = nullptr; cudaStream_t stream = nullptr;
+  void release(void* p) const {
+    if (!p) return;
+    if (ufree) ufree(p, uuser); else cudaFreeAsync(p, stream);
+  }
+};
+static inline DevAlloc ctx_devalloc(const fs_ctx* c) { return DevAlloc{c->ufree, c->uuser, c->stream}; }
+static inline void* ctx_malloc(fs_ctx* c, size_t bytes) {
+  if (c->ualloc) return c->ualloc(bytes ? bytes : 1, c->uuser);
+  void* p = nullptr;
+  return cudaMallocAsync(&p, bytes ? bytes : 1, c->stream) == cudaSuccess ? p : nullptr;
+}
 
 cudaEvent_t ctx_event(fs_ctx* c);
 void ctx_timing_flush(fs_ctx* c);
@@ -59,17 +78,19 @@ void ctx_timing_flush(fs_ctx* c);
   } while (0)
 
 // ------------------------------------------------------------------ scratch
-// Stream-ordered allocations freed at scope exit (cudaMallocAsync pool).
+// Stream-ordered allocations freed at scope exit (the context's allocator: fs_ctx_set_allocator,
+// else the cudaMallocAsync pool).
 struct Scratch {
   fs_ctx* ctx;
+  DevAlloc da;
   std::vector<void*> ptrs;
   bool failed = false;
-  explicit Scratch(fs_ctx* c) : ctx(c) {}
-  ~Scratch() { for (void* p : ptrs) cudaFreeAsync(p, ctx->stream); }
+  explicit Scratch(fs_ctx* c) : ctx(c), da(ctx_devalloc(c)) {}
+  ~Scratch() { for (void* p : ptrs) da.release(p); }
   template <class T> T* alloc(size_t n) {
-    void* p = nullptr;
     if (n == 0) n = 1;
-    if (cudaMallocAsync(&p, n * sizeof(T), ctx->stream) != cudaSuccess) { failed = true; return nullptr; }
+    void* p = ctx_malloc(ctx, n * sizeof(T));
+    if (!p) { failed = true; return nullptr; }
     ptrs.push_back(p);
     return (T*)p;
   }

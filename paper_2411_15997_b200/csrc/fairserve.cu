@@ -114,6 +114,12 @@ extern "C" int fs_ctx_error_detail(const fs_ctx* c, uint64_t* idx, char* msg, si
   return FS_OK;
 }
 
+extern "C" int fs_ctx_set_allocator(fs_ctx* c, fs_alloc_fn alloc, fs_free_fn free_, void* user) {
+  if (!c || (!alloc) != (!free_)) return FS_E_INVAL;
+  c->ualloc = alloc; c->ufree = free_; c->uuser = user;
+  return FS_OK;
+}
+
 extern "C" int fs_ctx_set_timing(fs_ctx* c, int on) { if (!c) return FS_E_INVAL; c->timing = on; return FS_OK; }
 extern "C" int fs_ctx_timing_reset(fs_ctx* c) { if (!c) return FS_E_INVAL; ctx_timing_flush(c); c->acc.clear(); return FS_OK; }
 extern "C" int fs_ctx_timing_read(fs_ctx* c, fs_kernel_time* out, int cap, int* n) {
@@ -237,7 +243,7 @@ extern "C" int fs_profile_local(fs_ctx* ctx, const fs_trace* tr, const fs_profil
   pp->qppm.assign(cfg->q_ppm_h, cfg->q_ppm_h + cfg->n_q);
   pp->cfg.q_ppm_h = pp->qppm.data();
   const u32 A = tr->n_apps, J = cfg->max_stage, U = tr->n_users, nq = cfg->n_q;
-  pp->P = profile_alloc(A, J, U, nq, ctx->stream);
+  pp->P = profile_alloc(ctx, A, J, U, nq);
   if (!pp->P) { delete pp; return FS_E_NOMEM; }
   pp->P->q_ppm = pp->qppm;
   err_reset(ctx);
@@ -387,8 +393,9 @@ extern "C" int fs_build_app_profiles(fs_ctx* ctx, const fs_trace* tr, const fs_p
   size_t words = 0;
   int rc = fs_profile_local(ctx, tr, cfg, &pp, &words);
   if (rc) return rc;
-  u64* buf = nullptr;
-  if (cudaMallocAsync(&buf, words * 8 + 8, ctx->stream) != cudaSuccess) { fs_profile_partial_free(pp); return FS_E_NOMEM; }
+  const DevAlloc da = ctx_devalloc(ctx);
+  u64* buf = (u64*)ctx_malloc(ctx, words * 8 + 8);
+  if (!buf) { fs_profile_partial_free(pp); return FS_E_NOMEM; }
   int done = 0;
   for (int r = 0; r < 8 && !done; r++) {        // one rank: the "reduced" payload is our own
     size_t w = 0;
@@ -397,8 +404,8 @@ extern "C" int fs_build_app_profiles(fs_ctx* ctx, const fs_trace* tr, const fs_p
   }
   if (!rc && !done) rc = FS_E_PROTOCOL;
   if (!rc) rc = fs_profile_finalize(pp, out);
-  cudaFreeAsync(buf, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
+  da.release(buf);
   fs_profile_partial_free(pp);
   return rc;
 }
@@ -407,7 +414,7 @@ extern "C" int fs_profile_from_host(fs_ctx* ctx, uint32_t A, uint32_t J, const u
                                     const uint64_t* s_sys, const uint64_t* s_out, const uint32_t* T_req_a,
                                     uint32_t T_req_g, const uint64_t* T_tok_a, uint64_t T_tok_g, fs_profile** out) {
   if (!ctx || !out || !cnt || !s_in || !s_sys || !s_out || A == 0 || A > 255 || J == 0 || J > 255) return FS_E_INVAL;
-  fs_profile* P = profile_alloc(A, J, 0, 0, ctx->stream);
+  fs_profile* P = profile_alloc(ctx, A, J, 0, 0);
   if (!P) return FS_E_NOMEM;
   u64 AJ = (u64)A * (J + 1);
   cudaStream_t s = ctx->stream;
@@ -455,7 +462,7 @@ extern "C" int fs_profile_read(fs_ctx* ctx, const fs_profile* P, fs_profile_host
 
 extern "C" void fs_profile_free(fs_profile* P) {
   if (!P) return;
-  cudaFreeAsync(P->block, P->stream);       // the creating context's stream (torch's current stream)
+  P->da.release(P->block);                 // the creating context's allocator / stream
   delete P;
 }
 

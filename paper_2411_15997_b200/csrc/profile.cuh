@@ -15,6 +15,7 @@ struct fs_profile {
   std::vector<u32> q_ppm;
   void* block = nullptr;                  // one device allocation for everything below
   cudaStream_t stream = nullptr;          // stream-ordered allocation / free (no device-wide syncs)
+  DevAlloc da;                            // the allocator the block came from
   u64 *cnt, *sum_in, *sum_sys, *sum_out, *ohat;   // [A][J1]
   u32* maxstage;                                  // [A]
   u64* hist;                                      // [A][5][240]
@@ -40,7 +41,8 @@ template <class T> static T* carve(char*& p, size_t n) {
   return r;
 }
 
-static fs_profile* profile_alloc(u32 A, u32 J, u32 U, u32 nq, cudaStream_t s) {
+static fs_profile* profile_alloc(fs_ctx* ctx, u32 A, u32 J, u32 U, u32 nq) {
+  cudaStream_t s = ctx->stream;
   fs_profile* P = new fs_profile();
   P->A = A; P->J = J; P->U = U; P->nq = nq;
   u64 J1 = J + 1;
@@ -51,9 +53,11 @@ static fs_profile* profile_alloc(u32 A, u32 J, u32 U, u32 nq, cudaStream_t s) {
   add((size_t)A * 4 * nq * 4); add((size_t)A * 4 * nq * 8);
   add(U * 4); add(U * 8); add((size_t)U * A * 4); add((size_t)U * A * 8);
   add(A * 4); add(A * 8); add(4); add(8); add(A * 4); add(A * 8); add(4); add(8);
-  if (cudaMallocAsync(&P->block, bytes, s) != cudaSuccess) { delete P; return nullptr; }
+  P->block = ctx_malloc(ctx, bytes);
+  if (!P->block) { delete P; return nullptr; }
   cudaMemsetAsync(P->block, 0, bytes, s);
   P->stream = s;
+  P->da = ctx_devalloc(ctx);
   char* p = (char*)P->block;
   P->cnt = carve<u64>(p, A * J1); P->sum_in = carve<u64>(p, A * J1); P->sum_sys = carve<u64>(p, A * J1);
   P->sum_out = carve<u64>(p, A * J1); P->ohat = carve<u64>(p, A * J1);

@@ -1024,6 +1024,10 @@ struct StepKArgs {
   const u32* fin; u32 nfin; const u32* arr; const i64* arr_t; u32 narr;
   uint8_t* arr_status; u32* admitted; u32* n_admitted; int* err_code; u64* err_idx;
 };
+// error codes: ERR_* + 1, or STEP_E_INVAL (a finished call of a filtered user, as the oracle's
+// or_step).  The persistent scalars are written back on every exit path; after an error the host
+// poisons the state (the heaps may be mid-update), so no later step sees it.
+static const int STEP_E_INVAL = 1000;
 __global__ void k_step(const __grid_constant__ StepKArgs a) {
   if (threadIdx.x != 0) return;
   EngState st;
@@ -1038,12 +1042,19 @@ __global__ void k_step(const __grid_constant__ StepKArgs a) {
   E.static_heads = false;                                         // caller-given arrival times
   E.occ = a.occ;
   *a.err_code = 0;
+  auto save = [&]() { a.scal[0] = E.e; a.scal[1] = E.seq; a.scal[2] = E.hk_n; a.scal[3] = E.hm_n; a.scal[4] = E.c_top; };
+  auto fail = [&](int code, u64 idx) { *a.err_code = code; *a.err_idx = idx; save(); };
+  const u64 n = a.sh.t.n;
   for (u32 q = 0; q < a.nfin; q++) {                              // l.44-48
-    if (!E.charge_call(a.fin[q])) { *a.err_code = E.err_code + 1; *a.err_idx = a.fin[q]; return; }
+    const u32 r = a.fin[q];
+    if (r >= n) { fail(ERR_RANGE + 1, q); return; }              // oracle or_step: index into the list
+    if (m_tier(__ldg(&a.sh.recA[r]).z) > a.cfg.tier_max) { fail(STEP_E_INVAL, q); return; }
+    if (!E.charge_call(r)) { fail(E.err_code + 1, r); return; }
   }
   bool ovl = E.overloaded();
   for (u32 q = 0; q < a.narr; q++) {                              // l.11-25
     u32 r = a.arr[q];
+    if (r >= n) { fail(ERR_RANGE + 1, q); return; }
     uint4 A = ldg4(&a.sh.recA[r]);
     if (m_tier(A.z) > a.cfg.tier_max) { a.arr_status[q] = FS_ST_FILTERED; continue; }
     int s;
@@ -1055,7 +1066,7 @@ __global__ void k_step(const __grid_constant__ StepKArgs a) {
     } else {
       s = E.deliver_cont(r, A.x, A.z, a.arr_t[q], ovl);
     }
-    if (s < 0) { *a.err_code = E.err_code + 1; *a.err_idx = r; return; }
+    if (s < 0) { fail(E.err_code + 1, r); return; }
     a.arr_status[q] = (uint8_t)s;
   }
   u32 na = 0;                                                      // l.28-39
@@ -1067,7 +1078,7 @@ __global__ void k_step(const __grid_constant__ StepKArgs a) {
     nb++;
   }
   *a.n_admitted = na;
-  a.scal[0] = E.e; a.scal[1] = E.seq; a.scal[2] = E.hk_n; a.scal[3] = E.hm_n; a.scal[4] = E.c_top;
+  save();
 }
 __global__ void k_step_read(u32 U, const UState* us, u64* out) {
   u32 k = blockIdx.x * blockDim.x + threadIdx.x;

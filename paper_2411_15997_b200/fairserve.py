@@ -44,7 +44,7 @@ def lib():
                                          C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_uint64))
         sig = {
             "fs_ctx_create": [I, V, PV], "fs_ctx_destroy": [V], "fs_ctx_error_detail": [V, PU64, C.c_char_p, SZ],
-            "fs_ctx_set_timing": [V, I], "fs_ctx_timing_read": [V, V, I, PI], "fs_ctx_timing_reset": [V],
+            "fs_ctx_set_timing": [V, I], "fs_ctx_set_allocator": [V, V, V, V], "fs_ctx_timing_read": [V, V, I, PI], "fs_ctx_timing_reset": [V],
             "fs_build_app_profiles": [V, V, V, PV],
             "fs_profile_from_host": [V, U32, U32, V, V, V, V, V, U32, V, U64, PV],
             "fs_profile_get_dims": [V, V], "fs_profile_read": [V, V, V], "fs_profile_free": [V],
@@ -155,6 +155,10 @@ def _dp(t):
     return None if t is None else t.data_ptr()
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
 class Context:
     """fs_ctx bound to a CUDA device and (by default) torch's current stream."""
 
@@ -173,6 +177,28 @@ class Context:
             if self.h:
                 lib().fs_ctx_error_detail(self.h, C.byref(idx), msg, C.c_size_t(160))
             raise FsError(code, int(idx.value), msg.value.decode(errors="replace"))
+
+    def use_torch_allocator(self, on=True):
+        """fs_ctx_set_allocator with torch's caching allocator on the context's stream: the library's
+        scratch and objects then share torch's memory pool (SURVEY §8(b) conventions)."""
+        if not on:
+            self._check(lib().fs_ctx_set_allocator(self.h, None, None, None))
+            self._alloc_cbs = None
+            return
+        dev, st = self.device.index, self.stream
+
+        def _alloc(nbytes, user):
+            try:
+                return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st)
+            except Exception:
+                return None
+
+        def _free(ptr, user):
+            if ptr:
+                torch.cuda.caching_allocator_delete(ptr)
+        self._alloc_cbs = (_ALLOC_FN(_alloc), _FREE_FN(_free))     # kept alive with the context
+        self._check(lib().fs_ctx_set_allocator(self.h, C.cast(self._alloc_cbs[0], C.c_void_p),
+                                               C.cast(self._alloc_cbs[1], C.c_void_p), None))
 
     def set_timing(self, on=True):
         lib().fs_ctx_set_timing(self.h, C.c_int(1 if on else 0))

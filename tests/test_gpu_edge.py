@@ -169,3 +169,81 @@ def test_sweep_empty_grid_and_bad_config(F, ctx):
     with pytest.raises(F.FsError) as e:                        # RPM takes explicit limits only (R8)
         F.sweep(ctx, F.Trace(tr), gp, [dict(ENG, mode=3, act=dict(window_ms=10, limits_from_profile=1))])
     assert e.value.code == -1
+
+
+def _step_pair(F, ctx, tr, cfg):
+    op = O.profile(tr, dict(tier_max=255))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=255))
+    T = F.Trace(tr)
+    return O.Step(tr, op, cfg), F.WscState(ctx, T, gp, cfg), T
+
+
+def _step_err(fn):
+    try:
+        fn()
+    except (O.OracleError, F_ERR) as x:
+        return x.code, x.bad_index
+    return None
+
+
+F_ERR = RuntimeError
+
+
+@pytest.mark.parametrize("case", ["finished_range", "arrived_range", "finished_filtered"])
+def test_step_bad_ids_match_oracle(F, ctx, case):
+    """fs_wsc_step with a call id >= n_calls (finished or arrived) returns FS_E_RANGE with the
+    list position, and a finished call of a filtered user (tier > tier_max) FS_E_INVAL, as the
+    oracle's or_step; the state is then poisoned (FS_E_PROTOCOL) instead of running on
+    half-updated heaps."""
+    tr = G.generate("c1")
+    n = tr["n_calls"]
+    eng = dict(G.CONFIGS["c1"]["engine"], mode=1, tier_max=0,
+               act=dict(window_ms=60000, limits_from_profile=0, T_req_g=8, T_req_a=[5, 5]))
+    so, sg, T = _step_pair(F, ctx, tr, eng)
+    ab = int(np.nonzero((tr["meta"] >> 24) > 0)[0][0])         # a call of the abusive user
+    args = {"finished_range": dict(finished=[0, n + 7]),
+            "arrived_range": dict(arrived=[0, n], arrived_ns=[0, 0]),
+            "finished_filtered": dict(finished=[ab])}[case]
+    a = dict(finished=[], arrived=[], arrived_ns=[])
+    a.update(args)
+    eo = _step_err(lambda: so.step(0, 0, 0, **a))
+    try:
+        sg.step(0, 0, 0, **a)
+        eg = None
+    except F.FsError as x:
+        eg = (x.code, x.bad_index)
+    assert eo is not None and eg == eo, (eo, eg)
+    with pytest.raises(F.FsError) as ex:
+        sg.step(0, 0, 0, [], [0], [0])
+    assert ex.value.code == -9                                   # FS_E_PROTOCOL
+
+
+def test_replay_with_torch_allocator(F):
+    """fs_ctx_set_allocator: with torch's caching allocator installed, every scratch / object
+    allocation of a profile + FS(W+I) replay + ACT + sweep comes from torch's pool (its
+    allocated-bytes counter moves) and the results equal the oracle's."""
+    import torch
+    c = F.Context(0)
+    c.use_torch_allocator(True)
+    tr = G.generate("c1")
+    T = F.Trace(tr)
+    before = torch.cuda.memory_stats()["allocation.all.allocated"]
+    gp = F.build_app_profiles(c, T, dict(tier_max=255))
+    eng = dict(G.CONFIGS["c1"]["engine"], mode=1, tier_max=255,
+               act=dict(window_ms=60000, limits_from_profile=0, T_req_g=8, T_req_a=[5, 5]))
+    o, s = F.wsc_replay(c, T, gp, eng)
+    st, _ = F.act_throttle(c, T, gp, eng["act"], overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+    gs, gc = F.sweep(c, T, gp, [eng, dict(eng, tier_max=0)])
+    torch.cuda.synchronize()
+    after = torch.cuda.memory_stats()["allocation.all.allocated"]
+    assert after - before > 20                                   # the library's allocations went through torch
+    op = O.profile(tr, dict(tier_max=255))
+    eo, es = O.replay(tr, op, eng)
+    assert s["digest"] == es["digest"]
+    assert (st.cpu().numpy() == eo["status"]).all()
+    e2, ec = O.sweep(tr, op, [eng, dict(eng, tier_max=0)])
+    assert [x["digest"] for x in gs] == [x["digest"] for x in e2] and list(gc) == list(ec)
+    del gp
+    c.use_torch_allocator(False)
+    _, s2 = F.wsc_replay(c, T, F.build_app_profiles(c, T, dict(tier_max=255)), eng, outputs=False)
+    assert s2["digest"] == es["digest"]

@@ -90,6 +90,48 @@ def run_c5(n_sample=12):
     print("c5 sample written", path, out["oracle_seconds"], flush=True)
 
 
+def run_c5_full():
+    """C5: oracle summaries of EVERY scenario of the bench's 4096-scenario grid
+    (bench.sweep_scenarios, the list bench.py times), computed by P oracle replays in
+    parallel threads (ctypes releases the GIL; the oracle keeps no global state), for the
+    full-grid sweep parity test (tests/test_gpu_fullsize.py::test_sweep_c5_full)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import bench
+    c = G.CONFIGS["c5"]
+    tr = G.generate("c5")
+    cfg, eng, pcfg = bench.workload_cfg("c2")
+    p = O.profile(tr, pcfg)
+    scen = bench.sweep_scenarios(eng, 4096)
+    P = len(os.sched_getaffinity(0))
+    t0 = time.time()
+    res = [None] * len(scen)
+    done = [0]
+
+    def one(i):
+        s, cd = O.sweep(tr, p, [scen[i]])
+        res[i] = (s[0], int(cd[0]))
+        done[0] += 1
+        if done[0] % 256 == 0:
+            print(f"  {done[0]}/{len(scen)} scenarios, {time.time() - t0:.0f} s", flush=True)
+
+    # longest first (participating calls grow with tier_max) for a balanced pool
+    order = sorted(range(len(scen)), key=lambda i: -scen[i]["tier_max"])
+    with ThreadPoolExecutor(P) as ex:
+        list(ex.map(one, order))
+    keys = list(res[0][0].keys())
+    out = {"citation": "written by tools/make_goldens.py run_c5_full from oracle/ only (SURVEY.md §8(c) O4, "
+                       "§8(d) run matrix 'C5: every scenario's summary + digest'); inputs: tracegen config c5 and "
+                       "bench.sweep_scenarios(4096)",
+           "config": "c5", "n_calls": tr["n_calls"], "seed": c["seed"], "profile_cfg": pcfg,
+           "keys": keys, "codes": [r[1] for r in res],
+           "summaries": [[r[0][k] for k in keys] for r in res],
+           "oracle_threads": P, "oracle_seconds": time.time() - t0}
+    path = os.path.join(ROOT, "tests", "golden", "full_c5.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print("c5 full grid written", path, out["oracle_seconds"], flush=True)
+
+
 def run_c2_metrics():
     """§5 metrics (oracle/metrics.py) of the full C2 FS(W+I) replay of the bench's configuration,
     global and per app, at three delay thresholds."""
@@ -139,4 +181,4 @@ def run_c4():
 
 if __name__ == "__main__":
     for nm in sys.argv[1:] or ["c2"]:
-        {"c5": run_c5, "c4": run_c4, "c2m": run_c2_metrics}.get(nm, lambda: run(nm))()
+        {"c5": run_c5, "c5full": run_c5_full, "c4": run_c4, "c2m": run_c2_metrics}.get(nm, lambda: run(nm))()
