@@ -197,25 +197,40 @@ static void prof_limits(fs_profile_partial* pp) {
             P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g, P->T_tok_g);
 }
 
-static void prof_windows(fs_profile_partial* pp, const Order& o, const uint2* pk, u32* peak_r, u64* peak_t) {
+// K5: window peaks of the user order (profile.cuh), after round 0 fixed O-hat: parallel pieces
+// (k_win_pieces), then the segments whose windows outgrew a piece's ring, one warp each
+static void prof_windows(fs_profile_partial* pp) {
   fs_ctx* ctx = pp->ctx;
   Scratch& S = *pp->S;
-  const DTrace& t = pp->t;
-  u64 n = t.n;
-  if (!n) return;
-  u32* ts = S.alloc<u32>(n);
-  u64* ptau = S.alloc<u64>(n + 1);
-  u32* pc = S.alloc<u32>(n + 1);
-  const u32 nt = div_up(n, WS_TILE);
-  u64* lt = S.alloc<u64>(2 * (size_t)nt);
-  u32* lc = S.alloc<u32>(3 * (size_t)nt + 1);                // agg, inc, stat, ticket
+  fs_profile* P = pp->P;
+  const UserOrder& uo = pp->uo;
+  const u32 U = pp->t.U;
+  if (!uo.n || pp->cfg.window_ms == 0) return;
+  u32* flag = S.zeros<u32>(U + 1);
+  u32* cnt = S.zeros<u32>(2);
+  u32* list = S.alloc<u32>(U + 1);
   if (S.failed) return;
-  cudaMemsetAsync(lc + 2 * (size_t)nt, 0, ((size_t)nt + 1) * 4, ctx->stream);
-  int B = 256;
-  WinScanArgs g{n, o.perm, pk, ts, ptau, pc, lt, lt + nt, lc, lc + nt, lc + 2 * (size_t)nt, lc + 3 * (size_t)nt};
-  FS_LAUNCH(ctx, "win_scan", k_win_scan, nt, WS_T, 0, g);
-  WinPeakArgs w{n, o.key, o.seg, ts, ptau, pc, nullptr, (i64)pp->cfg.window_ms, peak_r, peak_t};
-  FS_LAUNCH(ctx, "win_peaks", k_win_peaks, div_up(n, B), B, 0, w);
+  const TauW w = tau_w(pp->cfg.tau_w_in, pp->cfg.tau_w_sys, pp->cfg.tau_w_out);
+  SegWinArgs a{uo.it, uo.seg, U, P->A, P->J, w.wo, (i64)pp->cfg.window_ms, P->ohat, nullptr, nullptr, nullptr,
+               P->peak_r_u, P->peak_t_u, P->peak_r_ua, P->peak_t_ua, cnt + 1, list, 0, flag};
+  size_t smem = win_pieces_smem(P->A);
+  cudaFuncSetAttribute(k_win_pieces, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const u64 nch = (uo.n + WP_CH - 1) / WP_CH;
+  const int per_sm = std::max(1, (int)(ctx->smem_optin ? (ctx->smem_optin + 1024) / (smem + 1024) : 4));
+  const int grid = (int)std::max<u64>(1, std::min<u64>((u64)ctx->sm_count * std::min(per_sm, 8), div_up(nch, WP_T / 32)));
+  FS_LAUNCH(ctx, "win_pieces", k_win_pieces, grid, WP_T, smem, a, uo.n);
+  FS_LAUNCH(ctx, "win_flags", k_win_flags, div_up(U, 256), 256, 0, flag, U, list, cnt);
+  u32 nover = 0;
+  cudaMemcpyAsync(&nover, cnt, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  pp->n_win_overflow = nover;
+  if (!nover) return;
+  a.pt = S.alloc<u64>(uo.n); a.ca = S.alloc<u32>(uo.n); a.pta = S.alloc<u64>(uo.n);
+  if (S.failed) return;
+  a.n_users = nover;
+  smem = seg_win_smem(P->A);
+  cudaFuncSetAttribute(k_useg_win, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  FS_LAUNCH(ctx, "useg_win", k_useg_win, div_up(nover, SW_T / 32), SW_T, smem, a);
 }
 
 __global__ void k_pack_u32_u64(const u32* a, u64* b, u64 n) {
@@ -263,8 +278,12 @@ extern "C" int fs_profile_local(fs_ctx* ctx, const fs_trace* tr, const fs_profil
   pp->qwords = S.zeros<u64>(1);
   if (S.failed) { fs_profile_free(pp->P); delete pp; return FS_E_NOMEM; }
   prof_stream(ctx, pp->t, J, cfg->tier_max, pp->l_cnt, pp->l_in, pp->l_sys, pp->l_out, pp->l_hist);
-  build_order(ctx, S, pp->t, false, &pp->ou);
-  build_order(ctx, S, pp->t, true, &pp->oua);
+  {
+    const TauW w = tau_w(cfg->tau_w_in, cfg->tau_w_sys, cfg->tau_w_out);
+    if (!build_user_order(ctx, S, pp->t, cfg->tier_max, cfg->count_mode == FS_COUNT_HEADS_ONLY, w.wi, w.ws, &pp->uo)) {
+      fs_profile_free(pp->P); pp->P = nullptr; delete pp; return FS_E_NOMEM;
+    }
+  }
   rc = finish(ctx, &S);
   if (rc) { fs_profile_free(pp->P); delete pp; return rc; }
   size_t r0 = prof_r0_words(A, J);
@@ -325,14 +344,7 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
     cudaMemsetAsync(P->peak_t_u, 0, U * 8, ctx->stream);
     cudaMemsetAsync(P->peak_r_ua, 0, (u64)U * A * 4, ctx->stream);
     cudaMemsetAsync(P->peak_t_ua, 0, (u64)U * A * 8, ctx->stream);
-    uint2* wpk = pp->S->alloc<uint2>(pp->t.n + 1);
-    if (pp->t.n && wpk) {
-      WinPackArgs wp{pp->t, J, pp->cfg.tier_max, pp->cfg.count_mode, P->ohat, wpk,
-                     tau_w(pp->cfg.tau_w_in, pp->cfg.tau_w_sys, pp->cfg.tau_w_out)};
-      FS_LAUNCH(ctx, "win_pack", k_win_pack, div_up(pp->t.n, B), B, 0, wp);
-    }
-    prof_windows(pp, pp->ou, wpk, P->peak_r_u, P->peak_t_u);
-    prof_windows(pp, pp->oua, wpk, P->peak_r_ua, P->peak_t_ua);
+    prof_windows(pp);
     u64 w = prof_q_next(pp, buf);
     u64* pk = buf + w;
     if (U) {

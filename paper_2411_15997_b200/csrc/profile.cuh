@@ -4,7 +4,7 @@
 // per-app "normal range"; limits "based on the analysis of
 // historical data".  Readings Q8, Q9, Q23, Q30.
 #pragma once
-#include "index.cuh"
+#include "usort.cuh"
 
 static const int NBINS = 240, NF = 5;
 static const int QMAX = 16;              // max reported quantiles
@@ -205,171 +205,366 @@ __global__ void k_prof_finish(u32 A, u32 J, const u64* cnt, const u64* s_out, u6
 }
 
 // ------------------------------------------------------------------ K5 window peaks
-// Gather the order's times and token loads, exclusive-scan counts and loads, then
-// per position the half-open window (t - W, t] by galloping search (Q4); peaks per
-// segment by a warp segmented max over the sorted keys + one atomicMax per run.
-// One coalesced pass packs what the window scans need per call: {t_ms, tau | counted << 31}
-// (tau = L_I + L_S + O-hat(a, j') < 2^26); each order then gathers 8 B per call through its
-// permutation instead of four scattered 4-B fields.
-struct WinPackArgs {
-  DTrace t; u32 J, tier_max, heads_only;
-  const u64* ohat;                 // [A][J1]
-  uint2* pk;                       // per call
-  TauW w;                          // token load weights (R11)
+// Oracle step 4 ("based on the analysis of historical data"; Q4 half-open window):
+// per counted call p of user u, n_g(p) / tau_g(p) = calls / token load of u's counted calls x
+// with t_p - W < t_x and x at or before p in (t, id) order; n_a / tau_a the same over u's calls
+// of p's app; peaks = max over p.  Input: the (user, t, id)-ordered counted calls with their
+// payload (usort.cuh), so every position is streamed once, coalesced.
+//
+// One warp per user segment, 32 positions per step:
+//   * tau = base + w_out O-hat(a, j') (O-hat from the global sums: round 1 of the protocol);
+//   * segment prefix of tau (warp scan + carry), and per app the rank and tau prefix (one
+//     __match_any_sync group per app present in the step; a per-warp shared table per app
+//     carries them across steps);
+//   * the window start lb by a 5-step binary search over the step's lanes (times are sorted),
+//     continued backwards through the segment only when the window reaches past the step;
+//     the app window starts at the first call of p's app at or after lb;
+//   * positions older than the step are read back from per-position prefix arrays that are
+//     written only for calls whose successor in the segment lies inside the window (no later
+//     window can start at any other call);
+//   * user peaks in registers, (user, app) peaks in the per-warp table, written out when the
+//     segment ends (dense [U] and [U][A] tables, zeroed beforehand).
+struct SegWinArgs {
+  const uint4* it; const u64* seg; u32 U, A, J, wo; i64 W;
+  const u64* ohat;                       // [A][J + 1]
+  u64* pt; u32* ca; u64* pta;            // per position: segment tau prefix, app rank, app tau prefix
+  u32* peak_r_u; u64* peak_t_u; u32* peak_r_ua; u64* peak_t_ua;
+  u32* next;                             // user queue
+  const u32* users; u32 n_users;         // the segments to process (the overflow list of k_win_pieces)
+  u32* flag;                             // [U] k_win_pieces: segments whose windows outgrew the ring
 };
-__global__ void k_win_pack(WinPackArgs a) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= a.t.n) return;
-  u32 m = __ldg(&a.t.meta[i]);
-  bool c = m_tier(m) <= a.tier_max && (!a.heads_only || m_stage(m) == 1);
-  u32 v = 0;
-  if (c) v = 0x80000000u | (a.w.wi * __ldg(&a.t.len_in[i]) + a.w.ws * __ldg(&a.t.len_sys[i]) +
-                            a.w.wo * (u32)a.ohat[(u64)m_app(m) * (a.J + 1) + min(m_stage(m), a.J)]);
-  a.pk[i] = make_uint2(__ldg(&a.t.t_ms[i]), v);
+static const int SW_T = 128;
+__device__ __forceinline__ u64 warp_incl_scan_u64(u64 x, u32 lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(FULL_MASK, x, o); if (lane >= (u32)o) x += y; }
+  return x;
 }
-
-// gather + both window prefix sums in one pass (single-pass scan, decoupled look-back): per
-// position p of the order, ts[p] = t of call perm[p], ptau[p] = sum of tau over positions < p,
-// pc[p] = number of counted positions < p (ptau[n], pc[n] = totals).  No per-position tau / flag
-// arrays: the scan consumes the gathered values from shared memory.
-static const int WS_T = 256, WS_IPT = 16, WS_TILE = WS_T * WS_IPT;
-struct WinScanArgs {
-  u64 n; const u32* perm; const uint2* pk;
-  u32* ts; u64* ptau; u32* pc;
-  u64* agg_t; u64* inc_t; u32* agg_c; u32* inc_c; u32* stat; u32* ticket;   // per tile (stat zeroed)
-};
-__global__ void __launch_bounds__(WS_T) k_win_scan(WinScanArgs a) {
-  __shared__ uint2 tile[WS_TILE + WS_TILE / 16];
-  __shared__ u64 sht[32];
-  __shared__ u32 shc[32];
-  __shared__ u32 s_tile;
-  __shared__ u64 s_pt;
-  __shared__ u32 s_pc;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);   // tiles start in ticket order
-  __syncthreads();
-  const u32 tid = s_tile;
-  const u64 base = (u64)tid * WS_TILE;
-#pragma unroll
-  for (int r = 0; r < WS_IPT; r++) {                         // striped: coalesced perm and ts
-    u32 k = r * WS_T + threadIdx.x;
-    u64 i = base + k;
-    uint2 v = make_uint2(0, 0);
-    if (i < a.n) { v = a.pk[__ldg(&a.perm[i])]; a.ts[i] = v.x; }
-    tile[scan_pad(k)] = make_uint2(v.y & 0x7FFFFFFFu, v.y >> 31);
-  }
-  __syncthreads();
-  u32 tv[WS_IPT], cv[WS_IPT];
-  u64 st = 0; u32 sc = 0;
-#pragma unroll
-  for (int r = 0; r < WS_IPT; r++) {
-    uint2 e = tile[scan_pad(threadIdx.x * WS_IPT + r)];
-    tv[r] = e.x; cv[r] = e.y; st += e.x; sc += e.y;
-  }
-  u64 tot_t; u32 tot_c;
-  u64 ex_t = block_excl_scan<u64>(st, sht, &tot_t);
-  u32 ex_c = block_excl_scan<u32>(sc, shc, &tot_c);
-  if (threadIdx.x < 32) {                                    // warp 0: look back 32 tiles at a time
-    const int lane = threadIdx.x;
-    u64 pt = 0; u32 pcn = 0;
-    if (tid > 0) {
-      if (lane == 0) {
-        a.agg_t[tid] = tot_t; a.agg_c[tid] = tot_c;
-        __threadfence();
-        atomicExch(&a.stat[tid], 1u);
-      }
-      for (long long j0 = (long long)tid - 1;; j0 -= 32) {
-        const long long j = j0 - lane;                         // lane 0 = nearest predecessor
-        u32 f = 2;
-        if (j >= 0) while ((f = *(volatile u32*)&a.stat[j]) == 0) {}
-        __threadfence();
-        const u32 incm = __ballot_sync(FULL_MASK, f == 2);   // j < 0 counts as an inclusive 0
-        const int L = incm ? __ffs(incm) - 1 : 32;
-        u64 vt = 0; u32 vc = 0;
-        if (j >= 0 && lane < L) { vt = *(volatile u64*)&a.agg_t[j]; vc = *(volatile u32*)&a.agg_c[j]; }
-        else if (j >= 0 && lane == L) { vt = *(volatile u64*)&a.inc_t[j]; vc = *(volatile u32*)&a.inc_c[j]; }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) { vt += __shfl_xor_sync(FULL_MASK, vt, o); vc += __shfl_xor_sync(FULL_MASK, vc, o); }
-        pt += vt; pcn += vc;
-        if (incm) break;
-      }
-    }
-    if (lane == 0) {
-      a.inc_t[tid] = pt + tot_t; a.inc_c[tid] = pcn + tot_c;
-      __threadfence();
-      atomicExch(&a.stat[tid], 2u);
-      s_pt = pt; s_pc = pcn;
-      if (base + WS_TILE >= a.n) { a.ptau[a.n] = pt + tot_t; a.pc[a.n] = pcn + tot_c; }   // last tile
-    }
-  }
-  __syncthreads();
-  u64 rt = s_pt + ex_t;
-  u32 rc = s_pc + ex_c;
-  u64* t64 = (u64*)tile;                                       // 8 B per element: same padded slots
-#pragma unroll
-  for (int r = 0; r < WS_IPT; r++) { t64[scan_pad(threadIdx.x * WS_IPT + r)] = rt; rt += tv[r]; }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < WS_IPT; r++) {
-    u32 k = r * WS_T + threadIdx.x;
-    u64 i = base + k;
-    if (i < a.n) a.ptau[i] = t64[scan_pad(k)];
-  }
-  __syncthreads();
-  u32* t32 = (u32*)tile;
-#pragma unroll
-  for (int r = 0; r < WS_IPT; r++) { t32[scan_pad(threadIdx.x * WS_IPT + r)] = rc; rc += cv[r]; }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < WS_IPT; r++) {
-    u32 k = r * WS_T + threadIdx.x;
-    u64 i = base + k;
-    if (i < a.n) a.pc[i] = t32[scan_pad(k)];
-  }
-}
-
 __device__ __forceinline__ void atomic_max_u64(u64* p, u64 v) { atomicMax((unsigned long long*)p, (unsigned long long)v); }
-
-struct WinPeakArgs {
-  u64 n; const u32* key; const u64* seg; const u32* ts; const u64* ptau; const u32* pc; const u32* flag;
-  i64 W;
-  u32* peak_r; u64* peak_t;       // indexed by key
-};
-__global__ void k_win_peaks(WinPeakArgs a) {
-  u64 p = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  bool ok = p < a.n;
-  u32 k = ok ? a.key[p] : NONE32;
-  u32 nr = 0; u64 nt = 0;
-  if (ok && (a.flag ? a.flag[p] != 0 : a.pc[p + 1] != a.pc[p])) {
-    u64 s = a.seg[k];
-    u64 lb = window_lb<u32>(a.ts, s, p, (i64)a.ts[p] - a.W);
-    nr = a.pc[p + 1] - a.pc[lb];
-    nt = a.ptau[p + 1] - a.ptau[lb];
-  }
-  int lane = threadIdx.x & 31;
-  // most warps lie inside one segment (one key): plain warp max, one lane's atomics
-  if (__reduce_min_sync(FULL_MASK, k) == __reduce_max_sync(FULL_MASK, k)) {
-    if (k == NONE32) return;
-    const u32 mr = __reduce_max_sync(FULL_MASK, nr);
-    const u32 hi = __reduce_max_sync(FULL_MASK, (u32)(nt >> 32));
-    const u32 lo = __reduce_max_sync(FULL_MASK, (u32)(nt >> 32) == hi ? (u32)nt : 0u);
-    const u64 mt = (u64)hi << 32 | lo;
-    if (lane == 0 && (mr || mt)) { atomicMax(&a.peak_r[k], mr); atomic_max_u64(&a.peak_t[k], mt); }
-    return;
-  }
-  // else a warp segmented max over runs of equal keys (positions are sorted by key)
+__device__ __forceinline__ u64 reduce_max_u64(u32 mask, u64 v) {
+  const u32 hi = __reduce_max_sync(mask, (u32)(v >> 32));
+  const u32 lo = __reduce_max_sync(mask, (u32)(v >> 32) == hi ? (u32)v : 0u);
+  return (u64)hi << 32 | lo;
+}
+__host__ __device__ __forceinline__ size_t sw_stride(u32 A) { return ((size_t)A * 24 + ((A + 31) / 32) * 4 + 16 + 15) / 16 * 16; }
+__global__ void __launch_bounds__(SW_T) k_useg_win(const __grid_constant__ SegWinArgs a) {
+  extern __shared__ __align__(16) unsigned char smw[];
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, A = a.A, J1 = a.J + 1;
+  const u32 nwords = (A + 31) / 32;
+  unsigned char* mine = smw + (size_t)wid * sw_stride(A);
+  u64* tab_t = (u64*)mine;                     // app tau total so far
+  u64* tab_pt = tab_t + A;                     // app token peak
+  u32* tab_c = (u32*)(tab_pt + A);             // app calls so far
+  u32* tab_pr = tab_c + A;                     // app request peak
+  u32* touched = tab_pr + A;                   // apps seen in this segment
+  for (u32 k = lane; k < A; k += 32) { tab_t[k] = 0; tab_pt[k] = 0; tab_c[k] = 0; tab_pr[k] = 0; }
+  for (u32 k = lane; k < nwords; k += 32) touched[k] = 0;
+  __syncwarp();
+  const u32 lt = lanemask_lt();
+  for (;;) {
+    u32 qi = 0;
+    if (lane == 0) qi = atomicAdd(a.next, 1u);
+    qi = __shfl_sync(FULL_MASK, qi, 0);
+    if (qi >= a.n_users) break;
+    const u32 u = a.users[qi];
+    const u64 s = a.seg[u], e = a.seg[u + 1];
+    if (s == e) continue;
+    u64 carry = 0, mt = 0;
+    u32 mr = 0;
+    for (u64 c0 = s; c0 < e; c0 += 32) {
+      const u64 p = c0 + lane;
+      const bool ok = p < e;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (ok) v = a.it[p];
+      const u32 app = ok ? (v.w & 255u) : 256u + lane, jj = min((v.w >> 8) & 255u, a.J);
+      const u64 tau = ok ? (u64)v.y + (u64)a.wo * __ldg(&a.ohat[(u64)app * J1 + jj]) : 0;
+      const i64 t = v.x;
+      // segment prefix of tau
+      const u64 inc = warp_incl_scan_u64(tau, lane);
+      const u64 ex = carry + inc - tau;
+      carry += __shfl_sync(FULL_MASK, inc, 31);
+      // per-app groups: rank and tau prefix inside the step
+      const u32 vm = __ballot_sync(FULL_MASK, ok);
+      const u32 peers = __match_any_sync(FULL_MASK, app);
+      u64 exa;
+      if (__all_sync(FULL_MASK, !ok || peers == vm)) exa = inc - tau;   // one app in the step
+      else {
+        exa = 0;
+        u32 todo = vm;
+        while (todo) {
+          const u32 g = __shfl_sync(FULL_MASK, peers, __ffs(todo) - 1);
+          const u64 x = warp_incl_scan_u64(((g >> lane) & 1u) ? tau : 0, lane);
+          if ((g >> lane) & 1u) exa = x - tau;
+          todo &= ~g;
+        }
+      }
+      const u32 rank = __popc(peers & lt);
+      u32 bc = 0; u64 bt = 0;
+      if (ok) { bc = tab_c[app]; bt = tab_t[app]; }
+      const u32 cav = bc + rank + 1;           // app rank from 1 in the segment
+      const u64 ptav = bt + exa;               // app tau before p in the segment
+      // the step's successor time (lane 31 looks one position ahead)
+      u32 tnext = __shfl_down_sync(FULL_MASK, v.x, 1);
+      bool has_next = p + 1 < e;
+      if (lane == 31 && has_next) tnext = a.it[p + 1].x;
+      if (ok && has_next && (i64)tnext - a.W < t) { a.pt[p] = ex; a.ca[p] = cav; a.pta[p] = ptav; }
+      const u32 last = 31 - __clz(peers);
+      const u64 gtot = __shfl_sync(FULL_MASK, exa + tau, last);
+      __syncwarp();
+      if (ok && lane == (u32)(__ffs(peers) - 1)) {
+        tab_c[app] = bc + __popc(peers); tab_t[app] = bt + gtot;
+        atomicOr(&touched[app >> 5], 1u << (app & 31));
+      }
+      // window start: the first lane q <= lane with t_q > t - W (binary search over the step)
+      const i64 thr = t - a.W;
+      u32 lo = 0, hi = lane;                   // answer in [lo, hi]; t_lane > thr
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    u32 ko = __shfl_up_sync(FULL_MASK, k, o);
-    u32 ro = __shfl_up_sync(FULL_MASK, nr, o);
-    u64 to = __shfl_up_sync(FULL_MASK, nt, o);
-    if (lane >= o && ko == k) { nr = max(nr, ro); nt = max(nt, to); }
+      for (int k = 0; k < 5; k++) {
+        const u32 mid = (lo + hi) >> 1;
+        const i64 tm = (i64)__shfl_sync(FULL_MASK, v.x, mid);
+        if (lo < hi) { if (tm > thr) hi = mid; else lo = mid + 1; }
+      }
+      u64 lb = c0 + lo;
+      bool far = false;
+      if (ok && lo == 0 && c0 > s && (i64)a.it[c0 - 1].x > thr) {      // the window reaches past the step
+        far = true;
+        u64 k = 1, good = c0 - 1, hi2 = c0 - 1;                        // galloping back from c0 - 1
+        lb = s;
+        for (;;) {
+          if (hi2 < s + k) { u64 l2 = s, h2 = good; while (l2 < h2) { u64 m = (l2 + h2) >> 1; if ((i64)a.it[m].x > thr) h2 = m; else l2 = m + 1; } lb = l2; break; }
+          u64 q = hi2 - k;
+          if ((i64)a.it[q].x > thr) { good = q; k <<= 1; continue; }
+          u64 l2 = q + 1, h2 = good;
+          while (l2 < h2) { u64 m = (l2 + h2) >> 1; if ((i64)a.it[m].x > thr) h2 = m; else l2 = m + 1; }
+          lb = l2;
+          break;
+        }
+      }
+      // user window
+      const u32 ln = far ? 0 : (u32)(lb - c0);
+      const u64 ex_lb = __shfl_sync(FULL_MASK, ex, ln);
+      const u64 pt_lb = far ? a.pt[lb] : ex_lb;
+      const u32 n_g = (u32)(p - lb + 1);
+      const u64 tau_g = ex + tau - pt_lb;
+      // app window: from the first call of p's app at or after lb
+      u32 n_a; u64 tau_a;
+      u32 qlane = __ffs(peers & ~((1u << ln) - 1u)) - 1;                 // in the step (or the first peer)
+      bool qfar = false; u64 q = lb;
+      if (far) {
+        while (q < c0 && (a.it[q].w & 255u) != app) q++;
+        qfar = q < c0;
+        if (!qfar) qlane = __ffs(peers) - 1;
+      }
+      const u32 ca_q = __shfl_sync(FULL_MASK, cav, qlane);
+      const u64 pta_q = __shfl_sync(FULL_MASK, ptav, qlane);
+      if (qfar) { n_a = cav - a.ca[q] + 1; tau_a = ptav + tau - a.pta[q]; }
+      else { n_a = cav - ca_q + 1; tau_a = ptav + tau - pta_q; }
+      if (ok) { mr = max(mr, n_g); mt = max(mt, tau_g); }
+      // (user, app) peaks: group max, the group leader keeps it
+      if (ok) {
+        const u32 gr = __reduce_max_sync(peers, n_a);
+        const u64 gt = reduce_max_u64(peers, tau_a);
+        if (lane == (u32)(__ffs(peers) - 1)) { tab_pr[app] = max(tab_pr[app], gr); tab_pt[app] = max(tab_pt[app], gt); }
+      }
+      __syncwarp();
+    }
+    mr = __reduce_max_sync(FULL_MASK, mr);
+    mt = reduce_max_u64(FULL_MASK, mt);
+    if (lane == 0) { a.peak_r_u[u] = mr; a.peak_t_u[u] = mt; }
+    __syncwarp();
+    for (u32 k = lane; k < A; k += 32) {
+      if (!((touched[k >> 5] >> (k & 31)) & 1u)) continue;
+      a.peak_r_ua[(u64)u * A + k] = tab_pr[k]; a.peak_t_ua[(u64)u * A + k] = tab_pt[k];
+      tab_t[k] = 0; tab_pt[k] = 0; tab_c[k] = 0; tab_pr[k] = 0;
+    }
+    __syncwarp();
+    for (u32 k = lane; k < nwords; k += 32) touched[k] = 0;
+    __syncwarp();
   }
-  u32 kn = __shfl_down_sync(FULL_MASK, k, 1);
-  bool last = lane == 31 || kn != k;
-  if (ok && last && (nr || nt)) {
-    atomicMax(&a.peak_r[k], nr);
-    atomic_max_u64(&a.peak_t[k], nt);
+}
+static size_t seg_win_smem(u32 A) { return (size_t)(SW_T / 32) * sw_stride(A); }
+
+// The window peaks in parallel pieces: the sorted positions are cut into chunks of WP_CH, every
+// chunk into pieces at segment boundaries; one warp per chunk walks its pieces.  A piece
+// [ps, pe) of segment [s, e) starts its walk at h = lb(ps), the window start of its first call
+// (no window of the piece reaches further back), so every prefix is relative to h and no carry
+// from the previous piece is needed; positions in [h, ps) (the halo) only feed the prefixes.
+// The last WP_R positions' prefixes live in a per-warp shared ring; a window that reaches past
+// the ring flags its segment, which k_useg_win then redoes alone (plain stores overwrite).
+// Peaks combine across pieces with atomicMax (tables zeroed beforehand).
+static const int WP_T = 128, WP_CH = 2048, WP_R = 512;
+__host__ __device__ __forceinline__ size_t wp_stride(u32 A) {
+  return ((size_t)A * 24 + ((A + 31) / 32) * 4 + (size_t)WP_R * 21 + 15) / 16 * 16;
+}
+static size_t win_pieces_smem(u32 A) { return (size_t)(WP_T / 32) * wp_stride(A); }
+__global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ SegWinArgs a, u64 n) {
+  extern __shared__ __align__(16) unsigned char smw[];
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, A = a.A, J1 = a.J + 1;
+  const u32 nwords = (A + 31) / 32;
+  unsigned char* mine = smw + (size_t)wid * wp_stride(A);
+  u64* r_pt = (u64*)mine;                      // ring: segment tau prefix
+  u64* r_pta = r_pt + WP_R;                    //       app tau prefix
+  u64* tab_t = r_pta + WP_R;                   // app tau since h
+  u64* tab_pt = tab_t + A;                     // app token peak
+  u32* r_ca = (u32*)(tab_pt + A);              // ring: app rank
+  u32* tab_c = r_ca + WP_R;                    // app calls since h
+  u32* tab_pr = tab_c + A;                     // app request peak
+  u32* touched = tab_pr + A;
+  unsigned char* r_app = (unsigned char*)(touched + nwords);   // ring: app
+  for (u32 k = lane; k < A; k += 32) { tab_t[k] = 0; tab_pt[k] = 0; tab_c[k] = 0; tab_pr[k] = 0; }
+  for (u32 k = lane; k < nwords; k += 32) touched[k] = 0;
+  __syncwarp();
+  const u32 lt = lanemask_lt();
+  const u64 nch = (n + WP_CH - 1) / WP_CH;
+  for (u64 ch = (u64)blockIdx.x * (WP_T / 32) + wid; ch < nch; ch += (u64)gridDim.x * (WP_T / 32)) {
+    const u64 c_end = min(n, (ch + 1) * WP_CH);
+    u64 ps = ch * WP_CH;
+    while (ps < c_end) {
+      const u32 u = a.it[ps].z;
+      const u64 s = a.seg[u], e = a.seg[u + 1];
+      const u64 pe = min(e, c_end);
+      // h = lb(ps): first position in [s, ps] with t > t_ps - W
+      const i64 thr0 = (i64)a.it[ps].x - a.W;
+      u64 h;
+      {
+        u64 lo = s, hi = ps;
+        if (ps > s && (i64)a.it[ps - 1].x > thr0) {        // galloping back, then binary search
+          u64 k = 2, good = ps - 1;
+          lo = s;
+          for (;;) {
+            if (ps < s + k) break;
+            const u64 q = ps - k;
+            if ((i64)a.it[q].x > thr0) { good = q; k <<= 1; continue; }
+            lo = q + 1;
+            break;
+          }
+          hi = good;
+        } else lo = hi = ps;
+        while (lo < hi) { const u64 m = (lo + hi) >> 1; if ((i64)a.it[m].x > thr0) hi = m; else lo = m + 1; }
+        h = lo;
+      }
+      u64 carry = 0, mt = 0;
+      u32 mr = 0;
+      bool over = false;
+      for (u64 c0 = h; c0 < pe; c0 += 32) {
+        const u64 p = c0 + lane;
+        const bool ok = p < pe, real = ok && p >= ps;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ok) v = a.it[p];
+        const u32 app = ok ? (v.w & 255u) : 256u + lane, jj = min((v.w >> 8) & 255u, a.J);
+        const u64 tau = ok ? (u64)v.y + (u64)a.wo * __ldg(&a.ohat[(u64)app * J1 + jj]) : 0;
+        const i64 t = v.x;
+        const u64 inc = warp_incl_scan_u64(tau, lane);
+        const u64 ex = carry + inc - tau;
+        carry += __shfl_sync(FULL_MASK, inc, 31);
+        const u32 vm = __ballot_sync(FULL_MASK, ok);
+        const u32 peers = __match_any_sync(FULL_MASK, app);
+        u64 exa;
+        if (__all_sync(FULL_MASK, !ok || peers == vm)) exa = inc - tau;
+        else {
+          exa = 0;
+          u32 todo = vm;
+          while (todo) {
+            const u32 g = __shfl_sync(FULL_MASK, peers, __ffs(todo) - 1);
+            const u64 x = warp_incl_scan_u64(((g >> lane) & 1u) ? tau : 0, lane);
+            if ((g >> lane) & 1u) exa = x - tau;
+            todo &= ~g;
+          }
+        }
+        const u32 rank = __popc(peers & lt);
+        u32 bc = 0; u64 bt = 0;
+        if (ok) { bc = tab_c[app]; bt = tab_t[app]; }
+        const u32 cav = bc + rank + 1;
+        const u64 ptav = bt + exa;
+        const u32 last = 31 - __clz(peers);
+        const u64 gtot = __shfl_sync(FULL_MASK, exa + tau, last);
+        __syncwarp();
+        if (ok) {
+          const u32 slot = (u32)(p & (WP_R - 1));
+          r_pt[slot] = ex; r_pta[slot] = ptav; r_ca[slot] = cav; r_app[slot] = (unsigned char)app;
+        }
+        if (ok && lane == (u32)(__ffs(peers) - 1)) {
+          tab_c[app] = bc + __popc(peers); tab_t[app] = bt + gtot;
+          if (p >= ps || c0 + last >= ps) atomicOr(&touched[app >> 5], 1u << (app & 31));
+        }
+        __syncwarp();
+        if (!__any_sync(FULL_MASK, real)) continue;            // a halo step: prefixes only
+        const i64 thr = t - a.W;
+        u32 lo = 0, hi = lane;
+#pragma unroll
+        for (int k = 0; k < 5; k++) {
+          const u32 mid = (lo + hi) >> 1;
+          const i64 tm = (i64)__shfl_sync(FULL_MASK, v.x, mid);
+          if (lo < hi) { if (tm > thr) hi = mid; else lo = mid + 1; }
+        }
+        u64 lb = c0 + lo;
+        bool far = false;
+        if (real && lo == 0 && c0 > h && (i64)a.it[c0 - 1].x > thr) {
+          far = true;
+          u64 k = 1, good = c0 - 1, l2 = h;
+          for (;;) {
+            if (c0 - 1 < h + k) break;
+            const u64 q = c0 - 1 - k;
+            if ((i64)a.it[q].x > thr) { good = q; k <<= 1; continue; }
+            l2 = q + 1;
+            break;
+          }
+          u64 h2 = good;
+          while (l2 < h2) { const u64 m = (l2 + h2) >> 1; if ((i64)a.it[m].x > thr) h2 = m; else l2 = m + 1; }
+          lb = l2;
+        }
+        const u64 ring_lo = c0 + 32 > (u64)WP_R ? c0 + 32 - WP_R : 0;   // oldest position still in the ring
+        const bool miss = far && lb < ring_lo;
+        if (__any_sync(FULL_MASK, miss)) { over = true; break; }
+        const u32 ln = far ? 0 : (u32)(lb - c0);
+        const u64 ex_lb = __shfl_sync(FULL_MASK, ex, ln);
+        const u64 pt_lb = far ? r_pt[lb & (WP_R - 1)] : ex_lb;
+        const u32 n_g = (u32)(p - lb + 1);
+        const u64 tau_g = ex + tau - pt_lb;
+        u32 qlane = __ffs(peers & ~((1u << ln) - 1u)) - 1;
+        bool qfar = false; u64 q = lb;
+        if (far) {
+          while (q < c0 && r_app[q & (WP_R - 1)] != app) q++;
+          qfar = q < c0;
+          if (!qfar) qlane = __ffs(peers) - 1;
+        }
+        const u32 ca_q = __shfl_sync(FULL_MASK, cav, qlane);
+        const u64 pta_q = __shfl_sync(FULL_MASK, ptav, qlane);
+        u32 n_a; u64 tau_a;
+        if (qfar) { n_a = cav - r_ca[q & (WP_R - 1)] + 1; tau_a = ptav + tau - r_pta[q & (WP_R - 1)]; }
+        else { n_a = cav - ca_q + 1; tau_a = ptav + tau - pta_q; }
+        if (real) { mr = max(mr, n_g); mt = max(mt, tau_g); }
+        const u32 rm = peers & __ballot_sync(FULL_MASK, real);
+        if (real) {
+          const u32 gr = __reduce_max_sync(rm, n_a);
+          const u64 gt = reduce_max_u64(rm, tau_a);
+          if (lane == (u32)(__ffs(rm) - 1)) { tab_pr[app] = max(tab_pr[app], gr); tab_pt[app] = max(tab_pt[app], gt); }
+        }
+        __syncwarp();
+      }
+      if (over) {
+        if (lane == 0) a.flag[u] = 1;
+      } else {
+        mr = __reduce_max_sync(FULL_MASK, mr);
+        mt = reduce_max_u64(FULL_MASK, mt);
+        if (lane == 0) { atomicMax(&a.peak_r_u[u], mr); atomic_max_u64(&a.peak_t_u[u], mt); }
+      }
+      __syncwarp();
+      for (u32 k = lane; k < A; k += 32) {
+        if (!over && ((touched[k >> 5] >> (k & 31)) & 1u)) {
+          atomicMax(&a.peak_r_ua[(u64)u * A + k], tab_pr[k]); atomic_max_u64(&a.peak_t_ua[(u64)u * A + k], tab_pt[k]);
+        }
+        tab_t[k] = 0; tab_pt[k] = 0; tab_c[k] = 0; tab_pr[k] = 0;
+      }
+      __syncwarp();
+      for (u32 k = lane; k < nwords; k += 32) touched[k] = 0;
+      __syncwarp();
+      ps = pe;
+    }
   }
+}
+__global__ void k_win_flags(const u32* flag, u32 U, u32* list, u32* n) {
+  u32 u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u < U && flag[u]) list[atomicAdd(n, 1u)] = u;
 }
 
 // ------------------------------------------------------------------ K6 exact quantiles
@@ -658,7 +853,8 @@ struct fs_profile_partial {
   u32* d_qppm = nullptr;
   // local partials
   u64 *l_cnt, *l_in, *l_sys, *l_out, *l_hist;
-  Order ou, oua;
+  UserOrder uo;                  // counted calls in (user, t, id) order (round 0)
+  u32 n_win_overflow = 0;        // segments the window pieces handed to k_useg_win
   // quantiles
   QState* qst = nullptr; QIv* qiv = nullptr; u32* qniv = nullptr; u64* qwords = nullptr;
   u64 h2_words = 0;

@@ -152,6 +152,28 @@ def test_profile_tile_boundaries(F, ctx, n):
     _cmp_profile(gpr, O.profile(tr, cfg), 5)
 
 
+@pytest.mark.parametrize("case", ["dense", "dense_heads_tau", "users_2pass", "users_3pass"])
+def test_profile_user_order(F, ctx, case):
+    """The onesweep user order + segmented window kernel: dense users whose 60-s windows hold
+    hundreds of calls (windows reaching back past a 32-position step, several apps per user),
+    weighted token loads under heads-only counting, and user counts that need two (17 bits) and
+    three (19 bits) radix passes."""
+    if case.startswith("dense"):
+        tr = G.generate(dict(G.CONFIGS["c3"], n_users=40, n_calls=100_000, duration_ms=3_600_000, seed=44))
+        cfg = dict(tier_max=255) if case == "dense" else \
+            dict(tier_max=7, count_mode=1, tau_w_in=2, tau_w_sys=0, tau_w_out=5, window_ms=90_000)
+    elif case == "users_2pass":
+        tr, cfg = G.generate(dict(G.CONFIGS["c2"], n_users=70_000, n_calls=200_000, seed=42)), dict(tier_max=255)
+    else:
+        tr, cfg = G.generate(dict(G.CONFIGS["c2"], n_users=300_000, n_calls=400_000, seed=43)), dict(tier_max=2)
+    gpr = F.build_app_profiles(ctx, F.Trace(tr), cfg).read()
+    op = O.profile(tr, cfg)
+    _cmp_profile(gpr, op, 5)
+    if case == "dense":
+        assert int(np.max(op["peak_r_u"])) > 64                           # windows longer than two steps
+        assert (op["peak_r_ua"] > 0).sum() > (op["peak_r_u"] > 0).sum()  # users with several apps
+
+
 def test_profile_c2_full(F, ctx):
     tr = G.generate("c2")
     cfg = dict(tier_max=0)

@@ -1,0 +1,8 @@
+# profile v2 check: profile parity tests (incl. the user-order cases and the C4 golden) + C4/C3 timings
+mkdir -p gpurun_out
+python paper_2411_15997_b200/build.py
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "profile or example_P" > gpurun_out/prof_tests.log 2>&1; echo "exit $?" >> gpurun_out/prof_tests.log
+timeout 600 python -m pytest tests/test_gpu_fullsize.py -x -q -k "c4 or full_size" > gpurun_out/prof_full.log 2>&1; echo "exit $?" >> gpurun_out/prof_full.log
+timeout 300 python tools/time_profile.py c4 5 > gpurun_out/time_c4.log 2>&1
+timeout 300 python tools/time_profile.py c3 5 > gpurun_out/time_c3.log 2>&1
+tail -n 3 gpurun_out/prof_tests.log; tail -n 3 gpurun_out/prof_full.log; cat gpurun_out/time_c4.log gpurun_out/time_c3.log
