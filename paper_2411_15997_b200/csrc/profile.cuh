@@ -94,7 +94,7 @@ static void profile_mirror(fs_profile* P, cudaStream_t s) {   // device -> host 
 }
 
 // ------------------------------------------------------------------ K3 + K4 streaming pass
-// Persistent grid-stride CTAs.  Sums: shared u64 atomics per (app, stage').
+// Persistent grid-stride CTAs.  Sums: shared u32 atomics per (app, stage') with carry words.
 // Histograms: shared u32 bins for apps [a0, a0+na) (blockIdx.y chunks the apps
 // when A*5*240*4 B does not fit next to the sums).  Flush: one global atomic per
 // non-zero shared entry.
@@ -112,36 +112,32 @@ static const u32 HB_APP = 768;
 
 __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const u32 J1 = a.J + 1, A = a.t.A;
+  const u32 J1 = a.J + 1, A = a.t.A, AJ = A * J1;
   const u32 a0 = blockIdx.y * a.na_chunk, na = min(a.na_chunk, A - a0);
   const bool do_sums = blockIdx.y == 0;
-  u64* ssum = (u64*)sm;                              // [4][A*J1] (only chunk 0)
-  u32* shist = (u32*)(sm + (do_sums ? (size_t)4 * A * J1 * 8 : 0));   // [na][HB_APP]
-  const u32 nsum = do_sums ? 4 * A * J1 : 0, nh = na * HB_APP;
-  for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) ssum[k] = 0;
+  // sums as u32 pairs: lo[4][AJ] then hi[4][AJ] (a u64 shared atomicAdd is a CAS loop on sm_100a;
+  // a u32 add returns the old value, and the add that wraps it carries into hi)
+  u32* slo = (u32*)sm;
+  u32* shi = slo + 4 * AJ;
+  u32* shist = (u32*)(sm + (do_sums ? (size_t)4 * AJ * 8 : 0));   // [na][HB_APP]
+  const u32 nsum = do_sums ? 8 * AJ : 0, nh = na * HB_APP;
+  for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) slo[k] = 0;
   for (u32 k = threadIdx.x; k < nh; k += blockDim.x) shist[k] = 0;
   __syncthreads();
   const u64 n = a.t.n;
+  auto add64 = [&](u32 k, u32 v) {
+    if (!v) return;
+    const u32 old = atomicAdd(&slo[k], v);
+    if (old + v < old) atomicAdd(&shi[k], 1u);
+  };
   // one call: shared-memory atomics straight into the CTA's private sums and bins (integer adds
-  // commute, so the result is order-independent); same-address lanes are merged by the hardware
-  const int lane = threadIdx.x & 31;
-  // one call: few hot (app, stage') keys, so the sums take one warp-aggregated shared atomic
-  // per key (__match_any_sync); histogram bins take one shared atomic per call (measured
-  // faster than matching every field: 275 vs 416 / 438 us at C3)
+  // commute, so the result is order-independent)
   auto one = [&](bool ok, u32 m, u32 Li, u32 Ls, u32 Lo) {
     ok = ok && m_tier(m) <= a.tier_max;
     u32 app = m_app(m), st = m_stage(m);
-    if (do_sums) {
-      u32 key = ok ? app * J1 + min(st, a.J) : 0xFFFFFFFFu;
-      u32 peers = __match_any_sync(FULL_MASK, key);
-      u32 ri = __reduce_add_sync(peers, ok ? Li : 0u), rs = __reduce_add_sync(peers, ok ? Ls : 0u);
-      u32 ro = __reduce_add_sync(peers, ok ? Lo : 0u);
-      if (ok && lane == (int)(__ffs(peers) - 1)) {
-        atomicAdd((unsigned long long*)&ssum[key], (unsigned long long)__popc(peers));
-        atomicAdd((unsigned long long*)&ssum[A * J1 + key], (unsigned long long)ri);
-        atomicAdd((unsigned long long*)&ssum[2 * A * J1 + key], (unsigned long long)rs);
-        atomicAdd((unsigned long long*)&ssum[3 * A * J1 + key], (unsigned long long)ro);
-      }
+    if (do_sums && ok) {
+      const u32 key = app * J1 + min(st, a.J);
+      add64(key, 1u); add64(AJ + key, Li); add64(2 * AJ + key, Ls); add64(3 * AJ + key, Lo);
     }
     if (!ok || app < a0 || app >= a0 + na) return;
     u32* hb = shist + (app - a0) * HB_APP;              // (clamped: an out-of-range trace fails validation)
@@ -172,10 +168,10 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
     one(ok, m, Li, Ls, Lo);
   }
   __syncthreads();
-  for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) {
-    u64 v = ssum[k];
+  for (u32 k = threadIdx.x; k < 4 * AJ; k += blockDim.x) {
+    const u64 v = (u64)shi[k] << 32 | slo[k];
     if (v) {
-      u32 arr = k / (A * J1), idx = k % (A * J1);
+      u32 arr = k / AJ, idx = k % AJ;
       u64* dst = arr == 0 ? a.cnt : arr == 1 ? a.s_in : arr == 2 ? a.s_sys : a.s_out;
       atomicAdd((unsigned long long*)&dst[idx], (unsigned long long)v);
     }
@@ -445,11 +441,13 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
       u64 carry = 0, mt = 0;
       u32 mr = 0;
       bool over = false;
+      uint4 vnext = make_uint4(0, 0, 0, 0);
+      if (h + lane < pe) vnext = a.it[h + lane];
       for (u64 c0 = h; c0 < pe; c0 += 32) {
         const u64 p = c0 + lane;
         const bool ok = p < pe, real = ok && p >= ps;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (ok) v = a.it[p];
+        const uint4 v = vnext;                               // loaded one step ahead
+        if (p + 32 < pe) vnext = a.it[p + 32];
         const u32 app = ok ? (v.w & 255u) : 256u + lane, jj = min((v.w >> 8) & 255u, a.J);
         const u64 tau = ok ? (u64)v.y + (u64)a.wo * __ldg(&a.ohat[(u64)app * J1 + jj]) : 0;
         const i64 t = v.x;
@@ -664,13 +662,11 @@ __global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
   }
   __syncthreads();
   const u64 n = a.t.n, stride = (u64)gridDim.x * blockDim.x;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    u32 m = __ldg(&a.t.meta[i]);
-    if (m_tier(m) > a.tier_max) continue;
-    u32 app = m_app(m);
+  auto one = [&](u32 m, u32 li, u32 ls, u32 lo) {
+    if (m_tier(m) > a.tier_max) return;
+    const u32 app = m_app(m);
     u32 v[4];
-    v[0] = __ldg(&a.t.len_in[i]); v[1] = __ldg(&a.t.len_sys[i]); v[2] = __ldg(&a.t.len_out[i]);
-    v[3] = v[0] + v[1] + v[2];
+    v[0] = li; v[1] = ls; v[2] = lo; v[3] = li + ls + lo;
 #pragma unroll
     for (int f = 0; f < 4; f++) {
       u32 af = app * 4 + f, b = loglin_bin(v[f]);
@@ -683,7 +679,16 @@ __global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
         }
       }
     }
+  };
+  const bool vec = (((uintptr_t)a.t.meta | (uintptr_t)a.t.len_in | (uintptr_t)a.t.len_sys | (uintptr_t)a.t.len_out) & 15) == 0;
+  const u64 n4 = vec ? n / 4 : 0;
+  for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {   // 4 calls per thread
+    const uint4 M = __ldg((const uint4*)a.t.meta + q), I = __ldg((const uint4*)a.t.len_in + q);
+    const uint4 S4 = __ldg((const uint4*)a.t.len_sys + q), O = __ldg((const uint4*)a.t.len_out + q);
+    one(M.x, I.x, S4.x, O.x); one(M.y, I.y, S4.y, O.y); one(M.z, I.z, S4.z, O.z); one(M.w, I.w, S4.w, O.w);
   }
+  for (u64 i = n4 * 4 + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    one(__ldg(&a.t.meta[i]), __ldg(&a.t.len_in[i]), __ldg(&a.t.len_sys[i]), __ldg(&a.t.len_out[i]));
 }
 
 // thread per rank: narrow to the sub-bin holding it

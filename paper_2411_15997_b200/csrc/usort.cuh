@@ -8,22 +8,22 @@
 //   x = t_ms, y = w_in L_I + w_sys L_S (the output reserve w_out O-hat is added by the
 //   window kernel, after the multi-GPU round that fixes O-hat), z = user, w = app | stage << 8.
 //
-// Passes (digits of <= 9 bits, 1-3 passes for U <= 2^27):
-//   k_os_hist   one streaming read of user + meta: per-pass digit histograms (shared, then global)
-//   k_os_bases  exclusive scan of each pass's histogram -> the digits' global bases
-//   k_os_pass   per 4096-item tile: load (pass 0 from the trace's SoA fields, later passes from
-//               the previous pass's items), rank every item stably in the tile (bit-sliced
-//               ballots per warp round), publish the tile's digit counts and look back over the
-//               preceding tiles (decoupled look-back, one status word per tile and digit: 2 state
-//               bits + 30 count bits), then stage the tile in shared memory in digit order so
-//               that consecutive threads store consecutive addresses of a digit's run.
+// Passes (digits of <= 9 bits, 1-3 passes for U <= 2^27), reduce-then-scan per pass:
+//   k_os_tile_hist  per 4096-item tile: the digit histogram of its counted items (pass 0 reads
+//                   user + meta of the trace, later passes the items' user word), digit-major
+//   excl_scan       over [digit][tile]: every (tile, digit)'s global destination
+//   k_os_pass       per tile: load (pass 0 from the trace's SoA fields, later passes from the
+//                   previous pass's items), rank every item stably in the tile (bit-sliced
+//                   ballots per warp round), then stage the tile in shared memory in digit order
+//                   so that consecutive threads store consecutive addresses of a digit's run.
+//                   No tile waits on another (a decoupled look-back here serialised the tiles:
+//                   its chain of inclusive prefixes advanced a few tiles per L2 round trip).
 //   k_useg      segment offsets seg[u] = first position of user u (binary search).
 #pragma once
 #include "index.cuh"
 
 static const int OS_T = 256, OS_IPT = 16, OS_TILE = OS_T * OS_IPT, OS_W = OS_T / 32;
 static const int OS_RMAX = 512;                 // digits of up to 9 bits
-static const u32 OS_AGG = 1u << 30, OS_INC = 2u << 30, OS_VAL = (1u << 30) - 1;
 
 struct OsPlan { int passes, dbits, shift[3]; };
 static inline OsPlan os_plan(u32 U) {
@@ -42,51 +42,47 @@ __device__ __forceinline__ bool os_counted(const OsSrc& s, u32 m) {
   return m_tier(m) <= s.tier_max && (!s.heads_only || m_stage(m) == 1);
 }
 
-// per-pass digit histograms of the counted calls: hist[p][R]
-__global__ void __launch_bounds__(512) k_os_hist(OsSrc s, OsPlan pl, u32* hist) {
-  __shared__ u32 h[3][OS_RMAX];
-  const u32 R = 1u << pl.dbits;
-  for (u32 k = threadIdx.x; k < 3 * OS_RMAX; k += blockDim.x) (&h[0][0])[k] = 0;
+// per tile: digit histogram of the counted items, th[d * ntiles + tile]; pass 0 reads the trace
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_os_tile_hist(OsSrc s, const uint4* in, u64 n_in, int shift, u32 R, u32 ntiles,
+                                                      u32* th) {
+  __shared__ u32 h[OS_RMAX];
+  for (u32 k = threadIdx.x; k < R; k += blockDim.x) h[k] = 0;
   __syncthreads();
-  const u64 n = s.t.n, stride = (u64)gridDim.x * blockDim.x;
-  const bool vec = (((uintptr_t)s.t.user | (uintptr_t)s.t.meta) & 15) == 0;
-  const u64 n4 = vec ? n / 4 : 0;
-  auto one = [&](u32 u, u32 m) {
-    if (!os_counted(s, m)) return;
-    for (int p = 0; p < pl.passes; p++) atomicAdd(&h[p][(u >> pl.shift[p]) & (R - 1)], 1u);
-  };
-  for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
-    uint4 U4 = __ldg((const uint4*)s.t.user + q), M4 = __ldg((const uint4*)s.t.meta + q);
-    one(U4.x, M4.x); one(U4.y, M4.y); one(U4.z, M4.z); one(U4.w, M4.w);
+  const u64 base = (u64)blockIdx.x * OS_TILE;
+  if (FIRST) {
+    const bool vec = (((uintptr_t)s.t.user | (uintptr_t)s.t.meta) & 15) == 0 && base + OS_TILE <= n_in;
+    if (vec) {
+#pragma unroll
+      for (int r = 0; r < OS_TILE / 4 / 256; r++) {
+        const u64 q = base / 4 + (u64)r * 256 + threadIdx.x;
+        const uint4 U4 = __ldg((const uint4*)s.t.user + q), M4 = __ldg((const uint4*)s.t.meta + q);
+        if (os_counted(s, M4.x)) atomicAdd(&h[(U4.x >> shift) & (R - 1)], 1u);
+        if (os_counted(s, M4.y)) atomicAdd(&h[(U4.y >> shift) & (R - 1)], 1u);
+        if (os_counted(s, M4.z)) atomicAdd(&h[(U4.z >> shift) & (R - 1)], 1u);
+        if (os_counted(s, M4.w)) atomicAdd(&h[(U4.w >> shift) & (R - 1)], 1u);
+      }
+    } else {
+      for (u32 k = threadIdx.x; k < OS_TILE; k += 256) {
+        const u64 i = base + k;
+        if (i < n_in && os_counted(s, __ldg(&s.t.meta[i]))) atomicAdd(&h[(__ldg(&s.t.user[i]) >> shift) & (R - 1)], 1u);
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (u32 k = threadIdx.x; k < OS_TILE; k += 256) {
+      const u64 i = base + k;
+      if (i < n_in) atomicAdd(&h[(in[i].z >> shift) & (R - 1)], 1u);
+    }
   }
-  for (u64 i = n4 * 4 + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    one(__ldg(&s.t.user[i]), __ldg(&s.t.meta[i]));
   __syncthreads();
-  for (u32 k = threadIdx.x; k < (u32)pl.passes * R; k += blockDim.x) {
-    u32 v = h[k / R][k % R];
-    if (v) atomicAdd(&hist[k], v);
-  }
-}
-
-// one block per pass: bases[p][d] = sum of hist[p][d'] for d' < d; tot[p] = all
-__global__ void k_os_bases(const u32* hist, u32 R, u32* bases, u32* tot) {
-  __shared__ u32 sh[32];
-  const u32* h = hist + (u64)blockIdx.x * R;
-  u32* b = bases + (u64)blockIdx.x * R;
-  u32 v0 = 2 * threadIdx.x < R ? h[2 * threadIdx.x] : 0, v1 = 2 * threadIdx.x + 1 < R ? h[2 * threadIdx.x + 1] : 0;
-  u32 total;
-  u32 ex = block_excl_scan<u32>(v0 + v1, sh, &total);
-  if (2 * threadIdx.x < R) b[2 * threadIdx.x] = ex;
-  if (2 * threadIdx.x + 1 < R) b[2 * threadIdx.x + 1] = ex + v0;
-  if (threadIdx.x == 0) tot[blockIdx.x] = total;
+  for (u32 d = threadIdx.x; d < R; d += blockDim.x) th[(u64)d * ntiles + blockIdx.x] = h[d];
 }
 
 struct OsPassArgs {
   OsSrc src; const uint4* in; u64 n_in;       // pass 0 reads src (n_in = trace calls), else in[n_in]
-  uint4* out; int shift; u32 R;
-  const u32* base;                            // [R] digit bases of this pass
-  u32* look;                                  // [ntiles][R] status words (zeroed)
-  u32* ticket;                                // tile ticket (zeroed)
+  uint4* out; int shift; u32 R, ntiles;
+  const u32* off;                             // [R][ntiles] exclusive scan of the tile histograms
 };
 
 // lanes of the warp (ok lanes only) holding the same digit of `bits` bits: bit-sliced ballots
@@ -105,35 +101,56 @@ __global__ void __launch_bounds__(OS_T, 2) k_os_pass(const __grid_constant__ OsP
   __shared__ u32 wcnt[OS_W][OS_RMAX];         // per warp digit counts, then warp offsets
   __shared__ u32 tstart[OS_RMAX], gdst[OS_RMAX];
   __shared__ u32 sh[32];
-  __shared__ u32 s_tile, s_cnt;
-  if (threadIdx.x == 0) s_tile = atomicAdd(a.ticket, 1u);   // tiles start in ticket order (look-back progress)
+  __shared__ u32 s_cnt;
   for (u32 k = threadIdx.x; k < OS_W * OS_RMAX; k += OS_T) (&wcnt[0][0])[k] = 0;
+  const u32 tile = blockIdx.x, R = a.R, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (u32 d = threadIdx.x; d < R; d += OS_T) gdst[d] = a.off[(u64)d * a.ntiles + tile];
   __syncthreads();
-  const u32 tile = s_tile, R = a.R, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int bits = 31 - __clz(R);
   const u64 base = (u64)tile * OS_TILE + (u64)w * (OS_IPT * 32);
   uint4 it[OS_IPT];
   u32 dg[OS_IPT], rk[OS_IPT];
-  // every global load of the tile in flight before the ranking
+  // every global load of the tile in flight before the ranking: a full tile takes unguarded
+  // loads in one block (a guard per round kept only one round's loads in flight)
+  const bool full = (u64)(tile + 1) * OS_TILE <= a.n_in;
+  if (FIRST) {
+    const DTrace& t = a.src.t;
+    if (full) {
+      u32 m[OS_IPT], tm[OS_IPT], li[OS_IPT], ls[OS_IPT], us[OS_IPT];
 #pragma unroll
-  for (int r = 0; r < OS_IPT; r++) {
-    const u64 i = base + (u64)r * 32 + lane;
-    uint4 v = make_uint4(0, 0, 0, 0xFFFFFFFFu);            // w = all ones: not an item
-    if (i < a.n_in) {
-      if (FIRST) {
-        const DTrace& t = a.src.t;
-        const u32 m = __ldg(&t.meta[i]);
-        if (os_counted(a.src, m)) {
-          v.x = __ldg(&t.t_ms[i]);
-          v.y = a.src.wi * __ldg(&t.len_in[i]) + a.src.ws * __ldg(&t.len_sys[i]);
-          v.z = __ldg(&t.user[i]);
-          v.w = (m & 255u) | (m_stage(m) << 8);
+      for (int r = 0; r < OS_IPT; r++) {
+        const u64 i = base + (u64)r * 32 + lane;
+        m[r] = __ldg(&t.meta[i]); tm[r] = __ldg(&t.t_ms[i]); li[r] = __ldg(&t.len_in[i]);
+        ls[r] = __ldg(&t.len_sys[i]); us[r] = __ldg(&t.user[i]);
+      }
+#pragma unroll
+      for (int r = 0; r < OS_IPT; r++)
+        it[r] = os_counted(a.src, m[r]) ? make_uint4(tm[r], a.src.wi * li[r] + a.src.ws * ls[r], us[r],
+                                                    (m[r] & 255u) | (m_stage(m[r]) << 8))
+                                        : make_uint4(0, 0, 0, 0xFFFFFFFFu);
+    } else {
+#pragma unroll
+      for (int r = 0; r < OS_IPT; r++) {
+        const u64 i = base + (u64)r * 32 + lane;
+        uint4 v = make_uint4(0, 0, 0, 0xFFFFFFFFu);            // w = all ones: not an item
+        if (i < a.n_in) {
+          const u32 m = __ldg(&t.meta[i]);
+          if (os_counted(a.src, m))
+            v = make_uint4(__ldg(&t.t_ms[i]), a.src.wi * __ldg(&t.len_in[i]) + a.src.ws * __ldg(&t.len_sys[i]),
+                           __ldg(&t.user[i]), (m & 255u) | (m_stage(m) << 8));
         }
-      } else {
-        v = a.in[i];
+        it[r] = v;
       }
     }
-    it[r] = v;
+  } else if (full) {
+#pragma unroll
+    for (int r = 0; r < OS_IPT; r++) it[r] = a.in[base + (u64)r * 32 + lane];
+  } else {
+#pragma unroll
+    for (int r = 0; r < OS_IPT; r++) {
+      const u64 i = base + (u64)r * 32 + lane;
+      it[r] = i < a.n_in ? a.in[i] : make_uint4(0, 0, 0, 0xFFFFFFFFu);
+    }
   }
   const u32 lt = lanemask_lt();
 #pragma unroll
@@ -160,61 +177,6 @@ __global__ void __launch_bounds__(OS_T, 2) k_os_pass(const __grid_constant__ OsP
   if (d0 < R) tstart[d0] = ex;
   if (d1 < R) tstart[d1] = ex + c0;
   if (threadIdx.x == 0) s_cnt = total;
-  // decoupled look-back per digit over the preceding tiles: both digits of the thread walk
-  // back together, four tiles per round (independent loads), to the nearest inclusive prefix
-  u32* look = a.look;
-  const bool h0 = d0 < R, h1 = d1 < R;
-  if (tile == 0) {
-    if (h0) { *(volatile u32*)(look + d0) = OS_INC | c0; gdst[d0] = a.base[d0]; }
-    if (h1) { *(volatile u32*)(look + d1) = OS_INC | c1; gdst[d1] = a.base[d1]; }
-  } else {
-    if (h0) *(volatile u32*)(look + (u64)tile * R + d0) = OS_AGG | c0;
-    if (h1) *(volatile u32*)(look + (u64)tile * R + d1) = OS_AGG | c1;
-    u32 p0 = 0, p1 = 0;
-    bool done0 = !h0, done1 = !h1;
-    long long j = (long long)tile - 1;
-    while (!(done0 && done1)) {
-      u32 v0[4], v1[4];
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const long long jj = j - k;
-        v0[k] = v1[k] = OS_INC;                             // before tile 0: an inclusive 0
-        if (jj >= 0) {
-          if (!done0) v0[k] = *(volatile u32*)(look + (u64)jj * R + d0);
-          if (!done1) v1[k] = *(volatile u32*)(look + (u64)jj * R + d1);
-        }
-      }
-      bool ready = true;                                    // every state up to the first inclusive
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        if (!done0) { if (v0[k] >> 30 == 0) ready = false; }
-        if (!done1) { if (v1[k] >> 30 == 0) ready = false; }
-      }
-      if (!ready) {                                         // consume the prefix that is ready
-        bool stop0 = done0, stop1 = done1;
-        int adv = 4;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-          if (!stop0 && v0[k] >> 30 == 0) { adv = min(adv, k); stop0 = true; }
-          if (!stop1 && v1[k] >> 30 == 0) { adv = min(adv, k); stop1 = true; }
-        }
-        for (int k = 0; k < adv; k++) {
-          if (!done0) { p0 += v0[k] & OS_VAL; if (v0[k] >> 30 == 2) done0 = true; }
-          if (!done1) { p1 += v1[k] & OS_VAL; if (v1[k] >> 30 == 2) done1 = true; }
-        }
-        j -= adv;
-        continue;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        if (!done0) { p0 += v0[k] & OS_VAL; if (v0[k] >> 30 == 2) done0 = true; }
-        if (!done1) { p1 += v1[k] & OS_VAL; if (v1[k] >> 30 == 2) done1 = true; }
-      }
-      j -= 4;
-    }
-    if (h0) { *(volatile u32*)(look + (u64)tile * R + d0) = OS_INC | (p0 + c0); gdst[d0] = a.base[d0] + p0; }
-    if (h1) { *(volatile u32*)(look + (u64)tile * R + d1) = OS_INC | (p1 + c1); gdst[d1] = a.base[d1] + p1; }
-  }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < OS_IPT; r++)
@@ -248,25 +210,11 @@ static bool build_user_order(fs_ctx* ctx, Scratch& S, const DTrace& t, u32 tier_
   const OsPlan pl = os_plan(t.U);
   const u32 R = 1u << pl.dbits;
   OsSrc src{t, tier_max, heads_only, wi, ws};
-  u32* hist = S.zeros<u32>((size_t)3 * R);
-  u32* bases = S.alloc<u32>((size_t)3 * R);
-  u32* tot = S.alloc<u32>(4);
-  u32* tickets = S.zeros<u32>(4);
-  if (S.failed) return false;
   const u64 n = t.n;
-  if (n) {
-    const int grid = (int)std::max<u64>(1, std::min<u64>((u64)ctx->sm_count * 4, div_up(n, 2048)));
-    FS_LAUNCH(ctx, "os_hist", k_os_hist, grid, 512, 0, src, pl, hist);
-  }
-  FS_LAUNCH(ctx, "os_bases", k_os_bases, pl.passes, 256, 0, hist, R, bases, tot);
-  u32 m = 0;
-  cudaMemcpyAsync(&m, tot, 4, cudaMemcpyDeviceToHost, ctx->stream);
-  cudaStreamSynchronize(ctx->stream);
-  uo->n = m;
-  uint4* buf[2] = {S.alloc<uint4>(m + 1), pl.passes > 1 ? S.alloc<uint4>(m + 1) : nullptr};
+  const u32 nt0 = (u32)div_up(std::max<u64>(n, 1), OS_TILE);
+  u32* th = S.alloc<u32>((size_t)R * nt0 + 1);
+  u32* off = S.alloc<u32>((size_t)R * nt0 + 1);
   uo->seg = S.alloc<u64>((size_t)t.U + 1);
-  const u64 maxtiles = div_up(std::max<u64>(n, 1), OS_TILE);
-  u32* look = S.alloc<u32>(maxtiles * R);
   if (S.failed) return false;
   const size_t smem = (size_t)OS_TILE * sizeof(uint4);
   static bool attr = false;
@@ -275,21 +223,37 @@ static bool build_user_order(fs_ctx* ctx, Scratch& S, const DTrace& t, u32 tier_
     cudaFuncSetAttribute(k_os_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  u64 m = 0;
+  uint4* buf[2] = {nullptr, nullptr};
   const uint4* in = nullptr;
   for (int p = 0; p < pl.passes; p++) {
     const u64 nin = p == 0 ? n : m;
-    const int nt = div_up(std::max<u64>(nin, 1), OS_TILE);
+    const u32 nt = (u32)div_up(std::max<u64>(nin, 1), OS_TILE);
+    const u64 nw = (u64)R * nt;
+    if (nin) {
+      if (p == 0) FS_LAUNCH(ctx, "os_tile_hist", k_os_tile_hist<true>, nt, 256, 0, src, nullptr, nin, pl.shift[p], R, nt, th);
+      else FS_LAUNCH(ctx, "os_tile_hist", k_os_tile_hist<false>, nt, 256, 0, src, in, nin, pl.shift[p], R, nt, th);
+    } else cudaMemsetAsync(th, 0, nw * 4, ctx->stream);
+    excl_scan<u32>(ctx, S, th, off, nw, off + nw);
+    if (p == 0) {                               // the number of counted calls sizes the buffers
+      u32 hm = 0;
+      cudaMemcpyAsync(&hm, off + nw, 4, cudaMemcpyDeviceToHost, ctx->stream);
+      cudaStreamSynchronize(ctx->stream);
+      m = hm;
+      buf[0] = S.alloc<uint4>(m + 1);
+      if (pl.passes > 1) buf[1] = S.alloc<uint4>(m + 1);
+      if (S.failed) return false;
+    }
     uint4* out = buf[p & 1];
-    cudaMemsetAsync(look, 0, (size_t)nt * R * 4, ctx->stream);
-    OsPassArgs a{src, in, nin, out, pl.shift[p], R, bases + (size_t)p * R, look, tickets + p};
+    OsPassArgs a{src, in, nin, out, pl.shift[p], R, nt, off};
     if (nin) {
       if (p == 0) FS_LAUNCH(ctx, "os_pass", k_os_pass<true>, nt, OS_T, smem, a);
       else FS_LAUNCH(ctx, "os_pass", k_os_pass<false>, nt, OS_T, smem, a);
     }
     in = out;
   }
+  uo->n = m;
   uo->it = (uint4*)in;
-  if (!uo->it) uo->it = buf[0];
   FS_LAUNCH(ctx, "useg", k_useg, div_up((u64)t.U + 1, 256), 256, 0, uo->it, m, t.U, uo->seg);
   return true;
 }
