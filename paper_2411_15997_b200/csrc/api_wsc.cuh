@@ -116,7 +116,7 @@ static bool wsc_shared(fs_ctx* ctx, Scratch& S, const DTrace& t, const fs_profil
                        u64 ring_cap, WscShared* W, TauW tw = TauW{1, 1, 1}) {
   u64 n = t.n;
   int B = 256;
-  build_links(ctx, S, t, &W->L);
+  validate_trace(ctx, S, t, &W->L);
   u32* flag = S.alloc<u32>(n + 1);
   u32* pre = S.alloc<u32>(n + 1);
   W->utier = S.alloc<u32>(t.U + 1);

@@ -263,8 +263,7 @@ extern "C" int fs_profile_local(fs_ctx* ctx, const fs_trace* tr, const fs_profil
   pp->P->q_ppm = pp->qppm;
   err_reset(ctx);
   Scratch& S = *pp->S;
-  Links L;
-  build_links(ctx, S, pp->t, &L);
+  validate_trace(ctx, S, pp->t, nullptr);
   int rc = finish(ctx, &S);
   if (rc) { fs_profile_free(pp->P); delete pp; return rc; }
   u64 AJ = (u64)A * (J + 1);
@@ -549,7 +548,7 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   u64 n = t.n;
   if (n == 0) return FS_OK;
   Links L;
-  build_links(ctx, S, t, &L);
+  validate_trace(ctx, S, t, &L);
   LimitsDev LD;
   if (!act_limits(ctx, S, P, cfg, t.A, &LD)) return S.failed ? FS_E_NOMEM : FS_E_INVAL;
   DLimits hL;

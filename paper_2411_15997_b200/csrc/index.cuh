@@ -136,6 +136,138 @@ static bool build_links(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
   return true;
 }
 
+// ------------------------------------------------------------------ fast validity path
+// A valid trace passes every R1 check; the fast path decides validity exactly with two streaming
+// passes and no ordering atomics, and only an invalid trace pays for the exact kernels above
+// (which find the error code and the first offending index, as the oracle):
+//   k_vf_range  4 calls per thread (uint4 loads of the seven fields): range, time order; every
+//               head (stage 1) stores its record {index, user, app | ncalls << 8} and its size
+//               (plain stores: a second head of the same interaction is caught below)
+//   scan        slot offsets off[x] = sum of the heads' sizes before x
+//   k_vf_slots  per call: its interaction has a head with the same user / app / ncalls, a head
+//               is the recorded one, and its slot (off[x] + stage - 1) is claimed once (CAS)
+//   k_vf_links  per call below its interaction's last stage: the successor's slot holds a later
+//               index (every adjacent pair of stages is checked once); head_of / next_call are
+//               written when the caller wants the links
+// Valid <=> no flag and sum of the heads' sizes == n (then the n claims fill every slot, so
+// every predecessor and successor exists).
+struct VfArgs {
+  DTrace t; u32* flag; uint4* hrec; u32* hsize; unsigned long long* msum;
+};
+__device__ __forceinline__ bool vf_range(const DTrace& t, u32 u, u32 m, u32 x, u32 li, u32 ls, u32 lo) {
+  const u32 LMAX = 1u << 24, st = m_stage(m), nc = m_ncalls(m);
+  return u < t.U && m_app(m) < t.A && x < t.X && st != 0 && nc != 0 && st <= nc && li < LMAX && ls < LMAX &&
+         lo < LMAX && lo != 0;
+}
+__global__ void __launch_bounds__(256) k_vf_range(VfArgs a) {
+  const DTrace& t = a.t;
+  const u64 n = t.n, stride = (u64)gridDim.x * blockDim.x;
+  bool bad = false;
+  u64 ms = 0;
+  auto one = [&](u64 i, u32 u, u32 tm, u32 tp, u32 m, u32 x, u32 li, u32 ls, u32 lo) {
+    if (!vf_range(t, u, m, x, li, ls, lo) || (i > 0 && tm < tp)) { bad = true; return; }
+    if (m_stage(m) == 1) {
+      a.hrec[x] = make_uint4((u32)i, u, m & 0x00FF00FFu, 0);
+      a.hsize[x] = m_ncalls(m);
+      ms += m_ncalls(m);
+    }
+  };
+  const bool vec = (((uintptr_t)t.user | (uintptr_t)t.t_ms | (uintptr_t)t.meta | (uintptr_t)t.inter | (uintptr_t)t.len_in |
+                     (uintptr_t)t.len_sys | (uintptr_t)t.len_out) & 15) == 0;
+  const u64 n4 = vec ? n / 4 : 0;
+  for (u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
+    const uint4 U4 = __ldg((const uint4*)t.user + q), T4 = __ldg((const uint4*)t.t_ms + q);
+    const uint4 M4 = __ldg((const uint4*)t.meta + q), X4 = __ldg((const uint4*)t.inter + q);
+    const uint4 I4 = __ldg((const uint4*)t.len_in + q), S4 = __ldg((const uint4*)t.len_sys + q);
+    const uint4 O4 = __ldg((const uint4*)t.len_out + q);
+    const u32 tp = q ? __ldg(&t.t_ms[4 * q - 1]) : 0;
+    one(4 * q, U4.x, T4.x, tp, M4.x, X4.x, I4.x, S4.x, O4.x);
+    one(4 * q + 1, U4.y, T4.y, T4.x, M4.y, X4.y, I4.y, S4.y, O4.y);
+    one(4 * q + 2, U4.z, T4.z, T4.y, M4.z, X4.z, I4.z, S4.z, O4.z);
+    one(4 * q + 3, U4.w, T4.w, T4.z, M4.w, X4.w, I4.w, S4.w, O4.w);
+  }
+  for (u64 i = n4 * 4 + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    one(i, t.user[i], t.t_ms[i], i ? t.t_ms[i - 1] : 0, t.meta[i], t.inter[i], t.len_in[i], t.len_sys[i], t.len_out[i]);
+  if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
+  u64 w = ms;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(FULL_MASK, w, o);
+  if ((threadIdx.x & 31) == 0 && w) atomicAdd(a.msum, (unsigned long long)w);
+}
+struct VfSlotArgs {
+  DTrace t; u32* flag; const uint4* hrec; const u32* off; u32* slot;
+};
+__global__ void __launch_bounds__(256) k_vf_slots(VfSlotArgs a) {
+  const DTrace& t = a.t;
+  const u64 n = t.n;
+  bool bad = false;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u32 x = __ldg(&t.inter[i]), m = __ldg(&t.meta[i]), u = __ldg(&t.user[i]);
+    const uint4 e = a.hrec[x];
+    const u32 s = m_stage(m), nc = m_ncalls(m);
+    if (e.x == NONE32 || e.y != u || e.z != (m & 0x00FF00FFu) || (s == 1 && e.x != (u32)i)) { bad = true; continue; }
+    const u64 pos = (u64)a.off[x] + s - 1;
+    if (atomicCAS(&a.slot[pos], NONE32, (u32)i) != NONE32) bad = true;
+  }
+  if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
+}
+__global__ void __launch_bounds__(256) k_vf_links(DTrace t, const uint4* hrec, const u32* off, const u32* slot,
+                                                  u32* flag, u32* head_of, u32* next_call) {
+  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (i < t.n) {
+    const u32 x = __ldg(&t.inter[i]), m = __ldg(&t.meta[i]);
+    const u32 s = m_stage(m);
+    const u32 nx = s < m_ncalls(m) ? slot[(u64)off[x] + s] : NONE32;
+    bad = nx != NONE32 && nx <= (u32)i;                     // the successor comes later (R1)
+    if (head_of) { head_of[i] = hrec[x].x; next_call[i] = nx; }
+  }
+  if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+// Validate the trace (and fill the links if L): the fast path above, else the exact kernels.
+// Errors land in ctx->err.  Returns false on allocation failure.
+static bool validate_trace(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
+  const u64 n = t.n;
+  Links tmp;
+  Links* LL = L ? L : &tmp;
+  if (n == 0 || n >= 0xFFFFFFFFull || t.X == 0) return build_links(ctx, S, t, LL);
+  u32* flag = S.zeros<u32>(2);
+  u64* msum = S.zeros<u64>(1);
+  uint4* hrec = S.alloc<uint4>((size_t)t.X + 1);
+  u32* hsize = S.zeros<u32>((size_t)t.X + 1);
+  u32* off = S.alloc<u32>((size_t)t.X + 2);
+  if (S.failed) return false;
+  cudaMemsetAsync(hrec, 0xFF, ((size_t)t.X + 1) * sizeof(uint4), ctx->stream);
+  VfArgs va{t, flag, hrec, hsize, (unsigned long long*)msum};
+  const int g1 = (int)std::max<u64>(1, std::min<u64>((u64)ctx->sm_count * 16, div_up(div_up(n, 4), 256)));
+  FS_LAUNCH(ctx, "vf_range", k_vf_range, g1, 256, 0, va);
+  u64 h[2] = {0, 0};
+  cudaMemcpyAsync(&h[0], flag, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaMemcpyAsync(&h[1], msum, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if ((u32)h[0] || h[1] != n) return build_links(ctx, S, t, LL);          // invalid: the exact kernels
+  excl_scan<u32>(ctx, S, hsize, off, t.X, off + t.X);                     // sum == n < 2^32
+  u32* slot = S.alloc<u32>(n + 1);
+  if (S.failed) return false;
+  cudaMemsetAsync(slot, 0xFF, (n + 1) * 4, ctx->stream);
+  VfSlotArgs sa{t, flag, hrec, off, slot};
+  FS_LAUNCH(ctx, "vf_slots", k_vf_slots, div_up(n, 256), 256, 0, sa);
+  u32* ho = nullptr;
+  u32* nc = nullptr;
+  if (L) {
+    ho = S.alloc<u32>(n);
+    nc = S.alloc<u32>(n);
+    if (S.failed) return false;
+  }
+  FS_LAUNCH(ctx, "vf_links", k_vf_links, div_up(n, 256), 256, 0, t, hrec, off, slot, flag, ho, nc);
+  u32 f2 = 0;
+  cudaMemcpyAsync(&f2, flag, 4, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (f2) return build_links(ctx, S, t, LL);
+  if (L) { L->head_of = ho; L->next_call = nc; }
+  return true;
+}
 // ------------------------------------------------------------------ (t, id)-ordered index
 __global__ void k_key_user_app(DTrace t, u32* key) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;

@@ -235,6 +235,16 @@ __device__ __forceinline__ u64 warp_incl_scan_u64(u64 x, u32 lane) {
   for (int o = 1; o < 32; o <<= 1) { u64 y = __shfl_up_sync(FULL_MASK, x, o); if (lane >= (u32)o) x += y; }
   return x;
 }
+// inclusive warp scan of token loads: in u32 when every value is < 2^26 (32 of them fit), else u64
+__device__ __forceinline__ u64 warp_incl_scan_tau(u64 x, u32 lane) {
+  if (__all_sync(FULL_MASK, x < (1u << 26))) {
+    u32 y = (u32)x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) { u32 z = __shfl_up_sync(FULL_MASK, y, o); if (lane >= (u32)o) y += z; }
+    return y;
+  }
+  return warp_incl_scan_u64(x, lane);
+}
 __device__ __forceinline__ void atomic_max_u64(u64* p, u64 v) { atomicMax((unsigned long long*)p, (unsigned long long)v); }
 __device__ __forceinline__ u64 reduce_max_u64(u32 mask, u64 v) {
   const u32 hi = __reduce_max_sync(mask, (u32)(v >> 32));
@@ -438,8 +448,8 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
         while (lo < hi) { const u64 m = (lo + hi) >> 1; if ((i64)a.it[m].x > thr0) hi = m; else lo = m + 1; }
         h = lo;
       }
-      u64 carry = 0, mt = 0;
-      u32 mr = 0;
+      u64 carry = 0, mt = 0, lbw = h;            // lbw: window start of the previous step's last call
+      u32 mr = 0, tprev = 0;                     // tprev (lane 0): time of position c0 - 1
       bool over = false;
       uint4 vnext = make_uint4(0, 0, 0, 0);
       if (h + lane < pe) vnext = a.it[h + lane];
@@ -451,7 +461,7 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
         const u32 app = ok ? (v.w & 255u) : 256u + lane, jj = min((v.w >> 8) & 255u, a.J);
         const u64 tau = ok ? (u64)v.y + (u64)a.wo * __ldg(&a.ohat[(u64)app * J1 + jj]) : 0;
         const i64 t = v.x;
-        const u64 inc = warp_incl_scan_u64(tau, lane);
+        const u64 inc = warp_incl_scan_tau(tau, lane);
         const u64 ex = carry + inc - tau;
         carry += __shfl_sync(FULL_MASK, inc, 31);
         const u32 vm = __ballot_sync(FULL_MASK, ok);
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
           u32 todo = vm;
           while (todo) {
             const u32 g = __shfl_sync(FULL_MASK, peers, __ffs(todo) - 1);
-            const u64 x = warp_incl_scan_u64(((g >> lane) & 1u) ? tau : 0, lane);
+            const u64 x = warp_incl_scan_tau(((g >> lane) & 1u) ? tau : 0, lane);
             if ((g >> lane) & 1u) exa = x - tau;
             todo &= ~g;
           }
@@ -485,7 +495,8 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
           if (p >= ps || c0 + last >= ps) atomicOr(&touched[app >> 5], 1u << (app & 31));
         }
         __syncwarp();
-        if (!__any_sync(FULL_MASK, real)) continue;            // a halo step: prefixes only
+        const u32 tlast = __shfl_sync(FULL_MASK, v.x, 31);
+        if (!__any_sync(FULL_MASK, real)) { tprev = tlast; continue; }   // a halo step: prefixes only
         const i64 thr = t - a.W;
         u32 lo = 0, hi = lane;
 #pragma unroll
@@ -495,21 +506,27 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
           if (lo < hi) { if (tm > thr) hi = mid; else lo = mid + 1; }
         }
         u64 lb = c0 + lo;
-        bool far = false;
-        if (real && lo == 0 && c0 > h && (i64)a.it[c0 - 1].x > thr) {
-          far = true;
-          u64 k = 1, good = c0 - 1, l2 = h;
-          for (;;) {
-            if (c0 - 1 < h + k) break;
-            const u64 q = c0 - 1 - k;
-            if ((i64)a.it[q].x > thr) { good = q; k <<= 1; continue; }
-            l2 = q + 1;
-            break;
+        bool far = real && lo == 0 && c0 > h && (i64)tprev > thr;          // tprev is warp-uniform
+        if (__any_sync(FULL_MASK, far)) {
+          // windows reaching before the step (a prefix of the lanes): lb is monotone in p, so it
+          // lies in [lbw, c0) with lbw the previous step's last window start; the warp walks that
+          // range 32 positions at a time, every far lane binary-searching the chunk's times
+          bool pend = far;
+          for (u64 base = lbw; __any_sync(FULL_MASK, pend); base += 32) {
+            const u32 tj = base + lane < c0 ? a.it[base + lane].x : 0xFFFFFFFFu;
+            const bool some = (i64)__shfl_sync(FULL_MASK, tj, 31) > thr;   // a time > thr in the chunk
+            u32 l2 = 0, h2 = 31;
+#pragma unroll
+            for (int k = 0; k < 5; k++) {
+              const u32 mid = (l2 + h2) >> 1;
+              const i64 tm = (i64)__shfl_sync(FULL_MASK, tj, mid);
+              if (l2 < h2) { if (tm > thr) h2 = mid; else l2 = mid + 1; }
+            }
+            if (pend && some) { lb = base + l2; pend = false; }
           }
-          u64 h2 = good;
-          while (l2 < h2) { const u64 m = (l2 + h2) >> 1; if ((i64)a.it[m].x > thr) h2 = m; else l2 = m + 1; }
-          lb = l2;
         }
+        tprev = tlast;
+        lbw = max(lbw, __shfl_sync(FULL_MASK, real ? lb : 0, 31));
         const u64 ring_lo = c0 + 32 > (u64)WP_R ? c0 + 32 - WP_R : 0;   // oldest position still in the ring
         const bool miss = far && lb < ring_lo;
         if (__any_sync(FULL_MASK, miss)) { over = true; break; }
