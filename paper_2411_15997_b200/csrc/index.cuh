@@ -145,12 +145,13 @@ static bool build_links(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
 //               (plain stores: a second head of the same interaction is caught below)
 //   scan        slot offsets off[x] = sum of the heads' sizes before x
 //   k_vf_slots  per call: its interaction has a head with the same user / app / ncalls, a head
-//               is the recorded one, and its slot (off[x] + stage - 1) is claimed once (CAS)
-//   k_vf_links  per call below its interaction's last stage: the successor's slot holds a later
-//               index (every adjacent pair of stages is checked once); head_of / next_call are
+//               is the recorded one, and it writes its index to its slot (off[x] + stage - 1)
+//   k_vf_links  per call: its slot holds its own index (else two calls share the slot), and
+//               below its interaction's last stage the successor's slot holds a later index
+//               (every adjacent pair of stages is checked once); head_of / next_call are
 //               written when the caller wants the links
-// Valid <=> no flag and sum of the heads' sizes == n (then the n claims fill every slot, so
-// every predecessor and successor exists).
+// Valid <=> no flag and sum of the heads' sizes == n (then the n distinct slots are all filled,
+// so every predecessor and successor exists).
 struct VfArgs {
   DTrace t; u32* flag; uint4* hrec; u32* hsize; unsigned long long* msum;
 };
@@ -206,8 +207,7 @@ __global__ void __launch_bounds__(256) k_vf_slots(VfSlotArgs a) {
     const uint4 e = a.hrec[x];
     const u32 s = m_stage(m), nc = m_ncalls(m);
     if (e.x == NONE32 || e.y != u || e.z != (m & 0x00FF00FFu) || (s == 1 && e.x != (u32)i)) { bad = true; continue; }
-    const u64 pos = (u64)a.off[x] + s - 1;
-    if (atomicCAS(&a.slot[pos], NONE32, (u32)i) != NONE32) bad = true;
+    a.slot[(u64)a.off[x] + s - 1] = (u32)i;
   }
   if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
 }
@@ -218,9 +218,13 @@ __global__ void __launch_bounds__(256) k_vf_links(DTrace t, const uint4* hrec, c
   if (i < t.n) {
     const u32 x = __ldg(&t.inter[i]), m = __ldg(&t.meta[i]);
     const u32 s = m_stage(m);
-    const u32 nx = s < m_ncalls(m) ? slot[(u64)off[x] + s] : NONE32;
-    bad = nx != NONE32 && nx <= (u32)i;                     // the successor comes later (R1)
-    if (head_of) { head_of[i] = hrec[x].x; next_call[i] = nx; }
+    const u64 pos = (u64)off[x] + s - 1;
+    if (s == 0 || pos + (s < m_ncalls(m)) >= t.n) bad = true;          // (a call k_vf_slots rejected)
+    else {
+      const u32 nx = s < m_ncalls(m) ? slot[pos + 1] : NONE32;
+      bad = slot[pos] != (u32)i || (nx != NONE32 && nx <= (u32)i);     // own slot; the successor later (R1)
+      if (head_of) { head_of[i] = hrec[x].x; next_call[i] = nx; }
+    }
   }
   if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
