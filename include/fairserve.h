@@ -130,7 +130,13 @@ void fs_profile_free(fs_profile* p);
 /* Multi-GPU, user-hash-sharded input (each rank holds whole users).  Protocol:
  *   fs_profile_local -> loop { fs_profile_round(buf, &w, &done); if (done) break; allreduce_sum_u64(buf[0:w]) }
  *   -> fs_profile_finalize.  comm_words u64 words; buf is DEVICE memory owned by the caller.
- * Every rank finalises a bit-identical profile (integer sums commute). */
+ * Rounds: R0 sums + histograms (Eq. 2; "normal range" P:466); then quantile
+ * sub-bin counts and, for the derived limits, per-set peak counts + bit lengths, then one
+ * 8-bit digit of 256-bin histograms per set and round (a radix select over the ranks' disjoint
+ * users: <= 2 (A+1) x 256 words per round, never the peaks themselves).  Every rank finalises
+ * bit-identical sums, histograms, quantiles and limits (integer sums commute); the per-user window
+ * peaks (peak_*_u / peak_*_ua) of a finalised profile are the rank's own users' (0 elsewhere).
+ * fs_profile_read / fs_wsc_state_read take the ctx whose stream the copies run on. */
 typedef struct fs_profile_partial fs_profile_partial;
 int fs_profile_local(fs_ctx* ctx, const fs_trace* shard, const fs_profile_cfg* cfg,
                      fs_profile_partial** out, size_t* comm_words_h);

@@ -352,9 +352,30 @@ static EngCfg eng_cfg(const fs_replay_cfg* c, const ScenTables& T, u32 s, u32 A,
 
 static const int ERR_TO_FS[ERR_N] = {FS_E_RANGE, FS_E_ORDER, FS_E_PROFILE, FS_E_OVERSIZE, FS_E_OVERFLOW, FS_E_NOMEM};
 
+// warp-parallel engine pieces for the FairServe modes (replay.cuh EngineT TOUR bits: 2 lane-owned batch
+// slots, 4 lanes split the ACT ring); FS_TOUR overrides the measured defaults (sweep 0, replay 6)
+static int tour_bits(int dflt) {
+  static const int v = [] { const char* e = getenv("FS_TOUR"); return e ? atoi(e) & 6 : -1; }();
+  return v >= 0 ? v : dflt;
+}
+typedef void (*SweepFn)(SweepKArgs);
+typedef void (*ReplayFn)(ReplayKArgs);
+template <int T> static SweepFn sweep_kern(int minb) {
+  return minb >= 6 ? k_sweep<6, 32, false, T> : minb == 5 ? k_sweep<5, 32, false, T> :
+         minb == 4 ? k_sweep<4, 32, false, T> : k_sweep<3, 32, false, T>;
+}
+static SweepFn sweep_kern_t(int t, int minb) {
+  return t == 2 ? sweep_kern<2>(minb) : t == 4 ? sweep_kern<4>(minb) : t == 6 ? sweep_kern<6>(minb) : sweep_kern<0>(minb);
+}
+static ReplayFn replay_warp_kern_t(int t) {
+  return t == 2 ? k_replay_warp<false, 2> : t == 4 ? k_replay_warp<false, 4> : t == 6 ? k_replay_warp<false, 6>
+                                                                             : k_replay_warp<false, 0>;
+}
+
 // ------------------------------------------------------------------ fs_wsc_replay
 extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
                              const fs_replay_out* out, fs_replay_summary* sum) {
+  FS_NVTX("fs_wsc_replay");
   if (!ctx || !tr || !P || !sum || !replay_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
   memset(sum, 0, sizeof(*sum));
   if (P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
@@ -417,7 +438,8 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
     if (S.failed) return FS_E_NOMEM;
     ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
     const bool base = cfg->mode >= FS_MODE_VTC || ag;
-    auto rk = rwarp ? (base ? k_replay_warp<true> : k_replay_warp<false>) : (base ? k_replay<true> : k_replay<false>);
+    const int tour = base || cfg->max_batch > 1024 ? 0 : tour_bits(6);   // warp-parallel engine pieces
+    ReplayFn rk = rwarp ? (base ? k_replay_warp<true, 0> : replay_warp_kern_t(tour)) : (base ? k_replay<true> : k_replay<false>);
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
     FS_LAUNCH(ctx, "wsc_replay", rk, 1, rwarp ? 32 : 64, L.bytes_smem, a);
     cudaMemcpyAsync(&hcode, dcode, 4, cudaMemcpyDeviceToHost, ctx->stream);
@@ -438,6 +460,7 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
 // ------------------------------------------------------------------ fs_sweep
 extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* scen, uint32_t ns,
                         fs_replay_summary* out, int32_t* codes) {
+  FS_NVTX("fs_sweep");
   if (!ctx || !tr || !P || !scen || !out || !codes || tr->n_apps == 0) return FS_E_INVAL;
   if (ns == 0) return FS_OK;
   bool any_wi = false, any_dq = false, any_rpm = false, any_ag = false;
@@ -531,11 +554,10 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   // scenarios of the FairServe modes only: the engine without the baseline-mode paths
   // (FS_SWEEP_LPS = 16 / 8, several replays per warp, measured slower: FS-mode engine only)
   const bool base = any_dq || any_ag;
-  auto kern = base ? (minb >= 6 ? k_sweep<6, 32, true> : minb == 5 ? k_sweep<5, 32, true> :
-                        minb == 4 ? k_sweep<4, 32, true> : k_sweep<3, 32, true>)
-            : lps <= 8 ? k_sweep<4, 8, false> : lps == 16 ? k_sweep<4, 16, false>
-            : (minb >= 6 ? k_sweep<6, 32, false> : minb == 5 ? k_sweep<5, 32, false> :
-               minb == 4 ? k_sweep<4, 32, false> : k_sweep<3, 32, false>);
+  const int tour = base || lps < 32 || Bmax > 1024 ? 0 : tour_bits(0);   // warp-parallel engine pieces
+  SweepFn kern = base ? (minb >= 6 ? k_sweep<6, 32, true, 0> : minb == 5 ? k_sweep<5, 32, true, 0> :
+                           minb == 4 ? k_sweep<4, 32, true, 0> : k_sweep<3, 32, true, 0>)
+               : lps <= 8 ? k_sweep<4, 8, false, 0> : lps == 16 ? k_sweep<4, 16, false, 0> : sweep_kern_t(tour, minb);
   const u32 per_cta = base ? 4 : 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
   // the replays' state lives in global memory: give L1 every byte shared memory does not need
   static const int carve = [] { const char* v = getenv("FS_SWEEP_CARVE"); return v ? atoi(v) : -1; }();
@@ -567,8 +589,48 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next, dord};
   FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / per_cta), 128, 0, a);
   std::vector<int> hcodes(ns);
-  cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);
   cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);
+  rc = finish(ctx, &S);
+  if (rc) return rc;
+  // scenarios that outgrew a capacity (ACT ring per user, pending heap, continuation pool, window
+  // logs) run again with exact capacities: every user's continuation count, every interaction,
+  // every call -- so the sweep fails only where the oracle does
+  std::vector<u32> retry;
+  for (u32 q = 0; q < ns; q++)
+    if (hcodes[ord[q]] && hcodes[ord[q]] - 1 == ERR_NOMEM) retry.push_back(ord[q]);
+  if (!retry.empty()) {
+    const u32 nr = (u32)retry.size();
+    u64* ncont = S.zeros<u64>(t.U + 1);
+    u64* roff = S.alloc<u64>(t.U + 1);
+    u32* ut = S.alloc<u32>(t.U + 1);
+    u64* tc = S.zeros<u64>(256);
+    u32* dr = S.alloc<u32>(nr);
+    u32* next2 = S.zeros<u32>(1);
+    if (S.failed) return FS_E_NOMEM;
+    if (t.n) FS_LAUNCH(ctx, "user_stats", k_user_stats, div_up(t.n, 256), 256, 0, t, ut, (unsigned long long*)tc, ncont);
+    excl_scan<u64>(ctx, S, ncont, roff, t.U, roff + t.U);
+    u64 ring2 = 0;
+    cudaMemcpyAsync(&ring2, roff + t.U, 8, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaMemcpyAsync(dr, retry.data(), nr * 4, cudaMemcpyHostToDevice, ctx->stream);
+    rc = finish(ctx, &S);
+    if (rc) return rc;
+    const u32 p2 = std::max<u32>(t.X, 1), all = (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull);
+    EngLayout L2 = eng_layout(t.U, p2, W.n_heads, Bmax, p2, AJ, any_wi, ring2, false, 0, any_dq, any_rpm ? all : 0, t.A,
+                              any_ag ? all : 0);
+    const size_t sb2 = (L2.bytes_glob + 255) / 256 * 256;
+    cudaMemGetInfo(&free_b, &total_b);
+    u64 sl2 = std::min<u64>(std::min<u64>(nr, slots), (u64)(free_b / 2) / std::max<size_t>(sb2, 1));
+    if (sl2 == 0) return FS_E_NOMEM;
+    sl2 = (sl2 + per_cta - 1) / per_cta * per_cta;
+    unsigned char* gm2 = S.alloc<unsigned char>(sl2 * sb2 + 256);
+    if (S.failed) return FS_E_NOMEM;
+    EngShared sh2 = W.sh;
+    sh2.r_off = roff;
+    SweepKArgs a2{sh2, dc, nr, L2, t.U, gm2, sb2, p2, dsum, dcodes, next2, dr};
+    FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(sl2 / per_cta), 128, 0, a2);
+    cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);
+  }
+  cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);
   rc = finish(ctx, &S);
   if (rc) return rc;
   for (u32 s = 0; s < ns; s++) {
@@ -606,6 +668,7 @@ __global__ void k_step_init(EngLayout L, unsigned char* gm, u32 p_cap, EngShared
 
 extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_replay_cfg* cfg,
                                    fs_wsc_state** out) {
+  FS_NVTX("fs_wsc_state_create");
   if (!ctx || !tr || !P || !out || !replay_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
   if (cfg->mode == FS_MODE_RPM) return FS_E_INVAL;         // RPM needs the replay's time order (R8)
   if (cfg->mode == FS_MODE_WI && cfg->act.app_scope == FS_SCOPE_APP_GLOBAL) return FS_E_INVAL;   // R10
@@ -661,6 +724,7 @@ extern "C" int fs_wsc_state_create(fs_ctx* ctx, const fs_trace* tr, const fs_pro
 extern "C" int fs_wsc_step(fs_ctx* ctx, fs_wsc_state* st, int64_t now_ns, int64_t occ, uint32_t batch,
                            const uint32_t* fin, uint32_t nfin, const uint32_t* arr, const int64_t* arr_t, uint32_t narr,
                            uint8_t* arr_status, uint32_t* admitted, uint32_t* n_admitted) {
+  FS_NVTX("fs_wsc_step");
   (void)now_ns;
   if (!ctx || !st || !n_admitted || (nfin && !fin) || (narr && (!arr || !arr_t || !arr_status)) || !admitted)
     return FS_E_INVAL;

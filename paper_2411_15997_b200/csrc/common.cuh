@@ -8,6 +8,14 @@
 #include <vector>
 
 #include "../../include/fairserve.h"
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range over one C-ABI call (header-only NVTX v3: free unless a profiler is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define FS_NVTX(NAME) NvtxRange _fs_nvtx_range(NAME)
 
 typedef uint64_t u64;
 typedef int64_t i64;

@@ -188,13 +188,75 @@ static void prof_limits(fs_profile_partial* pp) {
   size_t smem = (size_t)NS * 256 * 4;
   const int priv = smem + 1024 <= ctx->smem_optin;     // block-private histograms when they fit
   if (!priv) smem = 0;
-  else cudaFuncSetAttribute(k_lim_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  else cudaFuncSetAttribute(k_lim_hist<u32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int d = top; d >= 0 && tot; d--) {
-    FS_LAUNCH(ctx, "lim_hist", k_lim_hist, grid, 256, smem, la, d, top, priv);
-    FS_LAUNCH(ctx, "lim_select", k_lim_select, div_up(NS, 4), 128, 0, la);
+    FS_LAUNCH(ctx, "lim_hist", k_lim_hist<u32>, grid, 256, smem, la, hist, d, top, priv);
+    FS_LAUNCH(ctx, "lim_select", k_lim_select<u32>, div_up(NS, 4), 128, 0, la, hist);
   }
   FS_LAUNCH(ctx, "lim_final", k_lim_final, div_up(NS, 128), 128, 0, la, P->nr_peak_r_a, P->nr_peak_t_a,
             P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g, P->T_tok_g);
+}
+
+// Multi-GPU limits: the same radix select over the ranks' disjoint users without gathering their
+// peaks -- the SUM all-reduce rounds carry each set's present count and a bit-length histogram
+// (NS + 65 words), then one digit's 256-bin histograms per set (NS x 256 words = 143 KB at A = 34);
+// every rank selects the same digits, so every rank finalises identical limits.
+static LimArgs lim_args(fs_profile_partial* pp) {
+  fs_profile* P = pp->P;
+  return LimArgs{P->A, pp->t.U, pp->cfg.limit_q_ppm, pp->cfg.limit_mult_q8, P->peak_r_u, P->peak_t_u, P->peak_r_ua,
+                 P->peak_t_ua, pp->lim_sel, nullptr};
+}
+static int lim_grid(fs_profile_partial* pp) {
+  const u64 tot = (u64)pp->t.U * pp->P->A + pp->t.U;
+  return (int)std::max<u64>(1, std::min<u64>(div_up(tot ? tot : 1, 256), (u64)pp->ctx->sm_count * 4));
+}
+static u64 lim_dist_send(fs_profile_partial* pp, u64* buf, u64 off) {      // this round's limit words
+  fs_ctx* ctx = pp->ctx;
+  fs_profile* P = pp->P;
+  const u32 NS = 2 * (P->A + 1);
+  LimArgs la = lim_args(pp);
+  unsigned long long* w = (unsigned long long*)(buf + off);
+  pp->lim_off = off;
+  if (pp->lim_stage == 0) {
+    cudaMemsetAsync(w, 0, (size_t)(NS + 65) * 8, ctx->stream);
+    if (pp->t.U) FS_LAUNCH(ctx, "lim_count", k_lim_count_words, lim_grid(pp), 256, 0, la, w);
+    pp->lim_stage = 1;
+    return NS + 65;
+  }
+  if (pp->lim_d < 0 || pp->t.U == 0) {
+    FS_LAUNCH(ctx, "lim_final", k_lim_final, div_up(NS, 128), 128, 0, la, P->nr_peak_r_a, P->nr_peak_t_a,
+              P->nr_peak_r_g, P->nr_peak_t_g, P->T_req_a, P->T_tok_a, P->T_req_g, P->T_tok_g);
+    pp->peaks_done = true;
+    return 0;
+  }
+  size_t smem = (size_t)NS * 256 * 4;
+  const int priv = smem + 1024 <= ctx->smem_optin;
+  if (!priv) smem = 0;
+  else cudaFuncSetAttribute(k_lim_hist<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaMemsetAsync(w, 0, (size_t)NS * 256 * 8, ctx->stream);
+  FS_LAUNCH(ctx, "lim_hist", k_lim_hist<unsigned long long>, lim_grid(pp), 256, smem, la, w, pp->lim_d, pp->lim_top, priv);
+  pp->lim_stage = 2;
+  return (u64)NS * 256;
+}
+static void lim_dist_recv(fs_profile_partial* pp, u64* buf) {             // the reduced limit words
+  fs_ctx* ctx = pp->ctx;
+  const u32 NS = 2 * (pp->P->A + 1);
+  LimArgs la = lim_args(pp);
+  unsigned long long* w = (unsigned long long*)(buf + pp->lim_off);
+  if (pp->lim_stage == 1) {
+    FS_LAUNCH(ctx, "lim_init", k_lim_init_words, div_up(NS, 128), 128, 0, la, w);
+    FS_LAUNCH(ctx, "lim_init", k_lim_init, div_up(NS, 128), 128, 0, la);
+    unsigned long long bl[65];
+    cudaMemcpyAsync(bl, w + NS, sizeof(bl), cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    int mb = 0;
+    for (int b = 0; b < 65; b++) if (bl[b]) mb = b;
+    pp->lim_top = std::max(0, (mb + 7) / 8 - 1);
+    pp->lim_d = pp->lim_top;
+  } else {
+    FS_LAUNCH(ctx, "lim_select", k_lim_select<unsigned long long>, div_up(NS, 4), 128, 0, la, w);
+    pp->lim_d--;
+  }
 }
 
 // K5: window peaks of the user order (profile.cuh), after round 0 fixed O-hat: parallel pieces
@@ -233,17 +295,9 @@ static void prof_windows(fs_profile_partial* pp) {
   FS_LAUNCH(ctx, "useg_win", k_useg_win, div_up(nover, SW_T / 32), SW_T, smem, a);
 }
 
-__global__ void k_pack_u32_u64(const u32* a, u64* b, u64 n) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) b[i] = a[i];
-}
-__global__ void k_unpack_u64_u32(const u64* a, u32* b, u64 n) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) b[i] = (u32)a[i];
-}
-
 extern "C" int fs_profile_local(fs_ctx* ctx, const fs_trace* tr, const fs_profile_cfg* cfg,
                                 fs_profile_partial** out, size_t* comm_words) {
+  FS_NVTX("fs_profile_local");
   if (!ctx || !tr || !out || !comm_words || !prof_cfg_ok(cfg) || tr->n_apps == 0 || tr->n_apps > 255)
     return FS_E_INVAL;
   if (tr->n_calls && (!tr->user || !tr->t_ms || !tr->len_in || !tr->len_sys || !tr->len_out || !tr->meta ||
@@ -287,7 +341,7 @@ extern "C" int fs_profile_local(fs_ctx* ctx, const fs_trace* tr, const fs_profil
   if (rc) { fs_profile_free(pp->P); delete pp; return rc; }
   size_t r0 = prof_r0_words(A, J);
   size_t h2max = (size_t)A * 4 * 3 * nq * (1u << QW);
-  size_t r1 = h2max + 2 * (size_t)U + 2 * (size_t)U * A;
+  size_t r1 = h2max + (size_t)2 * (A + 1) * 256;           // + the largest limit payload (digit histograms)
   pp->comm_words = std::max(r0, r1);
   *comm_words = pp->comm_words;
   *out = pp;
@@ -314,6 +368,7 @@ static u64 prof_q_next(fs_profile_partial* pp, u64* buf) {
 }
 
 extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* words, int* done) {
+  FS_NVTX("fs_profile_round");
   if (!pp || !buf || !words || !done) return FS_E_INVAL;
   fs_ctx* ctx = pp->ctx;
   fs_profile* P = pp->P;
@@ -344,39 +399,28 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
     cudaMemsetAsync(P->peak_r_ua, 0, (u64)U * A * 4, ctx->stream);
     cudaMemsetAsync(P->peak_t_ua, 0, (u64)U * A * 8, ctx->stream);
     prof_windows(pp);
+    if (pp->single) { prof_limits(pp); pp->peaks_done = true; }   // one rank: its peaks are all peaks
+    else pp->lim_sel = S.zeros<LimSel>(2 * (A + 1));
     u64 w = prof_q_next(pp, buf);
-    u64* pk = buf + w;
-    if (U) {
-      FS_LAUNCH(ctx, "pack", k_pack_u32_u64, div_up(U, B), B, 0, P->peak_r_u, pk, (u64)U);
-      cudaMemcpyAsync(pk + U, P->peak_t_u, U * 8, cudaMemcpyDeviceToDevice, ctx->stream);
-      FS_LAUNCH(ctx, "pack", k_pack_u32_u64, div_up((u64)U * A, B), B, 0, P->peak_r_ua, pk + 2 * U, (u64)U * A);
-      cudaMemcpyAsync(pk + 2 * U + (u64)U * A, P->peak_t_ua, (u64)U * A * 8, cudaMemcpyDeviceToDevice, ctx->stream);
-    }
-    *words = w + 2 * (u64)U + 2 * (u64)U * A;
-  } else {                                                // resolve previous level (+ peaks after R1)
+    if (!pp->peaks_done) w += lim_dist_send(pp, buf, w);
+    *words = w;
+    if (w == 0 && pp->peaks_done) *done = 1;
+  } else {                                                // resolve previous level (+ limit digits)
     if (pp->h2_words)
       FS_LAUNCH(ctx, "q_resolve", k_q_resolve, div_up((u64)A * 4 * 3 * P->nq, 128), 128, 0, A, P->nq, pp->qst,
                 pp->qiv, pp->qniv, buf);
-    if (!pp->peaks_done) {
-      u64* pk = buf + pp->h2_words;
-      if (U) {
-        FS_LAUNCH(ctx, "unpack", k_unpack_u64_u32, div_up(U, B), B, 0, pk, P->peak_r_u, (u64)U);
-        cudaMemcpyAsync(P->peak_t_u, pk + U, U * 8, cudaMemcpyDeviceToDevice, ctx->stream);
-        FS_LAUNCH(ctx, "unpack", k_unpack_u64_u32, div_up((u64)U * A, B), B, 0, pk + 2 * U, P->peak_r_ua, (u64)U * A);
-        cudaMemcpyAsync(P->peak_t_ua, pk + 2 * U + (u64)U * A, (u64)U * A * 8, cudaMemcpyDeviceToDevice, ctx->stream);
-      }
-      prof_limits(pp);
-      pp->peaks_done = true;
-    }
+    if (!pp->peaks_done) lim_dist_recv(pp, buf);
     u64 w = prof_q_next(pp, buf);
+    if (!pp->peaks_done) w += lim_dist_send(pp, buf, w);
     *words = w;
-    if (w == 0) *done = 1;
+    if (w == 0 && pp->peaks_done) *done = 1;
   }
   pp->round++;
   return finish(ctx, &S);
 }
 
 extern "C" int fs_profile_finalize(fs_profile_partial* pp, fs_profile** out) {
+  FS_NVTX("fs_profile_finalize");
   if (!pp || !out) return FS_E_INVAL;
   if (!pp->peaks_done) return FS_E_PROTOCOL;
   fs_ctx* ctx = pp->ctx;
@@ -400,6 +444,7 @@ extern "C" void fs_profile_partial_free(fs_profile_partial* pp) {
 }
 
 extern "C" int fs_build_app_profiles(fs_ctx* ctx, const fs_trace* tr, const fs_profile_cfg* cfg, fs_profile** out) {
+  FS_NVTX("fs_build_app_profiles");
   fs_profile_partial* pp = nullptr;
   size_t words = 0;
   int rc = fs_profile_local(ctx, tr, cfg, &pp, &words);
@@ -407,6 +452,7 @@ extern "C" int fs_build_app_profiles(fs_ctx* ctx, const fs_trace* tr, const fs_p
   const DevAlloc da = ctx_devalloc(ctx);
   u64* buf = (u64*)ctx_malloc(ctx, words * 8 + 8);
   if (!buf) { fs_profile_partial_free(pp); return FS_E_NOMEM; }
+  pp->single = true;
   int done = 0;
   for (int r = 0; r < 8 && !done; r++) {        // one rank: the "reduced" payload is our own
     size_t w = 0;
@@ -502,22 +548,29 @@ static bool act_limits(fs_ctx* ctx, Scratch& S, const fs_profile* P, const fs_ac
 }
 
 // (user[, app], t_ns, id) order of all calls; never-arrived calls sort last in their segment
-static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, int kind, i64 W, ActOrder* ao) {
+// calls in (arrival ns, id) order when arrival times are given (never arrived: last): one 64-bit
+// radix sort shared by both orders
+static bool act_time_perm(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, u32** permt) {
+  u64 n = t.n;
+  int B = 256;
+  unsigned long long* mx = S.zeros<unsigned long long>(1);
+  u64* tk = S.alloc<u64>(n);
+  if (S.failed) return false;
+  FS_LAUNCH(ctx, "act_tmax", k_act_tmax, div_up(n, B), B, 0, n, tov, mx);
+  FS_LAUNCH(ctx, "act_tkeys", k_act_tkeys, div_up(n, B), B, 0, n, tov, mx, tk);
+  unsigned long long hmx = 0;
+  cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  u64* tks;
+  return radix_sort<u64>(ctx, S, tk, nullptr, n, bits_for(hmx + 1), &tks, permt);
+}
+static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, const u32* permt, int kind, i64 W,
+                      ActOrder* ao) {
   u64 n = t.n;
   int B = 256;
   if (!tov) {
     if (!build_order(ctx, S, t, kind, &ao->o)) return false;
   } else {
-    unsigned long long* mx = S.zeros<unsigned long long>(1);
-    u64* tk = S.alloc<u64>(n);
-    if (S.failed) return false;
-    FS_LAUNCH(ctx, "act_tmax", k_act_tmax, div_up(n, B), B, 0, n, tov, mx);
-    FS_LAUNCH(ctx, "act_tkeys", k_act_tkeys, div_up(n, B), B, 0, n, tov, mx, tk);
-    unsigned long long hmx = 0;
-    cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream);
-    cudaStreamSynchronize(ctx->stream);
-    u64* tks; u32* permt;
-    if (!radix_sort<u64>(ctx, S, tk, nullptr, n, bits_for(hmx + 1), &tks, &permt)) return false;
     u32* k2 = S.alloc<u32>(n);
     if (S.failed) return false;
     FS_LAUNCH(ctx, "gather_key", k_gather_key, div_up(n, B), B, 0, n, permt, t, (u32)kind, k2);
@@ -539,6 +592,7 @@ static bool act_order(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* tov, 
 
 extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, const fs_act_cfg* cfg,
                                const uint8_t* overloaded, const int64_t* tov, uint8_t* status, fs_act_summary* sum) {
+  FS_NVTX("fs_act_throttle");
   if (!ctx || !tr || (!status && tr->n_calls) || !sum || !act_cfg_ok(cfg) || tr->n_apps == 0) return FS_E_INVAL;
   memset(sum, 0, sizeof(*sum));
   if (P && P->A != tr->n_apps) { ctx->bad_index = 0; return FS_E_PROFILE; }
@@ -569,7 +623,10 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
   ActOrder ou, oua;
   // second order: per (user, app), or per app with app-global counters (R10)
   const bool app_global = cfg->app_scope == FS_SCOPE_APP_GLOBAL;
-  if (!act_order(ctx, S, t, tov, 0, W, &ou) || !act_order(ctx, S, t, tov, app_global ? 2 : 1, W, &oua)) return FS_E_NOMEM;
+  u32* permt = nullptr;
+  if (tov && !act_time_perm(ctx, S, t, tov, &permt)) return FS_E_NOMEM;
+  if (!act_order(ctx, S, t, tov, permt, 0, W, &ou) || !act_order(ctx, S, t, tov, permt, app_global ? 2 : 1, W, &oua))
+    return FS_E_NOMEM;
   const u32 heads_only = cfg->count_mode == FS_COUNT_HEADS_ONLY;
   uint2* apk = S.alloc<uint2>(n);
   if (S.failed) return FS_E_NOMEM;

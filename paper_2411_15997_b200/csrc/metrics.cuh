@@ -173,6 +173,7 @@ __global__ void k_met_ranks(u32 A, int bits, const u64* kapp, const u64* kall, c
 extern "C" int fs_replay_metrics(fs_ctx* ctx, const fs_trace* tr, const uint8_t* status, const int64_t* arrive_ns,
                                  const int64_t* admit_ns, const int64_t* first_ns, int64_t delay_threshold_ns,
                                  fs_metrics* global_h, fs_metrics* per_app_h) {
+  FS_NVTX("fs_replay_metrics");
   if (!ctx || !tr || !global_h || tr->n_apps == 0 || (tr->n_calls && (!status || !arrive_ns || !admit_ns || !first_ns)))
     return FS_E_INVAL;
   memset(global_h, 0, sizeof(*global_h));

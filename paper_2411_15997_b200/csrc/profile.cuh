@@ -799,10 +799,12 @@ __global__ void k_lim_init(LimArgs a) {
   l.krank = k ? k - 1 : 0;
   l.prefix = 0;
 }
-__global__ void k_lim_hist(LimArgs a, int d, int top, int priv) {
+// H = u32 (one rank: the profile's own histogram) or unsigned long long (multi-GPU: the words of
+// the round's SUM all-reduce buffer)
+template <class H>
+__global__ void k_lim_hist(LimArgs a, H* hist, int d, int top, int priv) {
   extern __shared__ u32 lh[];                  // [2 (A + 1)][256] when priv (else global atomics)
   const u32 NS = 2 * (a.A + 1);
-  u32* hh = priv ? lh : a.hist;
   if (priv) for (u32 k = threadIdx.x; k < NS * 256; k += blockDim.x) lh[k] = 0;
   __syncthreads();
   const u64 tot = (u64)a.U * a.A + a.U;
@@ -815,20 +817,22 @@ __global__ void k_lim_hist(LimArgs a, int d, int top, int priv) {
       u32 s = mt * (a.A + 1) + st;
       u64 v = mt ? vt : vr;
       if (d < top && (v >> (sh + 8)) != a.sel[s].prefix) continue;
-      atomicAdd(&hh[s * 256 + ((v >> sh) & 255)], 1u);
+      if (priv) atomicAdd(&lh[s * 256 + ((v >> sh) & 255)], 1u);
+      else atomicAdd(&hist[s * 256 + ((v >> sh) & 255)], (H)1);
     }
   }
   __syncthreads();
   if (priv)
     for (u32 k = threadIdx.x; k < NS * 256; k += blockDim.x)
-      if (lh[k]) atomicAdd(&a.hist[k], lh[k]);
+      if (lh[k]) atomicAdd(&hist[k], (H)lh[k]);
 }
-__global__ void k_lim_select(LimArgs a) {      // one warp per (metric, set): the digit holding krank
+template <class H>
+__global__ void k_lim_select(LimArgs a, H* hist) {      // one warp per (metric, set): the digit holding krank
   u32 s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (s >= 2 * (a.A + 1)) return;
   LimSel& l = a.sel[s];
-  u32* h = a.hist + (u64)s * 256;
-  u32 c[8]; u64 loc = 0;
+  H* h = hist + (u64)s * 256;
+  u64 c[8]; u64 loc = 0;
 #pragma unroll
   for (int k = 0; k < 8; k++) { c[k] = h[lane * 8 + k]; loc += c[k]; }
   u64 inc = loc;
@@ -846,6 +850,35 @@ __global__ void k_lim_select(LimArgs a) {      // one warp per (metric, set): th
   (void)who;
   __syncwarp();
   for (int k = 0; k < 8; k++) h[lane * 8 + k] = 0;             // ready for the next digit
+}
+// multi-GPU limits: the rank's share of the per-set present counts (words [0, NS)) and a histogram
+// of bit lengths of every present peak (words [NS, NS + 65)): summed over ranks they give each
+// set's rank and the first digit
+__global__ void k_lim_count_words(LimArgs a, unsigned long long* w) {
+  __shared__ unsigned long long cn[256], bl[65];
+  for (u32 k = threadIdx.x; k <= a.A; k += blockDim.x) cn[k] = 0;
+  for (u32 k = threadIdx.x; k < 65; k += blockDim.x) bl[k] = 0;
+  __syncthreads();
+  const u64 tot = (u64)a.U * a.A + a.U;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (u64)gridDim.x * blockDim.x) {
+    u32 st; bool pr; u64 vr, vt;
+    lim_item(a, i, &st, &pr, &vr, &vt);
+    if (!pr) continue;
+    atomicAdd(&cn[st], 1ull);
+    atomicAdd(&bl[64 - __clzll((long long)vr)], 1ull);
+    atomicAdd(&bl[64 - __clzll((long long)vt)], 1ull);
+  }
+  __syncthreads();
+  const u32 NS = 2 * (a.A + 1);
+  for (u32 k = threadIdx.x; k <= a.A; k += blockDim.x)
+    if (cn[k]) { atomicAdd(&w[k], cn[k]); atomicAdd(&w[a.A + 1 + k], cn[k]); }
+  for (u32 k = threadIdx.x; k < 65; k += blockDim.x)
+    if (bl[k]) atomicAdd(&w[NS + k], bl[k]);
+}
+__global__ void k_lim_init_words(LimArgs a, const unsigned long long* w) {   // global counts -> ranks
+  u32 s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= 2 * (a.A + 1)) return;
+  a.sel[s].n = w[s];
 }
 __global__ void k_lim_final(LimArgs a, u32* nr_r_a, u64* nr_t_a, u32* nr_r_g, u64* nr_t_g, u32* T_r_a, u64* T_t_a,
                             u32* T_r_g, u64* T_t_g) {
@@ -882,6 +915,11 @@ struct fs_profile_partial {
   u64 h2_words = 0;
   size_t comm_words = 0;
   bool peaks_done = false;
+  bool single = false;           // fs_build_app_profiles: one rank, limits selected from its own peaks
+  // multi-GPU limits: stage 1 = set counts + bit lengths in flight, 2 = digit lim_d's histograms
+  int lim_stage = 0, lim_d = 0, lim_top = 0;
+  u64 lim_off = 0;               // where this round's limit words sit in the buffer
+  LimSel* lim_sel = nullptr;
   ~fs_profile_partial() { delete S; }
 };
 

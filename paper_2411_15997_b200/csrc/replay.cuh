@@ -76,6 +76,7 @@ struct RPEnt { i64 t; u32 user, app; }; // RPM window log entry (16 B)
 struct AGEnt { i64 t; u32 app, tau; };  // app-global window log entry (16 B)
 struct AGSum { u64 tau; u32 n, pad; };  // live logged calls of one app (all users)
 struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
+struct alignas(16) BKey { u64 fi; u32 r, pad; };      // warp batch: finish iteration and call of a B slot
 
 struct EngState {
   UState* us; HK* hk; HM* hm;
@@ -90,6 +91,7 @@ struct EngState {
   RPEnt* rf; u32 rf_cap; u32* rapp;     // RPM: window log of every arrival (FIFO), live arrivals per app
   AGEnt* ag; u32 ag_cap; AGSum* ags;    // app-global FS(W+I): window log of logged calls, per-app sums
   u64* W;                               // stage weights (smem copy or the scenario's table)
+  BKey* bk; u32* bfree; u32 b_cap;     // lane-owned batch slots: [Bmax] slot keys, free-slot stack (TB engines)
 };
 
 struct EngOut {                         // optional per-call outputs (single replay only)
@@ -112,8 +114,16 @@ enum { HS_DIRECT = 0,                   // heads read one at a time (online step
                                         // batch of the next 32 participating heads together (sweep)
 // HS_WARP with LPS < 32: the warp runs 32 / LPS independent scenarios, each on its own
 // group of LPS lanes (groups diverge freely; a group stays in lockstep)
-template <int HS, int LPS = 32, bool BASE = true>   // BASE: the NEXT-1 baseline modes compiled in
+// TOUR (HS_WARP, 32 lanes, FairServe modes): engine pieces the 32 lockstep lanes run in parallel
+// (DESIGN.md "Warp-parallel pieces"): bit 2 (TB) -- B slots are owned by lane (slot mod 32), each
+// lane keeping the minimum finish iteration of its slots, so the next finish is a warp min and a
+// finish batch is found by the lanes holding it (no 48-B heap sifts); bit 4 (TA) -- the lanes split
+// the ACT continuation ring of a user (expiry by ballot, counts by redux).  (Bit 1, a 32-group
+// warp tournament in place of the pick heaps, measured 40 % slower on the C5 sweep and was removed.)
+template <int HS, int LPS = 32, bool BASE = true, int TOUR = 0>   // BASE: the NEXT-1 baseline modes compiled in
 struct EngineT {
+  static_assert(!TOUR || (HS == HS_WARP && LPS == 32 && !BASE), "warp tournament: FairServe modes on a full warp");
+  static constexpr bool TB = (TOUR & 2) != 0, TA = (TOUR & 4) != 0;
   static constexpr bool RING = HS == HS_RING;
   const EngShared* sh;
   const EngCfg* c;
@@ -137,6 +147,16 @@ struct EngineT {
   u64 digest, n_adm;
   fs_replay_summary sum;
   int err_code; u64 err_idx;
+  // TB: this lane's B slots {lane + 32 j}
+  u64 lfi; u32 locc;                     // minimum finish iteration of the lane's slots, occupied slots
+  u32 bf_top;                            // free B-slot stack
+  __device__ __forceinline__ static u64 mn64(u64 a, u64 b) { return a < b ? a : b; }
+  __device__ __forceinline__ static u64 warp_min64(u64 v) {
+    const u32 hi = (u32)(v >> 32);
+    const u32 m1 = __reduce_min_sync(FULL_MASK, hi);
+    const u32 m2 = __reduce_min_sync(FULL_MASK, hi == m1 ? (u32)v : NONE32);
+    return ((u64)m1 << 32) | m2;
+  }
 
   // ---------------------------------------------------------------- heaps with inline keys
   __device__ __forceinline__ static bool kl(const HK& a, const HK& b) { return a.key < b.key || (a.key == b.key && a.tie < b.tie); }
@@ -198,6 +218,7 @@ struct EngineT {
     hb_i = hb_n = 0; rf_head = rf_len = 0; ag_head = ag_len = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
+    lfi = ~0ull; locc = 0; bf_top = st.b_cap;
   }
 
   // ---------------------------------------------------------------- Eq. 3 (l.44-48)
@@ -249,7 +270,34 @@ struct EngineT {
 
   // ---------------------------------------------------------------- ACT window check (l.19-24)
   __device__ __forceinline__ int act_check(UState& us, u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
-    if (!c->heads_only || !static_heads) {
+    if (TA && !c->heads_only) {                          // the lanes split the ring
+      const u64 base = sh->r_off[k]; const u32 cap = (u32)(sh->r_off[k + 1] - base);
+      const u32 lane = threadIdx.x & 31;
+      const i64 lim = tr - c->Wns;
+      u32 h = us.r_head, len = us.r_len;
+      while (len) {                                        // expired prefix (t <= tr - W, Q4), 32 at a time
+        bool ex = false;
+        if (lane < len) { u32 idx = h + lane; if (idx >= cap) idx -= cap; ex = s.r[base + idx].t <= lim; }
+        const u32 m = __ballot_sync(FULL_MASK, ex);
+        const u32 nx = m == FULL_MASK ? 32u : (u32)__ffs(~m) - 1;
+        h += nx; if (h >= cap) h -= cap;
+        len -= nx;
+        if (nx < 32) break;
+      }
+      us.r_head = h; us.r_len = len;
+      u32 cn = 0, ca = 0; u64 ct = 0, cta = 0;
+      for (u32 q = lane; q < len; q += 32) {
+        u32 idx = h + q; if (idx >= cap) idx -= cap;
+        const REnt re = s.r[base + idx];
+        cn++; ct += re.tau;
+        if (re.app == app) { ca++; cta += re.tau; }
+      }
+      if (len) {
+        n_g += __reduce_add_sync(FULL_MASK, cn); n_a += __reduce_add_sync(FULL_MASK, ca);
+        for (int o = 16; o; o >>= 1) { ct += __shfl_xor_sync(FULL_MASK, ct, o); cta += __shfl_xor_sync(FULL_MASK, cta, o); }
+        t_g += ct; t_a += cta;
+      }
+    } else if (!c->heads_only || !static_heads) {
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
       u32 h = us.r_head, len = us.r_len;
       while (len && s.r[base + h].t <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // (Q4)
@@ -617,6 +665,16 @@ struct EngineT {
   // B heap keyed (finish iteration, id)
   __device__ __forceinline__ static bool bless(const BEnt& a, const BEnt& b) { return a.fi < b.fi || (a.fi == b.fi && a.r < b.r); }
   __device__ __forceinline__ void b_push(const BEnt& x) {
+    if (TB) {                                            // a free slot; its lane's minimum, bfi
+      const u32 sl = s.bfree[--bf_top];
+      s.b[sl] = x;
+      BKey kk; kk.fi = x.fi; kk.r = x.r; kk.pad = 0;
+      s.bk[sl] = kk;
+      if ((threadIdx.x & 31) == (sl & 31)) { locc |= 1u << (sl >> 5); lfi = mn64(lfi, x.fi); }
+      bfi = b_n == 0 ? x.fi : mn64(bfi, x.fi);
+      b_n++;
+      return;
+    }
     u32 i = b_n++;
     while (i > 0) {
       u32 pi = (i - 1) >> 1;
@@ -728,7 +786,7 @@ struct EngineT {
           n_adm++;
         }
         pick_blocked = true;
-        if (nl_n) bfi = s.b[0].fi;
+        if (!TB && nl_n) bfi = s.b[0].fi;
       }
       if (b_n == 0) continue;
       u64 d = dB + pre * P_new;                                   // 4: iteration(s)
@@ -745,7 +803,46 @@ struct EngineT {
       occ += (i64)(m * b_n);
       sum.sum_ttft_ns += (u64)nl_n * (u64)clock - arr_sum;       // sum of (first token - arrival), mod 2^64
       if (o.first) for (u32 q = 0; q < nl_n; q++) o.first[s.nl_id[q]] = clock;
-      if (bfi == iter - 1) {                                      // finishes (l.43-48)
+      if (TB && bfi == iter - 1) {                              // finishes (l.43-48), warp batch
+        bool pushed = false;
+        const u64 fin = iter - 1;
+        const u32 lane = threadIdx.x & 31;
+        u32 fm = 0;                                               // the lane's finishing slots
+        if (lfi == fin)
+          for (u32 mm = locc; mm; mm &= mm - 1) { const u32 j = __ffs(mm) - 1; if (s.bk[lane + 32 * j].fi == fin) fm |= 1u << j; }
+        for (;;) {                                                // in call order (the oracle sorts them)
+          u32 myr = NONE32, mys = 0;
+          for (u32 mm = fm; mm; mm &= mm - 1) {
+            const u32 sl = lane + 32 * (__ffs(mm) - 1), rr = s.bk[sl].r;
+            if (rr < myr) { myr = rr; mys = sl; }
+          }
+          const u32 mr = __reduce_min_sync(FULL_MASK, myr);
+          if (mr == NONE32) break;
+          const u32 w = __ffs(__ballot_sync(FULL_MASK, myr == mr)) - 1;
+          const u32 sl = __shfl_sync(FULL_MASK, mys, w);
+          if (lane == w) { fm &= ~(1u << (sl >> 5)); locc &= ~(1u << (sl >> 5)); }
+          const BEnt f = s.b[sl];
+          s.bfree[bf_top++] = sl;
+          b_n--;
+          dB -= dec;
+          if (o.finish) o.finish[f.r] = clock;
+          occ -= (i64)f.rel;
+          if (!charge(f.user, f.inc, f.r)) return;
+          if (m_stage(f.meta) < m_ncalls(f.meta)) {
+            PEnt pe; pe.t = clock + (i64)f.think * 1000000; pe.r = f.link; pe.user = f.user;
+            pe.meta = f.meta + (1u << 8); pe.pad = 0;
+            if (!p_push(pe)) return;
+            pushed = true;
+          }
+        }
+        if (lfi == fin) {                                         // the finishing lanes' new minima
+          lfi = ~0ull;
+          for (u32 mm = locc; mm; mm &= mm - 1) lfi = mn64(lfi, s.bk[lane + 32 * (__ffs(mm) - 1)].fi);
+        }
+        bfi = b_n ? warp_min64(lfi) : 0;
+        pick_blocked = false;
+        if (pushed) { p_front(); next_arrival(); }
+      } else if (!TB && bfi == iter - 1) {                      // finishes (l.43-48)
         bool pushed = false;
         do {
           BEnt f = s.b[0];
@@ -831,7 +928,7 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
 
 // ------------------------------------------------------------------ state layout
 enum { L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_US, L_HK, L_HM, L_HPOS, L_CS, L_CF, L_BLK, L_RT, L_HSEQ, L_RF,
-       L_RAPP, L_AG, L_AGS, L_N };
+       L_RAPP, L_AG, L_AGS, L_BK, L_BF, L_N };
 struct EngLayout {
   size_t bytes_smem = 0, bytes_glob = 0;
   size_t off[L_N];
@@ -839,6 +936,7 @@ struct EngLayout {
   u32 c_cap = 0;                        // continuation-slot pool capacity
   u32 rf_cap = 0, A = 0;                // RPM window log capacity, apps
   u32 ag_cap = 0;                       // app-global window log capacity
+  u32 b_cap = 0;                        // B slots (Bmax)
 };
 
 // slots: capacity of the pool of queued-continuation slots (R5)
@@ -861,10 +959,12 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   sz[L_RAPP] = rf_cap ? (size_t)A * 4 : 0;
   sz[L_AG] = (size_t)ag_cap * sizeof(AGEnt);
   sz[L_AGS] = ag_cap ? (size_t)A * sizeof(AGSum) : 0;
+  sz[L_BK] = (size_t)Bmax * sizeof(BKey); sz[L_BF] = (size_t)Bmax * 4;
   // shared-memory priority: hottest first (the head ring must be shared)
-  static const int prio[] = {L_HR, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_RAPP, L_AGS, L_US, L_HK, L_HM, L_CS, L_CF};
+  static const int prio[] = {L_HR, L_BK, L_BF, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_RAPP, L_AGS, L_US, L_HK,
+                             L_HM, L_CS, L_CF};
   EngLayout L;
-  L.c_cap = (u32)slots;
+  L.c_cap = (u32)slots; L.b_cap = Bmax;
   L.rf_cap = rf_cap; L.A = A; L.ag_cap = ag_cap;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
@@ -887,6 +987,7 @@ __device__ inline void eng_bind(const EngLayout& L, unsigned char* sm, unsigned 
   s->r = (REnt*)P(L_RT); s->hpos = (uint2*)P(L_HPOS);
   s->hseq = (u32*)P(L_HSEQ); s->rf = (RPEnt*)P(L_RF); s->rf_cap = L.rf_cap; s->rapp = (u32*)P(L_RAPP);
   s->ag = (AGEnt*)P(L_AG); s->ag_cap = L.ag_cap; s->ags = (AGSum*)P(L_AGS);
+  s->bk = (BKey*)P(L_BK); s->bfree = (u32*)P(L_BF); s->b_cap = L.b_cap;
   if (hr) {
     unsigned char* base = (unsigned char*)P(L_HR);
     hr->prod = (volatile u32*)base; hr->cons = (volatile u32*)(base + 4); hr->eof = (volatile u32*)(base + 8);
@@ -906,6 +1007,7 @@ __device__ inline void eng_clear(const EngState& s, const EngShared& sh, const u
     z.qh_front = o; z.qh_next = o;
     s.us[k] = z;
   }
+  for (u32 k = lane; k < s.b_cap; k += nl) s.bfree[k] = s.b_cap - 1 - k;   // pops hand out 0, 1, 2, ...
   for (u64 w = lane; w < sh.n_heads / 32 + 2; w += nl) s.blocked[w] = 0;
   if (s.rf_cap) for (u32 a = lane; a < sh.A; a += nl) s.rapp[a] = 0;
   if (s.ag_cap) for (u32 a = lane; a < sh.A; a += nl) { AGSum z; z.tau = 0; z.n = 0; z.pad = 0; s.ags[a] = z; }
@@ -922,7 +1024,7 @@ struct ReplayKArgs {
 // warp 1 streams head arrivals into the shared ring
 // single replay, one warp: the 32 lanes run the engine in lockstep and refill the head batch
 // together (the sweep's engine; state in shared memory first)
-template <bool BASE>
+template <bool BASE, int TOUR>
 __global__ void __launch_bounds__(32) k_replay_warp(const __grid_constant__ ReplayKArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ HEnt hbs[32];
@@ -933,7 +1035,7 @@ __global__ void __launch_bounds__(32) k_replay_warp(const __grid_constant__ Repl
   eng_clear(st, a.sh, a.cfg.W, AJ, a.U, threadIdx.x, 32);
   __syncwarp();
   __threadfence_block();
-  EngineT<HS_WARP, 32, BASE> E;
+  EngineT<HS_WARP, 32, BASE, TOUR> E;
   E.init(&a.sh, &a.cfg, st, a.out, a.U);
   E.hb = hbs;
   E.run();
@@ -979,7 +1081,7 @@ struct SweepKArgs {
 // One scenario slot per group of LPS lanes.  Every lane of a group runs the (group-uniform)
 // engine: loads and stores of the replicated state are broadcast / merged, and head batch
 // refills use all LPS lanes.
-template <int MINB, int LPS, bool BASE>  // MINB CTAs per SM: caps registers (occupancy vs spills)
+template <int MINB, int LPS, bool BASE, int TOUR>  // MINB CTAs per SM: caps registers (occupancy vs spills)
 __global__ void __launch_bounds__(128, MINB) k_sweep(const __grid_constant__ SweepKArgs a) {
   __shared__ HEnt hbs[128];
   const u32 lane = threadIdx.x & 31, sub = threadIdx.x & (LPS - 1), lead = lane & ~(u32)(LPS - 1);
@@ -1003,7 +1105,7 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(const __grid_constant__ Swe
     __syncwarp(gm);
     __threadfence_block();
     {
-      EngineT<HS_WARP, LPS, BASE> E;
+      EngineT<HS_WARP, LPS, BASE, TOUR> E;
       E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
       E.hb = &hbs[threadIdx.x & ~(u32)(LPS - 1)];
       E.run();

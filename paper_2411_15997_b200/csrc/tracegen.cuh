@@ -159,6 +159,7 @@ __global__ void k_gen_wscan(u32 U, const double* w, double* wcum) {    // one th
 extern "C" int fs_generate_trace(fs_ctx* ctx, const fs_gen_cfg* c, uint32_t* user, uint32_t* t_ms, uint32_t* len_in,
                                  uint32_t* len_sys, uint32_t* len_out, uint32_t* think_ms, uint32_t* inter,
                                  uint32_t* meta, uint32_t* n_inters_h) {
+  FS_NVTX("fs_generate_trace");
   if (!ctx || !c || !n_inters_h || c->n_users == 0 || c->n_apps == 0 || c->n_apps > 255 || !c->app_means_h ||
       c->duration_ms == 0 || c->n_calls >= (1ull << 32) ||
       (c->n_calls && (!user || !t_ms || !len_in || !len_sys || !len_out || !think_ms || !inter || !meta)))

@@ -1,9 +1,9 @@
 """Multi-process (gloo, world_size 2, CPU) tests of the multi-GPU host logic.
 
 1. The user-hash-sharded profile protocol's decomposition: per-shard
-   integer sums and histograms SUM-all-reduce to the unsharded ones; dense per-user
-   window peaks (disjoint users) SUM-all-reduce to a gather; limits derived from the
-   gathered peaks equal the unsharded oracle's.  Computed with the oracle per shard.
+   integer sums and histograms SUM-all-reduce to the unsharded ones; the per-user window
+   peaks stay on their rank, and a radix select over SUM-all-reduced per-set counts and
+   digit histograms gives the unsharded limits.  Computed with the oracle per shard.
 2. The binding's round loop (build_app_profiles_dist) drives local -> rounds with
    all_reduce -> finalize in order, against a fake library speaking the protocol.
 3. bench.py's max-over-ranks timing reduction.
@@ -73,29 +73,73 @@ def _profile_decomposition(rank, world):
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     want = np.concatenate([ref[k].ravel() for k in ("cnt", "sum_in", "sum_sys", "sum_out", "hist")]).astype(np.int64)
     assert (t.numpy() == want).all()
-    # R1: dense peaks of this shard's users (zero elsewhere) -> SUM = gather.  The shard
-    # profile's Ô comes from the shard only, so recompute peaks against the global Ô by
-    # profiling the shard with the global sums: equal because tau uses Ô from R0.
+    # R1+: the window peaks stay on their rank (disjoint users).  The limits' nearest-rank
+    # quantiles come from a radix select whose per-set counts and 8-bit digit histograms are
+    # SUM-all-reduced: every rank picks the same digits and ends with the unsharded quantile.
     users = np.unique(sh["user"])
     mine = np.zeros(tr["n_users"], bool)
     mine[users] = True
-    pk = np.concatenate([np.where(mine, ref["peak_r_u"], 0), np.where(mine, ref["peak_t_u"], 0),
-                         np.where(mine[:, None], ref["peak_r_ua"], 0).ravel(),
-                         np.where(mine[:, None], ref["peak_t_ua"], 0).ravel()]).astype(np.int64)
-    t = torch.from_numpy(pk)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     U, A = tr["n_users"], tr["n_apps"]
-    g = t.numpy()
-    assert (g[:U] == ref["peak_r_u"]).all() and (g[U:2 * U] == ref["peak_t_u"]).all()
-    assert (g[2 * U:2 * U + U * A].reshape(U, A) == ref["peak_r_ua"]).all()
-    # limits from the gathered peaks = the unsharded limits (nearest rank, Q8 multiplier)
-    pr = g[:U][g[:U] > 0]
-    k = max(1, -(-990000 * len(pr) // 1000000))
-    nr = np.sort(pr)[k - 1]
-    assert max(1, -(-256 * int(nr) // 256)) == int(ref["T_req_g"][0])
-    # peaks per user only need the user's own calls: the shard's oracle profile with the
-    # same Ô gives the same peaks for its users whenever its sums equal the global ones
+    sets = []                                         # (request values, token values) per set
+    for a in range(A):
+        pres = mine & (ref["peak_r_ua"][:, a] > 0)
+        sets.append((ref["peak_r_ua"][pres, a].astype(np.uint64), ref["peak_t_ua"][pres, a].astype(np.uint64)))
+    pres = mine & (ref["peak_r_u"] > 0)
+    sets.append((ref["peak_r_u"][pres].astype(np.uint64), ref["peak_t_u"][pres].astype(np.uint64)))
+    vals = [v[0] for v in sets] + [v[1] for v in sets]
+    t = torch.tensor([len(v) for v in vals], dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    n = t.numpy()
+    krank = [max(1, -(-990000 * int(x) // 1000000)) - 1 if x else 0 for x in n]
+    prefix = [0] * len(vals)
+    mx = torch.tensor([max([int(v.max()) if len(v) else 0 for v in vals])], dtype=torch.int64)
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    top = max(0, (int(mx[0]).bit_length() + 7) // 8 - 1)
+    for d in range(top, -1, -1):
+        h = np.zeros((len(vals), 256), np.int64)
+        for s_, v in enumerate(vals):
+            sel = v if d == top else v[(v >> np.uint64(8 * d + 8)) == np.uint64(prefix[s_])]
+            np.add.at(h[s_], ((sel >> np.uint64(8 * d)) & np.uint64(255)).astype(np.int64), 1)
+        t = torch.from_numpy(h)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        for s_, row in enumerate(t.numpy()):
+            if not n[s_]:
+                continue
+            c = np.cumsum(row)
+            b = int(np.searchsorted(c, krank[s_], side="right"))
+            krank[s_] -= int(c[b - 1]) if b else 0
+            prefix[s_] = (prefix[s_] << 8) | b
+    nr = [p_ if n[s_] else 0 for s_, p_ in enumerate(prefix)]
+    assert nr[:A] == [int(x) for x in ref["nr_peak_r_a"]] and nr[A] == int(ref["nr_peak_r_g"][0])
+    assert nr[A + 1:2 * A + 1] == [int(x) for x in ref["nr_peak_t_a"]] and nr[2 * A + 1] == int(ref["nr_peak_t_g"][0])
+    assert max(1, -(-256 * nr[A] // 256)) == int(ref["T_req_g"][0])
     return int(mine.sum())
+
+
+def _act_sharded(rank, world):
+    """ACT shards by user with no exchange: the rank's shard throttled
+    alone with the replicated profile gives the unsharded statuses of its calls, and the
+    per-rank summaries SUM to the unsharded summary."""
+    import oracle as O
+    from paper_2411_15997_b200 import tracegen as G
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=80, n_calls=20_000, seed=78))
+    prof = O.profile(tr, dict(tier_max=0))
+    act = dict(window_ms=60000, limits_from_profile=1)
+    full, fsum = O.act(tr, prof, act)
+    with np.errstate(over="ignore"):
+        keep = np.nonzero(G.sm64(tr["user"].astype(np.uint64)) % np.uint64(world) == np.uint64(rank))[0]
+    st, ssum = O.act(G.shard_by_user(tr, rank, world), prof, act)
+    assert (np.asarray(st) == np.asarray(full)[keep]).all()
+    keys = ("n_in", "n_admit", "n_dropped", "n_inter_blocked")
+    t = torch.tensor([int(ssum[k]) for k in keys] + [int(x) for x in ssum["n_block"]], dtype=torch.int64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    assert t.tolist() == [int(fsum[k]) for k in keys] + [int(x) for x in fsum["n_block"]]
+    return int(sum(fsum["n_block"]))
+
+
+def test_act_user_sharded_gloo():
+    res = _run("_act_sharded", 2)
+    assert res[0] == res[1] and res[0] > 0
 
 
 def test_profile_protocol_decomposition_gloo():

@@ -181,9 +181,23 @@ def test_profile_c2_full(F, ctx):
     _cmp_profile(gpr, O.profile(tr, cfg), 5)
 
 
+def _cmp_profile_shard(gpr, op, nq, mine):
+    """A rank's finalised profile: every global table equals the unsharded one; the per-user
+    window peaks are the rank's own users' (zero elsewhere) -- they are never gathered."""
+    for k in ("peak_r_u", "peak_t_u", "peak_r_ua", "peak_t_ua"):
+        a, b = np.asarray(gpr[k]), np.asarray(op[k])
+        m = mine if a.ndim == 1 else mine[:, None]
+        assert a.shape == b.shape and (a == np.where(m, b, 0)).all(), k
+    g = dict(gpr)
+    for k in ("peak_r_u", "peak_t_u", "peak_r_ua", "peak_t_ua"):
+        g[k] = op[k]
+    _cmp_profile(g, op, nq)
+
+
 def test_profile_virtual_ranks(F, ctx):
     """The phased multi-GPU protocol with G virtual ranks on one GPU (SUM of the
-    per-shard round payloads) finalises the unsharded profile bit for bit."""
+    per-shard round payloads) finalises the unsharded profile bit for bit: sums, histograms,
+    quantiles and the limits (radix-selected from digit histograms of the ranks' peaks)."""
     import ctypes as C
     import torch
     tr = G.generate(dict(G.CONFIGS["c2"], n_users=120, n_calls=40_000, seed=31))
@@ -200,7 +214,7 @@ def test_profile_virtual_ranks(F, ctx):
             ctx._check(F.lib().fs_profile_local(ctx.h, F._a(sh.c), F._a(c), C.byref(p), C.byref(w)))
             parts.append(p)
             bufs.append(torch.zeros(w.value, dtype=torch.int64, device="cuda"))
-        for _ in range(8):
+        for _ in range(24):
             dones, ws = [], []
             for p, b in zip(parts, bufs):
                 w = C.c_size_t(0)
@@ -214,11 +228,49 @@ def test_profile_virtual_ranks(F, ctx):
             tot = sum(b[: ws[0]] for b in bufs)
             for b in bufs:
                 b[: ws[0]] = tot
-        for p in parts:
+        assert dones[0]
+        with np.errstate(over="ignore"):
+            owner = G.sm64(np.arange(tr["n_users"], dtype=np.uint64)) % np.uint64(Gn)
+        for r, p in enumerate(parts):
             h = C.c_void_p()
             ctx._check(F.lib().fs_profile_finalize(p, C.byref(h)))
-            _cmp_profile(F.Profile(ctx, h).read(), ref, 5)
+            _cmp_profile_shard(F.Profile(ctx, h).read(), ref, 5, owner == np.uint64(r))
             F.lib().fs_profile_partial_free(p)
+
+
+def _shard_keep(tr, r, Gn):
+    with np.errstate(over="ignore"):
+        return np.nonzero(G.sm64(tr["user"].astype(np.uint64)) % np.uint64(Gn) == np.uint64(r))[0]
+
+
+def test_act_user_sharded(F, ctx):
+    """ACT shards by user with no exchange (windows are per user and per
+    (user, app)) -- each user-hash shard throttled alone, with the replicated profile,
+    gives exactly the unsharded statuses of its calls; overload always and replay-recorded."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=150, n_calls=40_000, seed=41))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=0))
+    act = dict(window_ms=60000, limits_from_profile=1)
+    full, fs = F.act_throttle(ctx, F.Trace(tr), gp, act)
+    full = full.cpu().numpy()
+    assert fs["n_block"][0] + fs["n_block"][2] > 0
+    eng = dict(G.CONFIGS["c2"]["engine"], mode=1, tier_max=255, act=act)
+    o, _ = F.wsc_replay(ctx, F.Trace(tr), gp, eng)
+    ovl, arr = o["ovl"].cpu().numpy(), o["arrive_ns"].cpu().numpy()
+    full2, _ = F.act_throttle(ctx, F.Trace(tr), gp, act, overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
+    full2 = full2.cpu().numpy()
+    import torch
+    for Gn in (2, 4):
+        tot = 0
+        for r in range(Gn):
+            keep = _shard_keep(tr, r, Gn)
+            sh = F.Trace(G.shard_by_user(tr, r, Gn))
+            st, ss = F.act_throttle(ctx, sh, gp, act)
+            assert (st.cpu().numpy() == full[keep]).all()
+            tot += ss["n_admit"]
+            st2, _ = F.act_throttle(ctx, sh, gp, act, overloaded=torch.from_numpy(ovl[keep]).cuda(),
+                                    t_ns_override=torch.from_numpy(arr[keep]).cuda())
+            assert (st2.cpu().numpy() == full2[keep]).all()
+        assert tot == fs["n_admit"]
 
 
 # ------------------------------------------------------------------ ACT
@@ -387,6 +439,30 @@ def test_sweep_small(F, ctx):
     assert list(gcodes) == list(ecodes)
     for a, b in zip(gs, es):
         assert a == b
+
+
+def test_sweep_capacity_retry(F, ctx):
+    """Scenarios whose state outgrows the sweep's first capacities (a 512-entry ACT ring per user,
+    a 65 536-entry RPM window log) run again with exact capacities: same summaries as the oracle,
+    no FS_E_NOMEM.  Five users share 70 000 calls and the windows span the whole day."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=5, n_calls=70_000, seed=62))
+    op = O.profile(tr, dict(tier_max=255))
+    gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=255))
+    A = tr["n_apps"]
+    day = 86_400_000
+    base = dict(G.CONFIGS["c2"]["engine"], tier_max=255)
+    scen = [dict(base, mode=1, act=dict(window_ms=day, limits_from_profile=0, T_req_g=1 << 30, T_req_a=[1 << 30] * A)),
+            dict(base, mode=1, overload_permille=0,
+                 act=dict(window_ms=day, limits_from_profile=0, T_req_g=3000, T_req_a=[2000] * A)),
+            dict(base, mode=0),
+            dict(base, mode=3, act=dict(window_ms=day, limits_from_profile=0, T_req_g=1 << 30, T_req_a=[1 << 30] * A))]
+    es, ecodes = O.sweep(tr, op, scen)
+    assert list(ecodes) == [0] * len(scen)
+    for sub in (scen[:3], scen):            # FairServe modes only (tournament engine), then with RPM
+        gs, gcodes = F.sweep(ctx, F.Trace(tr), gp, sub)
+        assert list(gcodes) == [0] * len(sub)
+        for a, b in zip(gs, es):
+            assert a == b
 
 
 # ------------------------------------------------------------------ errors

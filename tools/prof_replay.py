@@ -1,6 +1,6 @@
 """Run one replay (and optionally the data-parallel calls) of a C2/C3-shaped trace,
 for ncu / timing experiments on the GPU box.  Usage:
-    python tools/prof_replay.py [c2|c3] [n_calls] [mode]"""
+    python tools/prof_replay.py [c2|c3] [n_calls] [mode] [n_users]"""
 import os
 import sys
 import time
@@ -17,11 +17,14 @@ from paper_2411_15997_b200 import tracegen as G  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 mode = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+nu = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 B.build()
 cfg = dict(G.CONFIGS[name])
 if n:
     cfg["n_users"] = max(50, int(cfg["n_users"] * n / cfg["n_calls"]))
     cfg["n_calls"] = n
+if nu:
+    cfg["n_users"] = nu
 tr = G.generate(cfg)
 ctx = F.Context(0)
 T = F.Trace(tr)
