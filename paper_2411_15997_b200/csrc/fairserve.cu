@@ -151,16 +151,17 @@ static void prof_stream(fs_ctx* ctx, const DTrace& t, u32 J, u32 tier_max, u64* 
                         u64* s_out, u64* hist) {
   const u32 A = t.A, J1 = J + 1;
   size_t sums = (size_t)4 * A * J1 * 8;
-  size_t budget = ctx->smem_optin ? ctx->smem_optin - 1024 : 200 * 1024;
-  size_t per_app = (size_t)HB_APP * 4;
-  u32 na = (u32)std::min<size_t>(A, (budget - sums) / per_app);
-  if (na == 0) na = 1;
+  const size_t budget = ctx->smem_optin ? ctx->smem_optin - 1024 : 200 * 1024;
+  const size_t per_app = (size_t)HB_APP * 4;
+  const u32 gsums = sums + per_app > budget;           // the sums alone would not leave room for one app
+  if (gsums) sums = 0;
+  const u32 na = (u32)std::max<size_t>(1, std::min<size_t>(A, (budget - sums) / per_app));
   u32 chunks = (A + na - 1) / na;
   size_t smem = sums + (size_t)na * per_app;
   cudaFuncSetAttribute(k_prof_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   u32 vec = al(t.meta) && al(t.len_in) && al(t.len_sys) && al(t.len_out);
-  ProfStreamArgs a{t, J, tier_max, na, vec, cnt, s_in, s_sys, s_out, hist};
+  ProfStreamArgs a{t, J, tier_max, na, vec, cnt, s_in, s_sys, s_out, hist, gsums};
   dim3 grid(ctx->sm_count, chunks);
   if (t.n) FS_LAUNCH(ctx, "prof_stream", k_prof_stream, grid, 1024, smem, a);
 }
@@ -360,10 +361,14 @@ static u64 prof_q_next(fs_profile_partial* pp, u64* buf) {
   pp->h2_words = w;
   if (!w) return 0;
   cudaMemsetAsync(buf, 0, w * 8, ctx->stream);
-  size_t smem = (size_t)A * 4 * 3 * nq * sizeof(QIv) + (size_t)A * 4 * 4 + (size_t)A * 4 * 8 * 4;
-  cudaFuncSetAttribute(k_q_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  QCountArgs a{pp->t, pp->cfg.tier_max, nq, pp->qiv, pp->qniv, buf};
-  if (pp->t.n) FS_LAUNCH(ctx, "q_count", k_q_count, ctx->sm_count * 2, 512, smem, a);
+  // apps in chunks whose interval tables fit shared memory (one pass over the trace per chunk)
+  const size_t per_app = q_count_smem_per_app(nq), budget = ctx->smem_optin ? ctx->smem_optin - 1024 : 96 * 1024;
+  const u32 na = (u32)std::max<size_t>(1, std::min<size_t>(A, budget / per_app));
+  cudaFuncSetAttribute(k_q_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(na * per_app + 16));
+  for (u32 a0 = 0; a0 < A && pp->t.n; a0 += na) {
+    QCountArgs a{pp->t, pp->cfg.tier_max, nq, pp->qiv, pp->qniv, buf, a0, std::min(na, A - a0)};
+    FS_LAUNCH(ctx, "q_count", k_q_count, ctx->sm_count * 2, 512, a.na * per_app + 16, a);
+  }
   return w;
 }
 

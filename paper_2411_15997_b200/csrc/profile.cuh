@@ -101,6 +101,7 @@ static void profile_mirror(fs_profile* P, cudaStream_t s) {   // device -> host 
 struct ProfStreamArgs {
   DTrace t; u32 J, tier_max, na_chunk, vec;
   u64 *cnt, *s_in, *s_sys, *s_out, *hist;
+  u32 gsums;                 // the Eq. 2 sums do not fit shared memory: global atomics (large A x J)
 };
 
 // shared-memory bins per app: only the bins a validated field can reach (L < 2^24: bins < 176;
@@ -114,19 +115,24 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const u32 J1 = a.J + 1, A = a.t.A, AJ = A * J1;
   const u32 a0 = blockIdx.y * a.na_chunk, na = min(a.na_chunk, A - a0);
-  const bool do_sums = blockIdx.y == 0;
+  const bool do_sums = blockIdx.y == 0, ssums = do_sums && !a.gsums;
   // sums as u32 pairs: lo[4][AJ] then hi[4][AJ] (a u64 shared atomicAdd is a CAS loop on sm_100a;
   // a u32 add returns the old value, and the add that wraps it carries into hi)
   u32* slo = (u32*)sm;
   u32* shi = slo + 4 * AJ;
-  u32* shist = (u32*)(sm + (do_sums ? (size_t)4 * AJ * 8 : 0));   // [na][HB_APP]
-  const u32 nsum = do_sums ? 8 * AJ : 0, nh = na * HB_APP;
+  u32* shist = (u32*)(sm + (ssums ? (size_t)4 * AJ * 8 : 0));     // [na][HB_APP]
+  const u32 nsum = ssums ? 8 * AJ : 0, nh = na * HB_APP;
   for (u32 k = threadIdx.x; k < nsum; k += blockDim.x) slo[k] = 0;
   for (u32 k = threadIdx.x; k < nh; k += blockDim.x) shist[k] = 0;
   __syncthreads();
   const u64 n = a.t.n;
   auto add64 = [&](u32 k, u32 v) {
     if (!v) return;
+    if (!ssums) {
+      u64* dst = k < AJ ? a.cnt : k < 2 * AJ ? a.s_in : k < 3 * AJ ? a.s_sys : a.s_out;
+      atomicAdd((unsigned long long*)&dst[k % AJ], (unsigned long long)v);
+      return;
+    }
     const u32 old = atomicAdd(&slo[k], v);
     if (old + v < old) atomicAdd(&shi[k], 1u);
   };
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(1024) k_prof_stream(ProfStreamArgs a) {
     one(ok, m, Li, Ls, Lo);
   }
   __syncthreads();
-  for (u32 k = threadIdx.x; k < 4 * AJ; k += blockDim.x) {
+  for (u32 k = threadIdx.x; k < (ssums ? 4 * AJ : 0); k += blockDim.x) {
     const u64 v = (u64)shi[k] << 32 | slo[k];
     if (v) {
       u32 arr = k / AJ, idx = k % AJ;
@@ -659,36 +665,42 @@ __global__ void k_q_intervals(u32 A, u32 nq, const QState* st, QIv* iv, u32* niv
 }
 
 // count pass: values inside candidate intervals -> sub-bin counters (u64)
-struct QCountArgs { DTrace t; u32 tier_max, nq; const QIv* iv; const u32* niv; u64* h2; };
+static const u32 NBINS_Q = 240;   // log-linear bins of a u32 value (loglin_bin < 240)
+struct QCountArgs { DTrace t; u32 tier_max, nq; const QIv* iv; const u32* niv; u64* h2; u32 a0, na; };
+// shared memory per app of a chunk [a0, a0 + na) (the launcher chunks the apps to fit)
+__host__ __device__ __forceinline__ size_t q_count_smem_per_app(u32 nq) {
+  return (size_t)4 * (3 * nq * sizeof(QIv) + 4 + NBINS_Q + 3 * nq);
+}
 __global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
-  const u32 A = a.t.A, maxi = 3 * a.nq;
-  QIv* siv = (QIv*)sm;                                  // [A*4][maxi]
-  u32* sniv = (u32*)(sm + (size_t)A * 4 * maxi * sizeof(QIv));
-  u32* mask = sniv + A * 4;                             // [A*4][8] bins that hold intervals
-  for (u32 k = threadIdx.x; k < A * 4 * maxi; k += blockDim.x) siv[k] = a.iv[k];
-  for (u32 k = threadIdx.x; k < A * 4; k += blockDim.x) sniv[k] = a.niv[k];
-  for (u32 k = threadIdx.x; k < A * 4 * 8; k += blockDim.x) mask[k] = 0;
+  const u32 NA = a.na, maxi = 3 * a.nq;
+  QIv* siv = (QIv*)sm;                                  // [NA*4][maxi]
+  u32* sniv = (u32*)(sm + (size_t)NA * 4 * maxi * sizeof(QIv));
+  for (u32 k = threadIdx.x; k < NA * 4 * maxi; k += blockDim.x) siv[k] = a.iv[(u64)a.a0 * 4 * maxi + k];
+  for (u32 k = threadIdx.x; k < NA * 4; k += blockDim.x) sniv[k] = a.niv[a.a0 * 4 + k];
+  // per (app, field, log-linear bin): the first candidate interval in the bin and a chain through the
+  // others (intervals never straddle a bin), so a value costs one byte lookup instead of a scan
+  unsigned char* tab = (unsigned char*)(sniv + NA * 4);        // [NA*4][NBINS_Q], 0xFF = none
+  unsigned char* nxt = tab + (size_t)NA * 4 * NBINS_Q;          // [NA*4][maxi]
+  for (u32 k = threadIdx.x; k < NA * 4 * NBINS_Q; k += blockDim.x) tab[k] = 0xFF;
   __syncthreads();
-  for (u32 k = threadIdx.x; k < A * 4 * maxi; k += blockDim.x) {
-    u32 af = k / maxi;
-    if (k % maxi < sniv[af]) {
-      u32 b = loglin_bin((u32)siv[k].lo);
-      atomicOr(&mask[af * 8 + b / 32], 1u << (b % 32));
+  for (u32 af = threadIdx.x; af < NA * 4; af += blockDim.x)
+    for (int k = (int)sniv[af] - 1; k >= 0; k--) {
+      const u32 b = loglin_bin((u32)siv[af * maxi + k].lo);
+      nxt[af * maxi + k] = tab[af * NBINS_Q + b];
+      tab[af * NBINS_Q + b] = (unsigned char)k;
     }
-  }
   __syncthreads();
   const u64 n = a.t.n, stride = (u64)gridDim.x * blockDim.x;
   auto one = [&](u32 m, u32 li, u32 ls, u32 lo) {
-    if (m_tier(m) > a.tier_max) return;
-    const u32 app = m_app(m);
+    const u32 app = m_app(m) - a.a0;                      // chunk-local (wraps for apps below a0)
+    if (m_tier(m) > a.tier_max || app >= NA) return;
     u32 v[4];
     v[0] = li; v[1] = ls; v[2] = lo; v[3] = li + ls + lo;
 #pragma unroll
     for (int f = 0; f < 4; f++) {
-      u32 af = app * 4 + f, b = loglin_bin(v[f]);
-      if (!(mask[af * 8 + b / 32] & (1u << (b % 32)))) continue;
-      for (u32 k = 0; k < sniv[af]; k++) {
+      const u32 af = app * 4 + f;
+      for (u32 k = tab[af * NBINS_Q + loglin_bin(v[f])]; k != 0xFF; k = nxt[af * maxi + k]) {
         const QIv& q = siv[af * maxi + k];
         if ((u64)v[f] >= q.lo && (u64)v[f] < q.lo + (1ull << q.w)) {
           atomicAdd((unsigned long long*)&a.h2[q.off + (((u64)v[f] - q.lo) >> q.shift)], 1ull);

@@ -194,6 +194,20 @@ def _cmp_profile_shard(gpr, op, nq, mine):
     _cmp_profile(g, op, nq)
 
 
+def test_profile_many_apps(F, ctx):
+    """A = 200 apps at J = 64: the Eq. 2 sums (200 x 65 x 4 u64) do not fit shared memory (global
+    atomics), the histograms and the quantile tables run in app chunks; same profile as the oracle."""
+    tr = G.generate(dict(G.CONFIGS["c2"], n_users=150, n_calls=30_000, seed=33))
+    tr = dict(tr)
+    A = 200
+    app = (tr["inter"].astype(np.uint64) * np.uint64(2654435761) % np.uint64(A)).astype(np.uint32)
+    tr["meta"] = (tr["meta"] & np.uint32(0xFFFFFF00)) | app
+    tr["n_apps"] = A
+    tr["app_names"] = [f"a{k}" for k in range(A)]
+    cfg = dict(tier_max=255, max_stage=64)
+    _cmp_profile(F.build_app_profiles(ctx, F.Trace(tr), cfg).read(), O.profile(tr, cfg), 5)
+
+
 def test_profile_virtual_ranks(F, ctx):
     """The phased multi-GPU protocol with G virtual ranks on one GPU (SUM of the
     per-shard round payloads) finalises the unsharded profile bit for bit: sums, histograms,
