@@ -82,12 +82,22 @@ __global__ void k_act_prep(ActPrepArgs a) {
 }
 
 // 64-bit time keys: arrived -> t_ns, never arrived -> maxv + 1 (sorted last)
+// grid-stride, one atomic per block (an atomic per warp on one word serialised 300k updates at C3)
 __global__ void k_act_tmax(u64 n, const i64* tov, unsigned long long* mx) {
-  u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  i64 v = i < n ? tov[i] : -1;
-  unsigned long long x = v < 0 ? 0ull : (unsigned long long)v;
+  __shared__ unsigned long long wm[32];
+  unsigned long long x = 0;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const i64 v = tov[i];
+    if (v > 0 && (unsigned long long)v > x) x = (unsigned long long)v;
+  }
   for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(FULL_MASK, x, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(mx, x);
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    x = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0;
+    for (int o = 16; o; o >>= 1) x = max(x, __shfl_xor_sync(FULL_MASK, x, o));
+    if (threadIdx.x == 0 && x) atomicMax(mx, x);
+  }
 }
 __global__ void k_act_tkeys(u64 n, const i64* tov, const unsigned long long* mx, u64* key) {
   u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;

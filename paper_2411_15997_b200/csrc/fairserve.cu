@@ -561,7 +561,7 @@ static bool act_time_perm(fs_ctx* ctx, Scratch& S, const DTrace& t, const i64* t
   unsigned long long* mx = S.zeros<unsigned long long>(1);
   u64* tk = S.alloc<u64>(n);
   if (S.failed) return false;
-  FS_LAUNCH(ctx, "act_tmax", k_act_tmax, div_up(n, B), B, 0, n, tov, mx);
+  FS_LAUNCH(ctx, "act_tmax", k_act_tmax, std::min(div_up(n, B), ctx->sm_count * 8), B, 0, n, tov, mx);
   FS_LAUNCH(ctx, "act_tkeys", k_act_tkeys, div_up(n, B), B, 0, n, tov, mx, tk);
   unsigned long long hmx = 0;
   cudaMemcpyAsync(&hmx, mx, 8, cudaMemcpyDeviceToHost, ctx->stream);

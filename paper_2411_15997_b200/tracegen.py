@@ -67,7 +67,8 @@ CONFIGS = {
                in_cap=16_000, sys_cap=4000, out_cap=4000,
                engine=dict(kv_capacity=49_152, max_batch=256, overload_permille=900,
                            iter_base_ns=200_000, decode_ns_per_req=2_000,
-                           prefill_ns_per_tok=1_000),
+                           prefill_ns_per_tok=1_500),   # calibrated (oracle, FS(W)): 22.5 % of arrivals
+                                                        # overloaded with every tier, 3.0 % benign only
                act=dict(window_ms=60_000),
                profile=dict(tier_max=0)),
     "c4": dict(name="c4", n_users=100_000, apps=[t[0] for t in APP_TEMPLATES],
