@@ -368,8 +368,8 @@ static SweepFn sweep_kern_t(int t, int minb) {
   return t == 2 ? sweep_kern<2>(minb) : t == 4 ? sweep_kern<4>(minb) : t == 6 ? sweep_kern<6>(minb) : sweep_kern<0>(minb);
 }
 static ReplayFn replay_warp_kern_t(int t) {
-  return t == 2 ? k_replay_warp<false, 2> : t == 4 ? k_replay_warp<false, 4> : t == 6 ? k_replay_warp<false, 6>
-                                                                             : k_replay_warp<false, 0>;
+  return t == 2 ? k_replay_warp<false, 2>
+       : t == 4 ? k_replay_warp<false, 4> : t == 6 ? k_replay_warp<false, 6> : k_replay_warp<false, 0>;
 }
 
 // ------------------------------------------------------------------ fs_wsc_replay

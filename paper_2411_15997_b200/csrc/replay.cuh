@@ -497,7 +497,8 @@ struct EngineT {
     CSlot cs;
     if (cont) cs = s.cs[x];
     u32 r = cont ? us.cf : us.hf;                            // no dependent load on the slot
-    uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
+    uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = make_uint4(0, 0, 0, 0);
+    if (!c->inc) Cc = ldg4(&sh->recC[r]);                  // only Eq. 3 on the fly needs slot, L_I, L_S
     u64 inc_pre = c->inc ? c->inc[r] : 0;
     u64 need = (u64)B.y + B.w;
     us.nf = (u32)need;
