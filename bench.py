@@ -9,9 +9,11 @@ is timed after the steps and reported as `single_replay`.
 
 Other workloads: c2 / c3 (profile -> FS(W+I) replay -> ACT on the replay's arrival
 times and overload flags), c4 (100M-call profile sharded by user, NCCL rounds).
-N > 1: one process per GPU (torchrun).  c2/c3/c5 give every rank its own independent
-problem (weak scaling; the replay itself does not shard -- DESIGN.md §8); c4 shards one
-trace by user (strong scaling).  Time = max over ranks of CUDA-event time around the K steps.
+N > 1: one process per GPU (torchrun).  c5 splits ONE 4096-scenario grid over the ranks
+(longest-processing-time slices, NCCL all_gather of the summaries: strong scaling;
+--sweep-split off gives every rank its own grid); c4 shards one trace by user (strong
+scaling); c2/c3 run a replica per rank (the single replay does not shard -- DESIGN.md §8).
+Time = max over ranks of CUDA-event time around the K steps.
 
 --impl reference: the CPU oracle (oracle/, plain single-threaded C++) on this host,
 timed on a bounded sample of the same workload, printed as the reference arm.
@@ -167,8 +169,9 @@ def sweep_scenarios(eng, total):
     return [out[i] for i in sorted(idx)]
 
 
-# ALGORITHMIC bytes per call of the kernels that touch every call once per launch
-ALGO_BYTES = {"prof_stream": 16, "win_scan": 28, "act_flags": 21, "pack_records": 84,
+# ALGORITHMIC bytes per call of the kernels that touch every call once per launch,
+# reported for the C3 / C4 workloads (the C5 trace is L2-resident: its stage rates are cache rates)
+ALGO_BYTES = {"prof_stream": 16, "act_flags": 21, "pack_records": 84,
               "radix_scatter": 16}   # radix pass: 4 B key + 4 B value read, the same written
 
 
@@ -570,7 +573,7 @@ def ncu_csv(path):
 def roofline(name, launches, ms, N, peaks, src, args, kt):
     per_s = ms / max(launches, 1) / 1e3
     stages = []
-    for k, b in ALGO_BYTES.items():
+    for k, b in (ALGO_BYTES.items() if args.workload in ("c3", "c4") else ()):
         if k in kt and kt[k][1] > 0:
             gbs = b * N * kt[k][0] / (kt[k][1] / 1e3) / 1e9
             stages.append({"kernel": k, "bound": "hbm", "bytes_per_call": b, "achieved": gbs,
@@ -581,12 +584,12 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
         if name == "wsc_replay":
             # dependent instruction chain: one engine warp (+ the head-prefetch warp) issuing at
             # most one warp-instruction per cycle each at the measured max SM clock.
-            prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_replay.csv")) if args.workload == "c2" else {}
+            prof = ncu_csv(os.path.join(ROOT, "profiles", "r02_replay.csv")) if args.workload == "c2" else {}
             peak = 2 * ghz
             ncalls = 1_000_000
         else:
             # many independent one-lane replays: every SMSP can issue one warp-instruction per cycle
-            prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_sweep.csv"))
+            prof = ncu_csv(os.path.join(ROOT, "profiles", "r02_sweep.csv"))
             peak = peaks.get("sm_count", 148) * 4 * ghz
             ncalls = 1_000_000 * int(prof.get("scenarios", 64))
             units = N * args.scenarios
@@ -603,11 +606,6 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
     b = ALGO_BYTES.get(name, 0) * N
     gbs = b / per_s / 1e9 if b else None
     traffic = None
-    if name == "win_scan" and args.workload == "c4" and N == 100_000_000:
-        # one ncu launch of the same kernel at this size (profiles/r01_c4_winscan.csv)
-        prof = ncu_csv(os.path.join(ROOT, "profiles", "r01_c4_winscan.csv"))
-        if prof.get("dram__bytes_read.sum") is not None:
-            traffic = prof["dram__bytes_read.sum"] + prof.get("dram__bytes_write.sum", 0.0)
     return {"bound": "hbm", "kernel": name, "ms_per_launch": per_s * 1e3, "achieved": gbs,
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"] if gbs else None,
             "traffic": traffic, "algorithmic_bytes_per_launch": b, "peak_source": src, "hbm_stages": stages}

@@ -54,6 +54,11 @@ def test_full_size(name):
         assert sa[k] == v, k
     _, sw = F.wsc_replay(ctx, T, prof, dict(g["engine"], mode=0), outputs=False)
     assert sw["digest"] == g["replay_w"]["digest"]
+    if "act_always_sha" in g:                   # ACT as standalone screening: overload always
+        st2, sa2 = F.act_throttle(ctx, T, prof, g["engine"]["act"])
+        assert h(st2.cpu().numpy()) == g["act_always_sha"]
+        for k, v in g["act_always"].items():
+            assert sa2[k] == v, k
 
 
 def test_sweep_c5_full():

@@ -41,6 +41,7 @@ def run(name):
     t2 = time.time()
     st, sa = O.act(tr, p, act, overloaded=o["ovl"], t_ns_override=o["arrive_ns"])
     t3 = time.time()
+    sta, saa = O.act(tr, p, act)                 # standalone screening: recorded times, overload always
     ow, sw = O.replay(tr, p, dict(eng, mode=0), outputs=False)
     out = {
         "citation": "written by tools/make_goldens.py from oracle/ only (SURVEY.md §8(c) O2-O5); "
@@ -57,6 +58,8 @@ def run(name):
         "act": {k: sa[k] for k in ("n_in", "n_admit", "n_block", "n_dropped", "n_filtered")},
         "act_sha": h(st),
         "act_equals_replay_status": bool((st == o["status"]).all()),
+        "act_always": {k: saa[k] for k in ("n_in", "n_admit", "n_block", "n_dropped", "n_filtered")},
+        "act_always_sha": h(sta),
         "oracle_seconds": {"profile": t1 - t0, "replay_wi": t2 - t1, "act": t3 - t2},
     }
     path = os.path.join(ROOT, "tests", "golden", f"full_{name}.json")

@@ -1,7 +1,7 @@
 """Device time of fs_act_throttle per kernel on a device-generated trace (C3 by default): with
 replay-like arrival times (heads at their recorded time, continuations delayed 0-50 ms) and a
 20 % overload mask, and with overload always.  Mean of `reps` L2-flushed calls after a warm-up.
-Usage: python tools/time_act.py [c3|c2|c4] [reps]"""
+Usage: python tools/time_act.py [c3|c2|c4] [reps] [both|replay|always]"""
 import os
 import sys
 
@@ -15,6 +15,7 @@ from paper_2411_15997_b200 import fairserve as F  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+which = sys.argv[3] if len(sys.argv) > 3 else "both"
 B.build()
 ctx = F.Context(0)
 T = F.generate_trace(ctx, name)
@@ -29,8 +30,10 @@ ovl = (torch.rand(n, device="cuda", generator=g) < 0.2).to(torch.uint8)
 act = dict(window_ms=60000, limits_from_profile=1)
 flush = torch.empty(256 << 20, dtype=torch.int8, device="cuda")
 s = torch.cuda.current_stream()
-for label, kw in (("replay-like arrivals, 20% overloaded", dict(overloaded=ovl, t_ns_override=tov)),
-                  ("recorded times, overload always", {})):
+cases = [("replay-like arrivals, 20% overloaded", dict(overloaded=ovl, t_ns_override=tov)),
+         ("recorded times, overload always", {})]
+cases = cases[:1] if which == "replay" else cases[1:] if which == "always" else cases
+for label, kw in cases:
     st, summ = F.act_throttle(ctx, T, prof, act, **kw)
     torch.cuda.synchronize()
     ctx.timing_reset()
