@@ -361,13 +361,17 @@ static u64 prof_q_next(fs_profile_partial* pp, u64* buf) {
   pp->h2_words = w;
   if (!w) return 0;
   cudaMemsetAsync(buf, 0, w * 8, ctx->stream);
-  // apps in chunks whose interval tables fit shared memory (one pass over the trace per chunk)
-  const size_t per_app = q_count_smem_per_app(nq), budget = ctx->smem_optin ? ctx->smem_optin - 1024 : 96 * 1024;
+  // apps in chunks whose interval tables fit shared memory next to the private counters (one pass
+  // over the trace per chunk)
+  static const u32 qpriv = [] { const char* v = getenv("FS_QC_PRIV"); return v ? (u32)atoi(v) : QC_PRIV; }();
+  static const u32 qnsub = [] { const char* v = getenv("FS_QC_NSUB"); return v ? (u32)atoi(v) : QC_NSUB; }();
+  const size_t per_app = q_count_smem_per_app(nq), priv = (size_t)qpriv * 4 + 64;
+  const size_t budget = (ctx->smem_optin ? ctx->smem_optin - 1024 : 96 * 1024) - priv;
   const u32 na = (u32)std::max<size_t>(1, std::min<size_t>(A, budget / per_app));
-  cudaFuncSetAttribute(k_q_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(na * per_app + 16));
+  cudaFuncSetAttribute(k_q_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(na * per_app + priv));
   for (u32 a0 = 0; a0 < A && pp->t.n; a0 += na) {
-    QCountArgs a{pp->t, pp->cfg.tier_max, nq, pp->qiv, pp->qniv, buf, a0, std::min(na, A - a0)};
-    FS_LAUNCH(ctx, "q_count", k_q_count, ctx->sm_count * 2, 512, a.na * per_app + 16, a);
+    QCountArgs a{pp->t, pp->cfg.tier_max, nq, pp->qiv, pp->qniv, buf, a0, std::min(na, A - a0), qpriv, qnsub};
+    FS_LAUNCH(ctx, "q_count", k_q_count, ctx->sm_count, QC_T, a.na * per_app + priv, a);
   }
   return w;
 }
@@ -398,7 +402,7 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
     cudaMemcpyAsync(P->hist, buf + 4 * AJ, HW * 8, cudaMemcpyDeviceToDevice, ctx->stream);
     FS_LAUNCH(ctx, "prof_finish", k_prof_finish, div_up(A, 128), 128, 0, A, J, P->cnt, P->sum_out, P->ohat,
               P->maxstage, P->n_app);
-    if (P->nq) FS_LAUNCH(ctx, "q_init", k_q_init, div_up(A * 4, 128), 128, 0, A, P->nq, pp->d_qppm, P->hist, pp->qst);
+    if (P->nq) FS_LAUNCH(ctx, "q_init", k_q_init, div_up((u64)A * 4 * 32, 128), 128, 0, A, P->nq, pp->d_qppm, P->hist, pp->qst);
     cudaMemsetAsync(P->peak_r_u, 0, U * 4, ctx->stream);
     cudaMemsetAsync(P->peak_t_u, 0, U * 8, ctx->stream);
     cudaMemsetAsync(P->peak_r_ua, 0, (u64)U * A * 4, ctx->stream);
@@ -412,7 +416,7 @@ extern "C" int fs_profile_round(fs_profile_partial* pp, uint64_t* buf, size_t* w
     if (w == 0 && pp->peaks_done) *done = 1;
   } else {                                                // resolve previous level (+ limit digits)
     if (pp->h2_words)
-      FS_LAUNCH(ctx, "q_resolve", k_q_resolve, div_up((u64)A * 4 * 3 * P->nq, 128), 128, 0, A, P->nq, pp->qst,
+      FS_LAUNCH(ctx, "q_resolve", k_q_resolve, div_up((u64)A * 4 * 3 * P->nq * 32, 128), 128, 0, A, P->nq, pp->qst,
                 pp->qiv, pp->qniv, buf);
     if (!pp->peaks_done) lim_dist_recv(pp, buf);
     u64 w = prof_q_next(pp, buf);

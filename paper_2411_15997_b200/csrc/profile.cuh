@@ -612,21 +612,45 @@ __device__ __forceinline__ void q_ranks(u64 n, u32 qppm, u64 r[3], double* frac)
 }
 
 // thread per (a, f): locate each rank's level-1 bin
+// the first index b of counts c[0..nb) (contiguous per lane: lane l holds [l*per, (l+1)*per)) with
+// cum(b) + c[b] > r, and cum(b) = sum of c[0..b); warp-cooperative (all lanes call it)
+__device__ __forceinline__ void warp_rank_find(const u64* c, u32 nb, u64 r, u32* bout, u64* cumout) {
+  const u32 lane = threadIdx.x & 31, per = (nb + 31) / 32, b0 = lane * per, b1 = min(b0 + per, nb);
+  u64 loc = 0;
+  for (u32 b = b0; b < b1; b++) loc += c[b];
+  u64 inc = loc;
+  for (int o = 1; o < 32; o <<= 1) { const u64 y = __shfl_up_sync(FULL_MASK, inc, o); if ((int)lane >= o) inc += y; }
+  const u64 ex = inc - loc;
+  const bool mine = ex <= r && r < inc;
+  const u32 who = __ballot_sync(FULL_MASK, mine);
+  u32 bb = nb; u64 cc = 0;
+  if (mine) {
+    u64 cum = ex; u32 b = b0;
+    for (; b < b1; b++) { if (cum + c[b] > r) break; cum += c[b]; }
+    bb = b; cc = cum;
+  }
+  const u32 src = who ? __ffs(who) - 1 : 31;
+  if (!who && lane == 31) { bb = nb; cc = inc; }          // rank beyond the total: past the end
+  *bout = __shfl_sync(FULL_MASK, bb, src);
+  *cumout = __shfl_sync(FULL_MASK, cc, src);
+}
+// one warp per (app, field): the histogram bin holding each reported rank (and its neighbours)
 __global__ void k_q_init(u32 A, u32 nq, const u32* qppm, const u64* hist, QState* st) {
-  u32 af = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 af = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (af >= A * 4) return;
-  u32 a = af / 4, f = af % 4;
+  const u32 a = af / 4, f = af % 4;
   const u64* h = hist + ((u64)a * NF + f) * NBINS;
   u64 n = 0;
-  for (int b = 0; b < NBINS; b++) n += h[b];
+  for (int b = lane; b < NBINS; b += 32) n += h[b];
+  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(FULL_MASK, n, o);
   for (u32 q = 0; q < nq; q++) {
     u64 r[3]; double fr;
-    if (n == 0) { for (int k = 0; k < 3; k++) st[((u64)af * nq + q) * 3 + k] = QState{0, 0, 0, 0}; continue; }
+    if (n == 0) { if (lane < 3) st[((u64)af * nq + q) * 3 + lane] = QState{0, 0, 0, 0}; continue; }
     q_ranks(n, qppm[q], r, &fr);
     for (int k = 0; k < 3; k++) {
-      u64 cum = 0; int b = 0;
-      for (; b < NBINS; b++) { if (cum + h[b] > r[k]) break; cum += h[b]; }
-      st[((u64)af * nq + q) * 3 + k] = QState{bin_lo(b), r[k] - cum, bin_log2w(b), 0};
+      u32 b; u64 cum;
+      warp_rank_find(h, NBINS, r[k], &b, &cum);
+      if (lane == 0) st[((u64)af * nq + q) * 3 + k] = QState{bin_lo(b), r[k] - cum, bin_log2w(b), 0};
     }
   }
 }
@@ -666,12 +690,15 @@ __global__ void k_q_intervals(u32 A, u32 nq, const QState* st, QIv* iv, u32* niv
 
 // count pass: values inside candidate intervals -> sub-bin counters (u64)
 static const u32 NBINS_Q = 240;   // log-linear bins of a u32 value (loglin_bin < 240)
-struct QCountArgs { DTrace t; u32 tier_max, nq; const QIv* iv; const u32* niv; u64* h2; u32 a0, na; };
+struct QCountArgs { DTrace t; u32 tier_max, nq; const QIv* iv; const u32* niv; u64* h2; u32 a0, na, priv, nsub; };
 // shared memory per app of a chunk [a0, a0 + na) (the launcher chunks the apps to fit)
 __host__ __device__ __forceinline__ size_t q_count_smem_per_app(u32 nq) {
-  return (size_t)4 * (3 * nq * sizeof(QIv) + 4 + NBINS_Q + 3 * nq);
+  return (size_t)4 * (3 * nq * sizeof(QIv) + 4 + NBINS_Q + 3 * nq + 3 * nq * 4);
 }
-__global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
+// block-private sub-bin counters for the narrow (crowded) candidate intervals: <= QC_NSUB sub-bins
+// each, QC_PRIV words per block; wider intervals count straight into global memory
+static const u32 QC_PRIV = 12288, QC_NSUB = 256, QC_T = 1024;
+__global__ void __launch_bounds__(QC_T) k_q_count(QCountArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
   const u32 NA = a.na, maxi = 3 * a.nq;
   QIv* siv = (QIv*)sm;                                  // [NA*4][maxi]
@@ -682,7 +709,27 @@ __global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
   // others (intervals never straddle a bin), so a value costs one byte lookup instead of a scan
   unsigned char* tab = (unsigned char*)(sniv + NA * 4);        // [NA*4][NBINS_Q], 0xFF = none
   unsigned char* nxt = tab + (size_t)NA * 4 * NBINS_Q;          // [NA*4][maxi]
+  u32* psoff = (u32*)(((uintptr_t)(nxt + (size_t)NA * 4 * maxi) + 15) & ~(uintptr_t)15);   // [NA*4][maxi]
+  u32* spriv = psoff + NA * 4 * maxi;                           // [QC_PRIV]
   for (u32 k = threadIdx.x; k < NA * 4 * NBINS_Q; k += blockDim.x) tab[k] = 0xFF;
+  for (u32 k = threadIdx.x; k < a.priv; k += blockDim.x) spriv[k] = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {                               // private offsets: a warp scan over the intervals
+    const u32 lane = threadIdx.x, tot_iv = NA * 4 * maxi;
+    u32 base = 0;
+    for (u32 k0 = 0; k0 < tot_iv; k0 += 32) {
+      const u32 k = k0 + lane;
+      u32 want = 0;
+      if (k < tot_iv && k % maxi < sniv[k / maxi]) {
+        const u32 ns = 1u << (siv[k].w - siv[k].shift);
+        want = ns <= a.nsub ? ns : 0;
+      }
+      u32 inc = want;
+      for (int o = 1; o < 32; o <<= 1) { const u32 y = __shfl_up_sync(FULL_MASK, inc, o); if ((int)lane >= o) inc += y; }
+      if (k < tot_iv) psoff[k] = want && base + inc <= a.priv ? base + inc - want : NONE32;
+      base += __shfl_sync(FULL_MASK, inc, 31);
+    }
+  }
   __syncthreads();
   for (u32 af = threadIdx.x; af < NA * 4; af += blockDim.x)
     for (int k = (int)sniv[af] - 1; k >= 0; k--) {
@@ -703,7 +750,9 @@ __global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
       for (u32 k = tab[af * NBINS_Q + loglin_bin(v[f])]; k != 0xFF; k = nxt[af * maxi + k]) {
         const QIv& q = siv[af * maxi + k];
         if ((u64)v[f] >= q.lo && (u64)v[f] < q.lo + (1ull << q.w)) {
-          atomicAdd((unsigned long long*)&a.h2[q.off + (((u64)v[f] - q.lo) >> q.shift)], 1ull);
+          const u32 sub = (u32)(((u64)v[f] - q.lo) >> q.shift), po = psoff[af * maxi + k];
+          if (po != NONE32) atomicAdd(&spriv[po + sub], 1u);
+          else atomicAdd((unsigned long long*)&a.h2[q.off + sub], 1ull);
           break;
         }
       }
@@ -718,23 +767,35 @@ __global__ void __launch_bounds__(512) k_q_count(QCountArgs a) {
   }
   for (u64 i = n4 * 4 + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     one(__ldg(&a.t.meta[i]), __ldg(&a.t.len_in[i]), __ldg(&a.t.len_sys[i]), __ldg(&a.t.len_out[i]));
+  __syncthreads();                                      // flush the private counters (non-zero words)
+  const u32 w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (u32 k = w; k < NA * 4 * maxi; k += QC_T / 32) {
+    const u32 po = psoff[k];
+    if (po == NONE32) continue;
+    const QIv q = siv[k];
+    const u32 ns = 1u << (q.w - q.shift);
+    for (u32 jj = lane; jj < ns; jj += 32) {
+      const u32 c = spriv[po + jj];
+      if (c) atomicAdd((unsigned long long*)&a.h2[q.off + jj], (unsigned long long)c);
+    }
+  }
 }
 
 // thread per rank: narrow to the sub-bin holding it
+// one warp per rank: narrow it to the sub-bin of its interval that holds it
 __global__ void k_q_resolve(u32 A, u32 nq, QState* st, const QIv* iv, const u32* niv, const u64* h2) {
-  u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-  u32 maxi = 3 * nq;
+  const u64 r = ((u64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const u32 maxi = 3 * nq, lane = threadIdx.x & 31;
   if (r >= (u64)A * 4 * maxi) return;
   QState s = st[r];
   if (s.w == 0) return;
-  u32 af = (u32)(r / maxi);
+  const u32 af = (u32)(r / maxi);
   for (u32 k = 0; k < niv[af]; k++) {
-    QIv q = iv[(u64)af * maxi + k];
+    const QIv q = iv[(u64)af * maxi + k];
     if (q.lo != s.lo || q.w != s.w) continue;
-    u64 nb = 1ull << (q.w - q.shift), cum = 0, b = 0;
-    for (; b < nb; b++) { u64 c = h2[q.off + b]; if (cum + c > s.rw) break; cum += c; }
-    s.lo += b << q.shift; s.rw -= cum; s.w = q.shift;
-    st[r] = s;
+    u32 b; u64 cum;
+    warp_rank_find(h2 + q.off, 1u << (q.w - q.shift), s.rw, &b, &cum);
+    if (lane == 0) { s.lo += (u64)b << q.shift; s.rw -= cum; s.w = q.shift; st[r] = s; }
     return;
   }
 }
