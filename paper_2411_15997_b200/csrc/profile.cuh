@@ -405,7 +405,7 @@ static size_t seg_win_smem(u32 A) { return (size_t)(SW_T / 32) * sw_stride(A); }
 // Peaks combine across pieces with atomicMax (tables zeroed beforehand).
 static const int WP_T = 128, WP_CH = 2048, WP_R = 512;
 __host__ __device__ __forceinline__ size_t wp_stride(u32 A) {
-  return ((size_t)A * 24 + ((A + 31) / 32) * 4 + (size_t)WP_R * 21 + 15) / 16 * 16;
+  return ((size_t)A * 24 + ((A + 31) / 32) * 4 + (size_t)WP_R * 13 + 15) / 16 * 16;
 }
 static size_t win_pieces_smem(u32 A) { return (size_t)(WP_T / 32) * wp_stride(A); }
 __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ SegWinArgs a, u64 n) {
@@ -413,11 +413,14 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
   const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5, A = a.A, J1 = a.J + 1;
   const u32 nwords = (A + 31) / 32;
   unsigned char* mine = smw + (size_t)wid * wp_stride(A);
-  u64* r_pt = (u64*)mine;                      // ring: segment tau prefix
-  u64* r_pta = r_pt + WP_R;                    //       app tau prefix
-  u64* tab_t = r_pta + WP_R;                   // app tau since h
+  // ring prefixes are kept mod 2^32: a window's token load is a difference of two of them and is
+  // below the piece's total since h, which is checked to stay below 2^32 (else the segment goes to
+  // k_useg_win); 13 B per ring entry instead of 21 lets more warps share an SM
+  u64* tab_t = (u64*)mine;                     // app tau since h
   u64* tab_pt = tab_t + A;                     // app token peak
-  u32* r_ca = (u32*)(tab_pt + A);              // ring: app rank
+  u32* r_pt = (u32*)(tab_pt + A);              // ring: segment tau prefix (mod 2^32)
+  u32* r_pta = r_pt + WP_R;                    //       app tau prefix (mod 2^32)
+  u32* r_ca = r_pta + WP_R;                    // ring: app rank
   u32* tab_c = r_ca + WP_R;                    // app calls since h
   u32* tab_pr = tab_c + A;                     // app request peak
   u32* touched = tab_pr + A;
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
         __syncwarp();
         if (ok) {
           const u32 slot = (u32)(p & (WP_R - 1));
-          r_pt[slot] = ex; r_pta[slot] = ptav; r_ca[slot] = cav; r_app[slot] = (unsigned char)app;
+          r_pt[slot] = (u32)ex; r_pta[slot] = (u32)ptav; r_ca[slot] = cav; r_app[slot] = (unsigned char)app;
         }
         if (ok && lane == (u32)(__ffs(peers) - 1)) {
           tab_c[app] = bc + __popc(peers); tab_t[app] = bt + gtot;
@@ -534,13 +537,12 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
         tprev = tlast;
         lbw = max(lbw, __shfl_sync(FULL_MASK, real ? lb : 0, 31));
         const u64 ring_lo = c0 + 32 > (u64)WP_R ? c0 + 32 - WP_R : 0;   // oldest position still in the ring
-        const bool miss = far && lb < ring_lo;
+        const bool miss = far && (lb < ring_lo || (carry >> 32) != 0);   // (mod-2^32 ring prefixes)
         if (__any_sync(FULL_MASK, miss)) { over = true; break; }
         const u32 ln = far ? 0 : (u32)(lb - c0);
         const u64 ex_lb = __shfl_sync(FULL_MASK, ex, ln);
-        const u64 pt_lb = far ? r_pt[lb & (WP_R - 1)] : ex_lb;
         const u32 n_g = (u32)(p - lb + 1);
-        const u64 tau_g = ex + tau - pt_lb;
+        const u64 tau_g = far ? (u64)((u32)(ex + tau) - r_pt[lb & (WP_R - 1)]) : ex + tau - ex_lb;
         u32 qlane = __ffs(peers & ~((1u << ln) - 1u)) - 1;
         bool qfar = false; u64 q = lb;
         if (far) {
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(WP_T) k_win_pieces(const __grid_constant__ Seg
         const u32 ca_q = __shfl_sync(FULL_MASK, cav, qlane);
         const u64 pta_q = __shfl_sync(FULL_MASK, ptav, qlane);
         u32 n_a; u64 tau_a;
-        if (qfar) { n_a = cav - r_ca[q & (WP_R - 1)] + 1; tau_a = ptav + tau - r_pta[q & (WP_R - 1)]; }
+        if (qfar) { n_a = cav - r_ca[q & (WP_R - 1)] + 1; tau_a = (u64)((u32)(ptav + tau) - r_pta[q & (WP_R - 1)]); }
         else { n_a = cav - ca_q + 1; tau_a = ptav + tau - pta_q; }
         if (real) { mr = max(mr, n_g); mt = max(mt, tau_g); }
         const u32 rm = peers & __ballot_sync(FULL_MASK, real);
