@@ -85,13 +85,6 @@ struct OsPassArgs {
   const u32* off;                             // [R][ntiles] exclusive scan of the tile histograms
 };
 
-// lanes of the warp (ok lanes only) holding the same digit of `bits` bits: bit-sliced ballots
-__device__ __forceinline__ u32 os_peers(u32 d, bool ok, int bits) {
-  u32 peers = __ballot_sync(FULL_MASK, ok);
-  for (int b = 0; b < bits; b++) {
-    u32 bb = __ballot_sync(FULL_MASK, (d >> b) & 1u);
-    peers &= ((d >> b) & 1u) ? bb : ~bb;
-  }
   return peers;
 }
 
@@ -106,7 +99,6 @@ __global__ void __launch_bounds__(OS_T, 2) k_os_pass(const __grid_constant__ OsP
   const u32 tile = blockIdx.x, R = a.R, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (u32 d = threadIdx.x; d < R; d += OS_T) gdst[d] = a.off[(u64)d * a.ntiles + tile];
   __syncthreads();
-  const int bits = 31 - __clz(R);
   const u64 base = (u64)tile * OS_TILE + (u64)w * (OS_IPT * 32);
   uint4 it[OS_IPT];
   u32 dg[OS_IPT], rk[OS_IPT];
@@ -157,7 +149,7 @@ __global__ void __launch_bounds__(OS_T, 2) k_os_pass(const __grid_constant__ OsP
   for (int r = 0; r < OS_IPT; r++) {
     const bool ok = it[r].w != 0xFFFFFFFFu;
     const u32 d = ok ? (it[r].z >> a.shift) & (R - 1) : 0;
-    u32 peers = os_peers(d, ok, bits);
+    u32 peers = __match_any_sync(FULL_MASK, ok ? d : 0xFFFFFFFFu);   // stable: rank = lanes below with d
     u32 pre = 0;
     if (ok) pre = wcnt[w][d];
     __syncwarp();

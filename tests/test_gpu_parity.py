@@ -194,6 +194,28 @@ def _cmp_profile_shard(gpr, op, nq, mine):
     _cmp_profile(g, op, nq)
 
 
+def test_profile_window_load_over_2_32(F, ctx):
+    """A user whose window token load passes 2^32 (400 calls of 16M input tokens inside 60 s): the
+    window pieces keep ring prefixes mod 2^32 and must hand that user to the exact u64 kernel;
+    peaks and limits equal the oracle's."""
+    from paper_2411_15997_b200.tracegen import from_columns
+    rows = []
+    for k in range(400):
+        rows.append(dict(user=0, t_ms=10 * k, app=0, inter=0, stage=1, ncalls=1, len_in=16_000_000, len_sys=0,
+                         len_out=1, think_ms=0, tier=0))
+    for k in range(300):
+        rows.append(dict(user=1 + k % 3, t_ms=5 * k + 1, app=1, inter=0, stage=1, ncalls=1, len_in=100 + k,
+                         len_sys=7, len_out=20, think_ms=0, tier=0))
+    rows.sort(key=lambda r: r["t_ms"])
+    for x, r in enumerate(rows):
+        r["inter"] = x
+    tr = from_columns(4, 2, rows)
+    cfg = dict(tier_max=255)
+    op = O.profile(tr, cfg)
+    assert int(op["peak_t_u"][0]) >= 1 << 32
+    _cmp_profile(F.build_app_profiles(ctx, F.Trace(tr), cfg).read(), op, 5)
+
+
 def test_profile_many_apps(F, ctx):
     """A = 200 apps at J = 64: the Eq. 2 sums (200 x 65 x 4 u64) do not fit shared memory (global
     atomics), the histograms and the quantile tables run in app chunks; same profile as the oracle."""
