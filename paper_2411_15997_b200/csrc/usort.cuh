@@ -13,8 +13,9 @@
 //                   user + meta of the trace, later passes the items' user word), digit-major
 //   excl_scan       over [digit][tile]: every (tile, digit)'s global destination
 //   k_os_pass       per tile: load (pass 0 from the trace's SoA fields, later passes from the
-//                   previous pass's items), rank every item stably in the tile (bit-sliced
-//                   ballots per warp round), then stage the tile in shared memory in digit order
+//                   previous pass's items), rank every item stably in the tile (__match_any_sync
+//                   per warp round: lanes below with the same digit), then stage the tile in shared
+//                   memory in digit order
 //                   so that consecutive threads store consecutive addresses of a digit's run.
 //                   No tile waits on another (a decoupled look-back here serialised the tiles:
 //                   its chain of inclusive prefixes advanced a few tiles per L2 round trip).
@@ -84,9 +85,6 @@ struct OsPassArgs {
   uint4* out; int shift; u32 R, ntiles;
   const u32* off;                             // [R][ntiles] exclusive scan of the tile histograms
 };
-
-  return peers;
-}
 
 template <bool FIRST>
 __global__ void __launch_bounds__(OS_T, 2) k_os_pass(const __grid_constant__ OsPassArgs a) {
