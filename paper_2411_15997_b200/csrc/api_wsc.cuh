@@ -432,13 +432,14 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
     // queued-continuation pool: same two-step capacity (n_inters is an exact bound)
     const bool ag = wi && cfg->act.app_scope == FS_SCOPE_APP_GLOBAL;
     const u32 all = (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull);        // exact log capacities
+    const bool base = cfg->mode >= FS_MODE_VTC || ag;
+    const int tour = base || !rwarp || cfg->max_batch > 1024 ? 0 : tour_bits(6);   // warp-parallel engine pieces
     EngLayout L = eng_layout(t.U, p_cap, W.n_heads, cfg->max_batch, p_cap, AJ, wi, W.ring_slots, !rwarp, budget,
-                             cfg->mode >= FS_MODE_VTC, cfg->mode == FS_MODE_RPM ? all : 0, t.A, ag ? all : 0);
+                             cfg->mode >= FS_MODE_VTC, cfg->mode == FS_MODE_RPM ? all : 0, t.A, ag ? all : 0,
+                             (tour & 2) != 0);
     unsigned char* gm = S.alloc<unsigned char>(L.bytes_glob + 256);
     if (S.failed) return FS_E_NOMEM;
     ReplayKArgs a{W.sh, ec, L, eo, t.U, gm, dsum, dcode, didx, p_cap};
-    const bool base = cfg->mode >= FS_MODE_VTC || ag;
-    const int tour = base || cfg->max_batch > 1024 ? 0 : tour_bits(6);   // warp-parallel engine pieces
     ReplayFn rk = rwarp ? (base ? k_replay_warp<true, 0> : replay_warp_kern_t(tour)) : (base ? k_replay<true> : k_replay<false>);
     cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.bytes_smem);
     FS_LAUNCH(ctx, "wsc_replay", rk, 1, rwarp ? 32 : 64, L.bytes_smem, a);
@@ -541,10 +542,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   if (S.failed) return FS_E_NOMEM;
   cudaMemcpyAsync(dc, hc.data(), ns * sizeof(EngCfg), cudaMemcpyHostToDevice, ctx->stream);
   u32 p_cap = std::max<u32>(std::min<u32>(t.X, 1u << 16), 1);
-  EngLayout L = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi,
-                           W.ring_slots, false, 0, any_dq, any_rpm ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0, t.A,
-                           any_ag ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0);
-  size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
+
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   // one scenario slot per group of LPS lanes (FS_SWEEP_LPS: 32 = a warp, 16, 8); FS_SWEEP_MINB
@@ -555,6 +553,11 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   // (FS_SWEEP_LPS = 16 / 8, several replays per warp, measured slower: FS-mode engine only)
   const bool base = any_dq || any_ag;
   const int tour = base || lps < 32 || Bmax > 1024 ? 0 : tour_bits(0);   // warp-parallel engine pieces
+  EngLayout L = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi,
+                           W.ring_slots, false, 0, any_dq, any_rpm ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0, t.A,
+                           any_ag ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0,
+                           (tour & 2) != 0);
+  const size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   SweepFn kern = base ? (minb >= 6 ? k_sweep<6, 32, true, 0> : minb == 5 ? k_sweep<5, 32, true, 0> :
                            minb == 4 ? k_sweep<4, 32, true, 0> : k_sweep<3, 32, true, 0>)
                : lps <= 8 ? k_sweep<4, 8, false, 0> : lps == 16 ? k_sweep<4, 16, false, 0> : sweep_kern_t(tour, minb);
@@ -616,7 +619,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
     if (rc) return rc;
     const u32 p2 = std::max<u32>(t.X, 1), all = (u32)std::min<u64>(t.n + 1, 0xFFFFFFFFull);
     EngLayout L2 = eng_layout(t.U, p2, W.n_heads, Bmax, p2, AJ, any_wi, ring2, false, 0, any_dq, any_rpm ? all : 0, t.A,
-                              any_ag ? all : 0);
+                              any_ag ? all : 0, (tour & 2) != 0);
     const size_t sb2 = (L2.bytes_glob + 255) / 256 * 256;
     cudaMemGetInfo(&free_b, &total_b);
     u64 sl2 = std::min<u64>(std::min<u64>(nr, slots), (u64)(free_b / 2) / std::max<size_t>(sb2, 1));

@@ -148,8 +148,9 @@ struct EngineT {
   fs_replay_summary sum;
   int err_code; u64 err_idx;
   // TB: this lane's B slots {lane + 32 j}
-  u64 lfi; u32 locc;                     // minimum finish iteration of the lane's slots, occupied slots
-  u32 bf_top;                            // free B-slot stack
+  struct LaneSlots { u64 lfi; u32 locc, bf_top; };   // min finish iteration of the lane's slots, occupied
+  struct NoSlots {};                                 // slots, free B-slot stack (TB engines only)
+  typename std::conditional<TB, LaneSlots, NoSlots>::type ls;
   __device__ __forceinline__ static u64 mn64(u64 a, u64 b) { return a < b ? a : b; }
   __device__ __forceinline__ static u64 warp_min64(u64 v) {
     const u32 hi = (u32)(v >> 32);
@@ -218,7 +219,7 @@ struct EngineT {
     hb_i = hb_n = 0; rf_head = rf_len = 0; ag_head = ag_len = 0;
     memset(&sum, 0, sizeof(sum));
     err_code = 0; err_idx = 0;
-    lfi = ~0ull; locc = 0; bf_top = st.b_cap;
+    if constexpr (TB) { ls.lfi = ~0ull; ls.locc = 0; ls.bf_top = st.b_cap; }
   }
 
   // ---------------------------------------------------------------- Eq. 3 (l.44-48)
@@ -270,7 +271,9 @@ struct EngineT {
 
   // ---------------------------------------------------------------- ACT window check (l.19-24)
   __device__ __forceinline__ int act_check(UState& us, u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
-    if (TA && !c->heads_only) {                          // the lanes split the ring
+    bool ring_done = false;
+    if constexpr (TA) {
+     if (!c->heads_only) {                               // the lanes split the ring
       const u64 base = sh->r_off[k]; const u32 cap = (u32)(sh->r_off[k + 1] - base);
       const u32 lane = threadIdx.x & 31;
       const i64 lim = tr - c->Wns;
@@ -297,7 +300,10 @@ struct EngineT {
         for (int o = 16; o; o >>= 1) { ct += __shfl_xor_sync(FULL_MASK, ct, o); cta += __shfl_xor_sync(FULL_MASK, cta, o); }
         t_g += ct; t_a += cta;
       }
-    } else if (!c->heads_only || !static_heads) {
+      ring_done = true;
+     }
+    }
+    if (!ring_done && (!c->heads_only || !static_heads)) {
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
       u32 h = us.r_head, len = us.r_len;
       while (len && s.r[base + h].t <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // (Q4)
@@ -497,8 +503,7 @@ struct EngineT {
     CSlot cs;
     if (cont) cs = s.cs[x];
     u32 r = cont ? us.cf : us.hf;                            // no dependent load on the slot
-    uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = make_uint4(0, 0, 0, 0);
-    if (!c->inc) Cc = ldg4(&sh->recC[r]);                  // only Eq. 3 on the fly needs slot, L_I, L_S
+    uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
     u64 inc_pre = c->inc ? c->inc[r] : 0;
     u64 need = (u64)B.y + B.w;
     us.nf = (u32)need;
@@ -666,12 +671,12 @@ struct EngineT {
   // B heap keyed (finish iteration, id)
   __device__ __forceinline__ static bool bless(const BEnt& a, const BEnt& b) { return a.fi < b.fi || (a.fi == b.fi && a.r < b.r); }
   __device__ __forceinline__ void b_push(const BEnt& x) {
-    if (TB) {                                            // a free slot; its lane's minimum, bfi
-      const u32 sl = s.bfree[--bf_top];
+    if constexpr (TB) {                                  // a free slot; its lane's minimum, bfi
+      const u32 sl = s.bfree[--ls.bf_top];
       s.b[sl] = x;
       BKey kk; kk.fi = x.fi; kk.r = x.r; kk.pad = 0;
       s.bk[sl] = kk;
-      if ((threadIdx.x & 31) == (sl & 31)) { locc |= 1u << (sl >> 5); lfi = mn64(lfi, x.fi); }
+      if ((threadIdx.x & 31) == (sl & 31)) { ls.locc |= 1u << (sl >> 5); ls.lfi = mn64(ls.lfi, x.fi); }
       bfi = b_n == 0 ? x.fi : mn64(bfi, x.fi);
       b_n++;
       return;
@@ -804,13 +809,14 @@ struct EngineT {
       occ += (i64)(m * b_n);
       sum.sum_ttft_ns += (u64)nl_n * (u64)clock - arr_sum;       // sum of (first token - arrival), mod 2^64
       if (o.first) for (u32 q = 0; q < nl_n; q++) o.first[s.nl_id[q]] = clock;
-      if (TB && bfi == iter - 1) {                              // finishes (l.43-48), warp batch
+      if constexpr (TB) {
+       if (bfi == iter - 1) {                                     // finishes (l.43-48), warp batch
         bool pushed = false;
         const u64 fin = iter - 1;
         const u32 lane = threadIdx.x & 31;
         u32 fm = 0;                                               // the lane's finishing slots
-        if (lfi == fin)
-          for (u32 mm = locc; mm; mm &= mm - 1) { const u32 j = __ffs(mm) - 1; if (s.bk[lane + 32 * j].fi == fin) fm |= 1u << j; }
+        if (ls.lfi == fin)
+          for (u32 mm = ls.locc; mm; mm &= mm - 1) { const u32 j = __ffs(mm) - 1; if (s.bk[lane + 32 * j].fi == fin) fm |= 1u << j; }
         for (;;) {                                                // in call order (the oracle sorts them)
           u32 myr = NONE32, mys = 0;
           for (u32 mm = fm; mm; mm &= mm - 1) {
@@ -821,9 +827,9 @@ struct EngineT {
           if (mr == NONE32) break;
           const u32 w = __ffs(__ballot_sync(FULL_MASK, myr == mr)) - 1;
           const u32 sl = __shfl_sync(FULL_MASK, mys, w);
-          if (lane == w) { fm &= ~(1u << (sl >> 5)); locc &= ~(1u << (sl >> 5)); }
+          if (lane == w) { fm &= ~(1u << (sl >> 5)); ls.locc &= ~(1u << (sl >> 5)); }
           const BEnt f = s.b[sl];
-          s.bfree[bf_top++] = sl;
+          s.bfree[ls.bf_top++] = sl;
           b_n--;
           dB -= dec;
           if (o.finish) o.finish[f.r] = clock;
@@ -836,14 +842,15 @@ struct EngineT {
             pushed = true;
           }
         }
-        if (lfi == fin) {                                         // the finishing lanes' new minima
-          lfi = ~0ull;
-          for (u32 mm = locc; mm; mm &= mm - 1) lfi = mn64(lfi, s.bk[lane + 32 * (__ffs(mm) - 1)].fi);
+        if (ls.lfi == fin) {                                      // the finishing lanes' new minima
+          ls.lfi = ~0ull;
+          for (u32 mm = ls.locc; mm; mm &= mm - 1) ls.lfi = mn64(ls.lfi, s.bk[lane + 32 * (__ffs(mm) - 1)].fi);
         }
-        bfi = b_n ? warp_min64(lfi) : 0;
+        bfi = b_n ? warp_min64(ls.lfi) : 0;
         pick_blocked = false;
         if (pushed) { p_front(); next_arrival(); }
-      } else if (!TB && bfi == iter - 1) {                      // finishes (l.43-48)
+       }
+      } else if (bfi == iter - 1) {                               // finishes (l.43-48)
         bool pushed = false;
         do {
           BEnt f = s.b[0];
@@ -944,7 +951,7 @@ struct EngLayout {
 // hseq: per-head delivery seqs (VTC / RPM / FCFS); rf_cap > 0: the RPM window log + per-app counts
 static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, u64 AJ, bool act_ring, u64 ring_slots,
                             bool hring, size_t smem_budget, bool hseq = false, u32 rf_cap = 0, u32 A = 0,
-                            u32 ag_cap = 0) {
+                            u32 ag_cap = 0, bool lane_batch = false) {
   size_t sz[L_N];
   sz[L_HR] = hring ? (size_t)HRING * (sizeof(HEnt) + 8) + 64 : 0;
   sz[L_B] = (size_t)Bmax * sizeof(BEnt); sz[L_NLID] = (size_t)Bmax * 4; sz[L_NLARR] = (size_t)Bmax * 8;
@@ -960,12 +967,12 @@ static EngLayout eng_layout(u32 U, u64 slots, u64 n_heads, u32 Bmax, u32 p_cap, 
   sz[L_RAPP] = rf_cap ? (size_t)A * 4 : 0;
   sz[L_AG] = (size_t)ag_cap * sizeof(AGEnt);
   sz[L_AGS] = ag_cap ? (size_t)A * sizeof(AGSum) : 0;
-  sz[L_BK] = (size_t)Bmax * sizeof(BKey); sz[L_BF] = (size_t)Bmax * 4;
+  sz[L_BK] = lane_batch ? (size_t)Bmax * sizeof(BKey) : 0; sz[L_BF] = lane_batch ? (size_t)Bmax * 4 : 0;
   // shared-memory priority: hottest first (the head ring must be shared)
   static const int prio[] = {L_HR, L_BK, L_BF, L_B, L_NLID, L_NLARR, L_W, L_P, L_HPOS, L_RAPP, L_AGS, L_US, L_HK,
                              L_HM, L_CS, L_CF};
   EngLayout L;
-  L.c_cap = (u32)slots; L.b_cap = Bmax;
+  L.c_cap = (u32)slots; L.b_cap = lane_batch ? Bmax : 0;
   L.rf_cap = rf_cap; L.A = A; L.ag_cap = ag_cap;
   for (int k = 0; k < L_N; k++) L.smem[k] = false;
   for (int k : prio) {
