@@ -358,6 +358,207 @@ __global__ void __launch_bounds__(UJ_T) k_act_user_jacobi(ActUserJacobiArgs a) {
   if (threadIdx.x == 0) atomicMax(a.iters, it_max);
 }
 
+// ------------------------------------------------------------------ per-user sequential walk (one warp per user)
+// The users still changing after the global passes: one warp walks the user's (t, id) order 32
+// positions at a time, in order (the sequential definition, batched).  Every position
+// before the batch is final, so a batch depends only on final values and on itself: it iterates
+// (counted flags -> warp scans -> decisions of its overloaded heads) until nothing changes -- one
+// round per in-batch head -> continuation link at most -- then records its prefixes and decisions
+// and moves on.  All n_a / t_a lookups are made in the u order too: the window's first same-app
+// call sits at a u position (lbau), and the prefix kept per position is that position's own-app
+// prefix, so one shared-memory ring of the last UW_R positions serves every window lookup (the
+// global arrays only when a window reaches further back).
+//   k_act_walk_prep  per position of the walked users, coalesced output: {lbu, lbau} (u positions
+//                    of the window's first call / first same-app call), the continuation's head
+//                    position, {app, checked, start status}; the user's farthest lookback
+//   k_act_user_walk  the walk: per batch, one coalesced record load (prefetched a batch ahead),
+//                    ring lookups, warp scans
+static const int UW_R = 1024, UW_AMAX = 256;
+struct ActWalkPrepArgs {
+  const u32* users; const u64* seg_u; const u32* perm_u; const u32* pos_u; const u32* pos_ua; const u32* perm_ua;
+  const uint2* pre_u; const u64* lb_ua; const u32* meta; const uint8_t* ovl; const uint8_t* status;
+  u64* lbx;                    // in: lb_u (heads), out: lbu | lbau << 32   (the u order's lb array, reused)
+  u32* hpx; u32* ax; u32* far; // continuation's head position (NONE), app | chk << 8 | status << 16; per user
+};
+__global__ void __launch_bounds__(256) k_act_walk_prep(const ActWalkPrepArgs a) {
+  const u32 u = a.users[blockIdx.x];
+  const u64 s = a.seg_u[u], e = a.seg_u[u + 1];
+  u32 fr = 0;
+  for (u64 p = s + (u64)blockIdx.y * blockDim.x + threadIdx.x; p < e; p += (u64)gridDim.y * blockDim.x) {
+    const uint2 v = a.pre_u[p];
+    const u32 i = a.perm_u[p];
+    const u32 app = m_app(a.meta[i]);
+    const bool chk = v.x == ACT_HEAD && (!a.ovl || a.ovl[i]);
+    u32 lbu = (u32)p, lbau = (u32)p;
+    if (chk) {
+      lbu = (u32)a.lbx[p];
+      lbau = a.pos_u[a.perm_ua[a.lb_ua[a.pos_ua[i]]]];
+      fr = max(fr, (u32)p - min(lbu, lbau));
+    }
+    a.lbx[p] = (u64)lbu | (u64)lbau << 32;
+    a.hpx[p] = v.x != NONE32 && v.x != ACT_HEAD ? a.pos_u[v.x] : NONE32;
+    a.ax[p] = app | (u32)chk << 8 | (u32)a.status[i] << 16;
+  }
+  for (int o = 16; o; o >>= 1) fr = max(fr, __shfl_xor_sync(FULL_MASK, fr, o));
+  if ((threadIdx.x & 31) == 0 && fr) atomicMax(&a.far[blockIdx.x], fr);
+}
+struct ActUserWalkArgs {
+  const u32* users; u32 n_users_w; u32 A;
+  const u64* seg_u; const u32* perm_u; const uint2* pre_u;
+  const u64* lbx; const u32* hpx; const u32* ax; const u32* far;
+  u32* pc_u; u64* ptau_u; u32* pc_au; u64* ptau_au;   // far lookups: prefixes by u position (scratch)
+  const uint8_t* ovl; const DLimits* L; const u32* ra; const u64* ta;
+  uint8_t* status; u32* iters;
+};
+struct UWPos { uint2 v; u32 i, ax, hp; u64 lb; };
+__device__ __forceinline__ void uw_load(const ActUserWalkArgs& a, u64 p, u64 e, UWPos& x) {
+  if (p < e) { x.v = a.pre_u[p]; x.i = a.perm_u[p]; x.ax = a.ax[p]; x.hp = a.hpx[p]; x.lb = a.lbx[p]; }
+  else { x.v = make_uint2(NONE32, 0u); x.i = 0; x.ax = 0xFFu; x.hp = NONE32; x.lb = 0; }
+}
+__device__ __forceinline__ u64 warp_excl_scan64(u64 v, u32 lane) {
+  u64 x = v;
+#pragma unroll
+  for (u32 o = 1; o < 32; o <<= 1) { const u64 y = __shfl_up_sync(FULL_MASK, x, o); if (lane >= o) x += y; }
+  return x - v;
+}
+__global__ void __launch_bounds__(32) k_act_user_walk(const ActUserWalkArgs a) {
+  __shared__ u32 r_ec[UW_R], r_eca[UW_R];        // ring of the last UW_R positions: exclusive prefixes
+  __shared__ u64 r_et[UW_R], r_eta[UW_R];        //   (u order, own app), and statuses
+  __shared__ uint8_t r_st[UW_R];
+  __shared__ u32 acnt[UW_AMAX];                  // per-app carries
+  __shared__ u64 atau[UW_AMAX];
+  __shared__ u32 sidx[32];                       // the batch's lanes in (app, lane) order
+  const u32 lane = threadIdx.x;
+  const u32 u = a.users[blockIdx.x];
+  for (u32 k = lane; k < a.A; k += 32) { acnt[k] = 0; atau[k] = 0; }
+  __syncwarp();
+  const u64 s = a.seg_u[u], e = a.seg_u[u + 1];
+  const bool gfar = a.far[blockIdx.x] + 32 > UW_R;   // some window reaches past the ring: keep global copies
+  const DLimits L = *a.L;
+  const u32 lt = lanemask_lt();
+  u32 cu = 0; u64 tu = 0;                        // u-order carries (counted calls, token load)
+  u32 it_max = 0;
+  UWPos nx, nx2;                                 // the next two batches (loads two batches ahead)
+  uw_load(a, s + lane, e, nx);
+  uw_load(a, s + 32 + lane, e, nx2);
+  for (u64 p0 = s; p0 < e; p0 += 32) {
+    const UWPos x = nx;
+    const u64 p = p0 + lane;
+    const bool in = p < e;
+    nx = nx2;
+    if (p0 + 64 < e) uw_load(a, p0 + 64 + lane, e, nx2);
+    const u32 app = x.ax & 0xFFu;
+    const bool chk = (x.ax >> 8) & 1u;
+    const u32 peers = __match_any_sync(FULL_MASK, in ? app : NONE32);
+    const u32 leaders = __ballot_sync(FULL_MASK, in && (peers & lt) == 0);
+    const u32 inmask = __ballot_sync(FULL_MASK, in);
+    const u64 lbu = (u32)x.lb, lbau = (u32)(x.lb >> 32);
+    const bool lbu_in = lbu >= p0, lba_in = lbau >= p0;
+    // final values before the batch: the ring, else the global copies
+    u32 gc_u = 0, gc_a = 0; u64 gt_u = 0, gt_a = 0;
+    if (chk && !lbu_in) {
+      if (lbu + UW_R >= p0) { const u32 k = (u32)lbu & (UW_R - 1); gc_u = r_ec[k]; gt_u = r_et[k]; }
+      else { gc_u = a.pc_u[lbu]; gt_u = a.ptau_u[lbu]; }
+    }
+    if (chk && !lba_in) {
+      if (lbau + UW_R >= p0) { const u32 k = (u32)lbau & (UW_R - 1); gc_a = r_eca[k]; gt_a = r_eta[k]; }
+      else { gc_a = a.pc_au[lbau]; gt_a = a.ptau_au[lbau]; }
+    }
+    const bool cont = x.hp != NONE32;
+    const bool hin = cont && (u64)x.hp >= p0 && (u64)x.hp < p0 + 32;
+    bool hfin = false;
+    if (cont && !hin) {
+      if ((u64)x.hp < p0 && (u64)x.hp + UW_R >= p0) hfin = r_st[x.hp & (UW_R - 1)] == FS_ST_ADMIT;
+      else hfin = a.status[x.v.x] == FS_ST_ADMIT;    // far back, or a never-arrived head (sorted last)
+    }
+    const u32 ca = in ? acnt[app] : 0u;
+    const u64 cta = in ? atau[app] : 0ull;
+    const u32 su = chk && lbu_in ? (u32)(lbu - p0) : lane;
+    const u32 sa = chk && lba_in ? (u32)(lbau - p0) : lane;
+    const u32 hsrc = hin ? (u32)((u64)x.hp - p0) : lane;
+    const bool small = __all_sync(FULL_MASK, x.v.y < (1u << 26));     // 32 loads sum below 2^31: u32 scans
+    // lanes in (app, lane) order (static over the batch's iterations): the own-app token prefixes are
+    // one segmented scan in that order -- srank: my place, src: the lane at place `lane`, sst: where
+    // the app's run starts in that order
+    u32 srank = 0, src = lane, sst = 0;
+    const bool multi = (leaders & (leaders - 1)) != 0;
+    if (multi) {
+      u32 below = 0;                                                // lanes of smaller apps (out-of-batch lanes: last)
+      for (u32 lm = leaders; lm; lm &= lm - 1) {
+        const u32 ld = __ffs(lm) - 1;
+        const u32 la = __shfl_sync(FULL_MASK, app, ld), lp = __shfl_sync(FULL_MASK, peers, ld);
+        if (in && la < app) below += __popc(lp);
+      }
+      if (!in) below = __popc(inmask);
+      srank = below + __popc(peers & lt);
+      sidx[srank] = lane;
+      __syncwarp();
+      src = sidx[lane];
+      sst = __shfl_sync(FULL_MASK, below, src);
+      __syncwarp();
+    }
+    u32 st = (x.ax >> 16) & 0xFFu, it = 0, fm, ec, eca, tv;
+    const u32 st0 = st;
+    u64 et, eta;
+    for (;;) {
+      const u32 hst = __shfl_sync(FULL_MASK, st, hsrc);
+      const bool f = x.v.x == ACT_HEAD || (cont && (hin ? hst == FS_ST_ADMIT : hfin));
+      tv = f ? x.v.y : 0u;
+      fm = __ballot_sync(FULL_MASK, f);
+      ec = cu + __popc(fm & lt);
+      u64 ex;
+      if (small) {
+        u32 xs = tv;
+#pragma unroll
+        for (u32 o = 1; o < 32; o <<= 1) { const u32 y = __shfl_up_sync(FULL_MASK, xs, o); if (lane >= o) xs += y; }
+        ex = xs - tv;
+      } else ex = warp_excl_scan64(tv, lane);
+      et = tu + ex;
+      eca = ca + __popc(fm & peers & lt);
+      if (!multi) eta = cta + ex;                                  // one app in the batch
+      else {                                                        // segmented scan in (app, lane) order
+        const u32 y0 = __shfl_sync(FULL_MASK, tv, src);
+        u64 y = y0;
+#pragma unroll
+        for (u32 o = 1; o < 32; o <<= 1) { const u64 z = __shfl_up_sync(FULL_MASK, y, o); if (lane >= sst + o) y += z; }
+        eta = cta + __shfl_sync(FULL_MASK, y - y0, srank);
+      }
+      u32 lc = __shfl_sync(FULL_MASK, ec, su); u64 ltt = __shfl_sync(FULL_MASK, et, su);
+      u32 lac = __shfl_sync(FULL_MASK, eca, sa); u64 lat = __shfl_sync(FULL_MASK, eta, sa);
+      u32 nst = st;
+      if (chk) {                                                    // Alg. 1 l.20-24
+        if (!lbu_in) { lc = gc_u; ltt = gt_u; }
+        if (!lba_in) { lac = gc_a; lat = gt_a; }
+        const u64 n_g = (u64)ec + 1 - lc, t_g = et + x.v.y - ltt;
+        const u64 n_a = (u64)eca + 1 - lac, t_a = eta + x.v.y - lat;
+        nst = FS_ST_ADMIT;
+        if (L.rg && n_g > L.rg) nst = FS_ST_BLOCK_USER_REQ;
+        else if (L.tg && t_g > L.tg) nst = FS_ST_BLOCK_USER_TOK;
+        else if (a.ra[app] && n_a > a.ra[app]) nst = FS_ST_BLOCK_APP_REQ;
+        else if (a.ta[app] && t_a > a.ta[app]) nst = FS_ST_BLOCK_APP_TOK;
+      }
+      const bool ch = __any_sync(FULL_MASK, nst != st);
+      st = nst;
+      it++;
+      if (!ch) break;
+    }
+    const u32 fb = (fm >> lane) & 1u;
+    if (in) {
+      const u32 k = (u32)p & (UW_R - 1);
+      r_ec[k] = ec; r_et[k] = et; r_eca[k] = eca; r_eta[k] = eta; r_st[k] = (uint8_t)st;
+      if (gfar) { a.pc_u[p] = ec; a.ptau_u[p] = et; a.pc_au[p] = eca; a.ptau_au[p] = eta; }
+      if (chk && st != st0) a.status[x.i] = (uint8_t)st;
+      if ((peers >> lane) == 1u) { acnt[app] = eca + fb; atau[app] = eta + tv; }   // the app's last lane
+    }
+    const u32 last = 31 - __clz(inmask);
+    cu = __shfl_sync(FULL_MASK, ec + fb, last);
+    tu = __shfl_sync(FULL_MASK, et + tv, last);
+    __syncwarp();
+    if (it > it_max) it_max = it;
+  }
+  if (lane == 0) atomicMax(a.iters, it_max);
+}
+
 __global__ void k_act_list(u32 U, const u32* uchg, u32* list, u32* n) {
   u32 u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u < U && uchg[u]) list[atomicAdd(n, 1u)] = u;

@@ -493,7 +493,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
       break;
     }
   WscShared W;
-  if (!wsc_shared(ctx, S, t, P, win, any_wi, SWEEP_RING_CAP, &W, tw)) return FS_E_NOMEM;
+  static const u64 ring_cap = [] { const char* v = getenv("FS_SWEEP_RING_CAP"); return v ? (u64)atol(v) : (u64)SWEEP_RING_CAP; }();
+  if (!wsc_shared(ctx, S, t, P, win, any_wi, ring_cap, &W, tw)) return FS_E_NOMEM;
   int rc = finish(ctx, &S);
   if (rc) return rc;
   ScenTables T;
@@ -630,7 +631,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
     EngShared sh2 = W.sh;
     sh2.r_off = roff;
     SweepKArgs a2{sh2, dc, nr, L2, t.U, gm2, sb2, p2, dsum, dcodes, next2, dr};
-    FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(sl2 / per_cta), 128, 0, a2);
+    FS_LAUNCH(ctx, "wsc_sweep_retry", kern, (u32)(sl2 / per_cta), 128, 0, a2);
     cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);
   }
   cudaMemcpyAsync(out, dsum, ns * sizeof(fs_replay_summary), cudaMemcpyDeviceToHost, ctx->stream);

@@ -681,13 +681,27 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
       cudaMemcpyAsync(&nw, nlist, 4, cudaMemcpyDeviceToHost, ctx->stream);
       cudaStreamSynchronize(ctx->stream);
       fixup = nw;
-      // users still changing: per-user Jacobi to the fixed point, one CTA each (k_act_user_jacobi)
+      // users still changing: the sequential walk, one warp per user (k_act_user_walk); FS_ACT_FIXUP=
+      // jacobi selects the blocked Gauss-Seidel CTA per user it replaced (A/B measurements)
       u32* uit = S.zeros<u32>(1);
       if (S.failed) return FS_E_NOMEM;
-      ActUserJacobiArgs ja{ulist, nw, t.A, ou.o.seg, oua.o.seg, ou.o.perm, oua.pos, ou.pre, oua.pre, ou.ts, ou.lb,
-                           oua.lb, ou.pc, ou.ptau, oua.pc, oua.ptau, t.meta, overloaded, LD.L, LD.ra, LD.ta, status,
-                           uit};
-      if (nw) FS_LAUNCH(ctx, "act_user_jacobi", k_act_user_jacobi, nw, UJ_T, 0, ja);
+      static const bool fix_jacobi = [] { const char* v = getenv("FS_ACT_FIXUP"); return v && !strcmp(v, "jacobi"); }();
+      if (nw && (fix_jacobi || t.A > UW_AMAX)) {
+        ActUserJacobiArgs ja{ulist, nw, t.A, ou.o.seg, oua.o.seg, ou.o.perm, oua.pos, ou.pre, oua.pre, ou.ts, ou.lb,
+                             oua.lb, ou.pc, ou.ptau, oua.pc, oua.ptau, t.meta, overloaded, LD.L, LD.ra, LD.ta, status,
+                             uit};
+        FS_LAUNCH(ctx, "act_user_jacobi", k_act_user_jacobi, nw, UJ_T, 0, ja);
+      } else if (nw) {
+        u32* far = S.zeros<u32>(nw);
+        if (S.failed) return FS_E_NOMEM;
+        // per-pass scratch of both orders reused by position of the u order (the passes are over)
+        ActWalkPrepArgs pw{ulist, ou.o.seg, ou.o.perm, ou.pos, oua.pos, oua.o.perm, ou.pre, oua.lb, t.meta, overloaded,
+                           status, ou.lb, oua.flag, ou.flag, far};
+        FS_LAUNCH(ctx, "act_walk_prep", k_act_walk_prep, dim3(nw, 64), 256, 0, pw);
+        ActUserWalkArgs wa{ulist, nw, t.A, ou.o.seg, ou.o.perm, ou.pre, ou.lb, oua.flag, ou.flag, far,
+                           ou.pc, ou.ptau, oua.pc, oua.ptau, overloaded, LD.L, LD.ra, LD.ta, status, uit};
+        FS_LAUNCH(ctx, "act_user_walk", k_act_user_walk, nw, 32, 0, wa);
+      }
       u32 hit = 0;
       cudaMemcpyAsync(&hit, uit, 4, cudaMemcpyDeviceToHost, ctx->stream);
       cudaStreamSynchronize(ctx->stream);

@@ -198,33 +198,79 @@ __global__ void __launch_bounds__(256) k_vf_range(VfArgs a) {
 struct VfSlotArgs {
   DTrace t; u32* flag; const uint4* hrec; const u32* off; u32* slot;
 };
+// k_vf_slots / k_vf_links: 4 calls per thread (uint4 loads of the streamed fields), every
+// dependent gather of the four issued before any is used -- the passes are latency-bound
+// gathers / scatters (head record, slot offset, slots), so memory-level parallelism is the lever
 __global__ void __launch_bounds__(256) k_vf_slots(VfSlotArgs a) {
   const DTrace& t = a.t;
   const u64 n = t.n;
   bool bad = false;
-  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-    const u32 x = __ldg(&t.inter[i]), m = __ldg(&t.meta[i]), u = __ldg(&t.user[i]);
-    const uint4 e = a.hrec[x];
-    const u32 s = m_stage(m), nc = m_ncalls(m);
-    if (e.x == NONE32 || e.y != u || e.z != (m & 0x00FF00FFu) || (s == 1 && e.x != (u32)i)) { bad = true; continue; }
-    a.slot[(u64)a.off[x] + s - 1] = (u32)i;
+  auto one = [&](u64 i, u32 x, u32 m, u32 u, const uint4& e, u32 o) {
+    const u32 s = m_stage(m);
+    if (e.x == NONE32 || e.y != u || e.z != (m & 0x00FF00FFu) || (s == 1 && e.x != (u32)i)) { bad = true; return; }
+    a.slot[(u64)o + s - 1] = (u32)i;
+  };
+  const bool vec = (((uintptr_t)t.user | (uintptr_t)t.meta | (uintptr_t)t.inter) & 15) == 0;
+  const u64 n4 = vec ? n / 4 : 0;
+  const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n4) {
+    const uint4 X = __ldg((const uint4*)t.inter + q), M = __ldg((const uint4*)t.meta + q);
+    const uint4 U = __ldg((const uint4*)t.user + q);
+    const uint4 e0 = a.hrec[X.x], e1 = a.hrec[X.y], e2 = a.hrec[X.z], e3 = a.hrec[X.w];
+    const u32 o0 = a.off[X.x], o1 = a.off[X.y], o2 = a.off[X.z], o3 = a.off[X.w];
+    one(4 * q, X.x, M.x, U.x, e0, o0); one(4 * q + 1, X.y, M.y, U.y, e1, o1);
+    one(4 * q + 2, X.z, M.z, U.z, e2, o2); one(4 * q + 3, X.w, M.w, U.w, e3, o3);
+  }
+  for (u64 i = n4 * 4 + q; i < n; i += (u64)gridDim.x * blockDim.x) {   // tail (every call if unaligned)
+    const u32 x = __ldg(&t.inter[i]);
+    one(i, x, __ldg(&t.meta[i]), __ldg(&t.user[i]), a.hrec[x], a.off[x]);
   }
   if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1u);
 }
 __global__ void __launch_bounds__(256) k_vf_links(DTrace t, const uint4* hrec, const u32* off, const u32* slot,
                                                   u32* flag, u32* head_of, u32* next_call) {
-  const u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 n = t.n;
   bool bad = false;
-  if (i < t.n) {
-    const u32 x = __ldg(&t.inter[i]), m = __ldg(&t.meta[i]);
+  u32 ho[4], nc[4];
+  auto one = [&](u64 i, u32 m, u32 o, u32 sl, u32 sn, int k) {
     const u32 s = m_stage(m);
-    const u64 pos = (u64)off[x] + s - 1;
-    if (s == 0 || pos + (s < m_ncalls(m)) >= t.n) bad = true;          // (a call k_vf_slots rejected)
-    else {
-      const u32 nx = s < m_ncalls(m) ? slot[pos + 1] : NONE32;
-      bad = slot[pos] != (u32)i || (nx != NONE32 && nx <= (u32)i);     // own slot; the successor later (R1)
-      if (head_of) { head_of[i] = hrec[x].x; next_call[i] = nx; }
+    const u64 pos = (u64)o + s - 1;
+    if (s == 0 || pos + (s < m_ncalls(m)) >= n) { bad = true; return; }  // (a call k_vf_slots rejected)
+    const u32 nx = s < m_ncalls(m) ? sn : NONE32;
+    bad |= sl != (u32)i || (nx != NONE32 && nx <= (u32)i);               // own slot; the successor later (R1)
+    nc[k] = nx;
+  };
+  const bool vec = (((uintptr_t)t.meta | (uintptr_t)t.inter | (uintptr_t)head_of | (uintptr_t)next_call) & 15) == 0;
+  const u64 n4 = vec ? n / 4 : 0;
+  const u64 q = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n4) {
+    const uint4 X = __ldg((const uint4*)t.inter + q), M = __ldg((const uint4*)t.meta + q);
+    const u32 xs[4] = {X.x, X.y, X.z, X.w}, ms[4] = {M.x, M.y, M.z, M.w};
+    u32 o[4], sl[4], sn[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) { o[k] = off[xs[k]]; if (head_of) ho[k] = hrec[xs[k]].x; }
+#pragma unroll
+    for (int k = 0; k < 4; k++) {                                       // both slots of each call up front
+      const u64 pos = (u64)o[k] + m_stage(ms[k]) - 1;                   // (clamped: checked in one())
+      const bool ok = m_stage(ms[k]) != 0 && pos + 1 < n + 1;
+      sl[k] = ok ? slot[pos] : NONE32;
+      sn[k] = ok && pos + 1 <= n ? slot[pos + 1] : NONE32;
     }
+#pragma unroll
+    for (int k = 0; k < 4; k++) { nc[k] = NONE32; one(4 * q + k, ms[k], o[k], sl[k], sn[k], k); }
+    if (head_of) {
+      ((uint4*)head_of)[q] = make_uint4(ho[0], ho[1], ho[2], ho[3]);
+      ((uint4*)next_call)[q] = make_uint4(nc[0], nc[1], nc[2], nc[3]);
+    }
+  }
+  for (u64 i = n4 * 4 + q; i < n; i += (u64)gridDim.x * blockDim.x) {
+    const u32 x = __ldg(&t.inter[i]), m = __ldg(&t.meta[i]);
+    const u32 o0 = off[x];
+    const u64 pos = (u64)o0 + m_stage(m) - 1;
+    const bool ok = m_stage(m) != 0 && pos + 1 < n + 1;
+    nc[0] = NONE32;
+    one(i, m, o0, ok ? slot[pos] : NONE32, ok && pos + 1 <= n ? slot[pos + 1] : NONE32, 0);
+    if (head_of) { head_of[i] = hrec[x].x; next_call[i] = nc[0]; }
   }
   if (__any_sync(FULL_MASK, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
 }
@@ -256,7 +302,7 @@ static bool validate_trace(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
   if (S.failed) return false;
   cudaMemsetAsync(slot, 0xFF, (n + 1) * 4, ctx->stream);
   VfSlotArgs sa{t, flag, hrec, off, slot};
-  FS_LAUNCH(ctx, "vf_slots", k_vf_slots, div_up(n, 256), 256, 0, sa);
+  FS_LAUNCH(ctx, "vf_slots", k_vf_slots, div_up(std::max<u64>(n / 4, 4), 256), 256, 0, sa);
   u32* ho = nullptr;
   u32* nc = nullptr;
   if (L) {
@@ -264,7 +310,7 @@ static bool validate_trace(fs_ctx* ctx, Scratch& S, const DTrace& t, Links* L) {
     nc = S.alloc<u32>(n);
     if (S.failed) return false;
   }
-  FS_LAUNCH(ctx, "vf_links", k_vf_links, div_up(n, 256), 256, 0, t, hrec, off, slot, flag, ho, nc);
+  FS_LAUNCH(ctx, "vf_links", k_vf_links, div_up(std::max<u64>(n / 4, 4), 256), 256, 0, t, hrec, off, slot, flag, ho, nc);
   u32 f2 = 0;
   cudaMemcpyAsync(&f2, flag, 4, cudaMemcpyDeviceToHost, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
