@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(256) k_act_walk_prep(const ActWalkPrepArgs a) 
   if ((threadIdx.x & 31) == 0 && fr) atomicMax(&a.far[blockIdx.x], fr);
 }
 struct ActUserWalkArgs {
-  const u32* users; u32 n_users_w; u32 A;
+  const u32* users; u32 n_users_w; u32 A, app_bits;
   const u64* seg_u; const u32* perm_u; const uint2* pre_u;
   const u64* lbx; const u32* hpx; const u32* ax; const u32* far;
   u32* pc_u; u64* ptau_u; u32* pc_au; u64* ptau_au;   // far lookups: prefixes by u position (scratch)
@@ -473,6 +473,8 @@ __global__ void __launch_bounds__(32) k_act_user_walk(const ActUserWalkArgs a) {
     }
     const u32 ca = in ? acnt[app] : 0u;
     const u64 cta = in ? atau[app] : 0ull;
+    const u32 ra_app = chk ? a.ra[app] : 0u;                       // the app's limits, loaded with the batch
+    const u64 ta_app = chk ? a.ta[app] : 0ull;
     const u32 su = chk && lbu_in ? (u32)(lbu - p0) : lane;
     const u32 sa = chk && lba_in ? (u32)(lbau - p0) : lane;
     const u32 hsrc = hin ? (u32)((u64)x.hp - p0) : lane;
@@ -483,11 +485,10 @@ __global__ void __launch_bounds__(32) k_act_user_walk(const ActUserWalkArgs a) {
     u32 srank = 0, src = lane, sst = 0;
     const bool multi = (leaders & (leaders - 1)) != 0;
     if (multi) {
-      u32 below = 0;                                                // lanes of smaller apps (out-of-batch lanes: last)
-      for (u32 lm = leaders; lm; lm &= lm - 1) {
-        const u32 ld = __ffs(lm) - 1;
-        const u32 la = __shfl_sync(FULL_MASK, app, ld), lp = __shfl_sync(FULL_MASK, peers, ld);
-        if (in && la < app) below += __popc(lp);
+      u32 below = 0, eq = inmask;                                   // lanes of smaller apps: a radix rank by
+      for (int b = (int)a.app_bits - 1; b >= 0; b--) {              //   one ballot per app bit (out-of-batch
+        const u32 one = __ballot_sync(FULL_MASK, in && ((app >> b) & 1u));   // lanes last)
+        if ((app >> b) & 1u) { below += __popc(eq & ~one); eq &= one; } else eq &= ~one;
       }
       if (!in) below = __popc(inmask);
       srank = below + __popc(peers & lt);
@@ -518,10 +519,17 @@ __global__ void __launch_bounds__(32) k_act_user_walk(const ActUserWalkArgs a) {
       if (!multi) eta = cta + ex;                                  // one app in the batch
       else {                                                        // segmented scan in (app, lane) order
         const u32 y0 = __shfl_sync(FULL_MASK, tv, src);
-        u64 y = y0;
+        if (small) {
+          u32 y = y0;
 #pragma unroll
-        for (u32 o = 1; o < 32; o <<= 1) { const u64 z = __shfl_up_sync(FULL_MASK, y, o); if (lane >= sst + o) y += z; }
-        eta = cta + __shfl_sync(FULL_MASK, y - y0, srank);
+          for (u32 o = 1; o < 32; o <<= 1) { const u32 z = __shfl_up_sync(FULL_MASK, y, o); if (lane >= sst + o) y += z; }
+          eta = cta + __shfl_sync(FULL_MASK, y - y0, srank);
+        } else {
+          u64 y = y0;
+#pragma unroll
+          for (u32 o = 1; o < 32; o <<= 1) { const u64 z = __shfl_up_sync(FULL_MASK, y, o); if (lane >= sst + o) y += z; }
+          eta = cta + __shfl_sync(FULL_MASK, y - y0, srank);
+        }
       }
       u32 lc = __shfl_sync(FULL_MASK, ec, su); u64 ltt = __shfl_sync(FULL_MASK, et, su);
       u32 lac = __shfl_sync(FULL_MASK, eca, sa); u64 lat = __shfl_sync(FULL_MASK, eta, sa);
@@ -534,10 +542,14 @@ __global__ void __launch_bounds__(32) k_act_user_walk(const ActUserWalkArgs a) {
         nst = FS_ST_ADMIT;
         if (L.rg && n_g > L.rg) nst = FS_ST_BLOCK_USER_REQ;
         else if (L.tg && t_g > L.tg) nst = FS_ST_BLOCK_USER_TOK;
-        else if (a.ra[app] && n_a > a.ra[app]) nst = FS_ST_BLOCK_APP_REQ;
-        else if (a.ta[app] && t_a > a.ta[app]) nst = FS_ST_BLOCK_APP_TOK;
+        else if (ra_app && n_a > ra_app) nst = FS_ST_BLOCK_APP_REQ;
+        else if (ta_app && t_a > ta_app) nst = FS_ST_BLOCK_APP_TOK;
       }
-      const bool ch = __any_sync(FULL_MASK, nst != st);
+      // another round only if a continuation's in-batch head flipped between admitted and blocked
+      // (a change between block codes, or of a head without in-batch continuations, moves no flag)
+      const bool flip = (nst == FS_ST_ADMIT) != (st == FS_ST_ADMIT);
+      const bool hflip = __shfl_sync(FULL_MASK, (u32)flip, hsrc) != 0;
+      const bool ch = __any_sync(FULL_MASK, hin && hflip);
       st = nst;
       it++;
       if (!ch) break;

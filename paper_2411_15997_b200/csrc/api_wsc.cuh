@@ -553,6 +553,12 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   // scenarios of the FairServe modes only: the engine without the baseline-mode paths
   // (FS_SWEEP_LPS = 16 / 8, several replays per warp, measured slower: FS-mode engine only)
   const bool base = any_dq || any_ag;
+  // every scenario FS(W+I), all arrivals counted per (user, app), increments precomputed, unweighted
+  // token loads: the engine with those tests compiled out (FS_SWEEP_FWI=0 disables, A/B)
+  static const int fwi_env = [] { const char* v = getenv("FS_SWEEP_FWI"); return v ? atoi(v) : 1; }();
+  bool fwi = fwi_env != 0 && !base && W.sh.tau_w == nullptr;
+  for (u32 s = 0; s < ns && fwi; s++)
+    fwi = scen[s].mode == FS_MODE_WI && hc[s].heads_only == 0 && hc[s].app_global == 0 && hc[s].inc != nullptr;
   const int tour = base || lps < 32 || Bmax > 1024 ? 0 : tour_bits(0);   // warp-parallel engine pieces
   EngLayout L = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi,
                            W.ring_slots, false, 0, any_dq, any_rpm ? (u32)std::min<u64>(t.n + 1, SWEEP_RPM_CAP) : 0, t.A,
@@ -561,7 +567,8 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   const size_t slot_bytes = (L.bytes_glob + 255) / 256 * 256;
   SweepFn kern = base ? (minb >= 6 ? k_sweep<6, 32, true, 0> : minb == 5 ? k_sweep<5, 32, true, 0> :
                            minb == 4 ? k_sweep<4, 32, true, 0> : k_sweep<3, 32, true, 0>)
-               : lps <= 8 ? k_sweep<4, 8, false, 0> : lps == 16 ? k_sweep<4, 16, false, 0> : sweep_kern_t(tour, minb);
+               : lps <= 8 ? k_sweep<4, 8, false, 0> : lps == 16 ? k_sweep<4, 16, false, 0>
+               : fwi && tour == 0 && minb == 4 ? k_sweep<4, 32, false, 0, true> : sweep_kern_t(tour, minb);
   const u32 per_cta = base ? 4 : 128 / (lps <= 8 ? 8 : lps == 16 ? 16 : 32);
   // the replays' state lives in global memory: give L1 every byte shared memory does not need
   static const int carve = [] { const char* v = getenv("FS_SWEEP_CARVE"); return v ? atoi(v) : -1; }();

@@ -698,7 +698,7 @@ extern "C" int fs_act_throttle(fs_ctx* ctx, const fs_trace* tr, const fs_profile
         ActWalkPrepArgs pw{ulist, ou.o.seg, ou.o.perm, ou.pos, oua.pos, oua.o.perm, ou.pre, oua.lb, t.meta, overloaded,
                            status, ou.lb, oua.flag, ou.flag, far};
         FS_LAUNCH(ctx, "act_walk_prep", k_act_walk_prep, dim3(nw, 64), 256, 0, pw);
-        ActUserWalkArgs wa{ulist, nw, t.A, ou.o.seg, ou.o.perm, ou.pre, ou.lb, oua.flag, ou.flag, far,
+        ActUserWalkArgs wa{ulist, nw, t.A, bits_for(t.A - 1), ou.o.seg, ou.o.perm, ou.pre, ou.lb, oua.flag, ou.flag, far,
                            ou.pc, ou.ptau, oua.pc, oua.ptau, overloaded, LD.L, LD.ra, LD.ta, status, uit};
         FS_LAUNCH(ctx, "act_user_walk", k_act_user_walk, nw, 32, 0, wa);
       }

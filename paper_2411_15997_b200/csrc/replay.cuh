@@ -120,7 +120,10 @@ enum { HS_DIRECT = 0,                   // heads read one at a time (online step
 // finish batch is found by the lanes holding it (no 48-B heap sifts); bit 4 (TA) -- the lanes split
 // the ACT continuation ring of a user (expiry by ballot, counts by redux).  (Bit 1, a 32-group
 // warp tournament in place of the pick heaps, measured 40 % slower on the C5 sweep and was removed.)
-template <int HS, int LPS = 32, bool BASE = true, int TOUR = 0>   // BASE: the NEXT-1 baseline modes compiled in
+// FWI: every scenario of the launch is FS(W+I) counting all arrivals per (user, app), with precomputed
+// Eq. 3 increments and unweighted token loads -- the mode tests, the increment-table test and the
+// R11 weight lookups become compile-time (the default C5 grid; the sweep picks it on the host)
+template <int HS, int LPS = 32, bool BASE = true, int TOUR = 0, bool FWI = false>   // BASE: the NEXT-1 baseline modes compiled in
 struct EngineT {
   static_assert(!TOUR || (HS == HS_WARP && LPS == 32 && !BASE), "warp tournament: FairServe modes on a full warp");
   static constexpr bool TB = (TOUR & 2) != 0, TA = (TOUR & 4) != 0;
@@ -273,7 +276,7 @@ struct EngineT {
   __device__ __forceinline__ int act_check(UState& us, u32 k, u32 app, i64 tr, u64 n_g, u64 t_g, u64 n_a, u64 t_a) {
     bool ring_done = false;
     if constexpr (TA) {
-     if (!c->heads_only) {                               // the lanes split the ring
+     if (FWI || !c->heads_only) {                        // the lanes split the ring
       const u64 base = sh->r_off[k]; const u32 cap = (u32)(sh->r_off[k + 1] - base);
       const u32 lane = threadIdx.x & 31;
       const i64 lim = tr - c->Wns;
@@ -303,7 +306,7 @@ struct EngineT {
       ring_done = true;
      }
     }
-    if (!ring_done && (!c->heads_only || !static_heads)) {
+    if (!ring_done && (FWI || !c->heads_only || !static_heads)) {
       u64 base = sh->r_off[k]; u32 cap = (u32)(sh->r_off[k + 1] - base);
       u32 h = us.r_head, len = us.r_len;
       while (len && s.r[base + h].t <= tr - c->Wns) { h = h + 1 == cap ? 0 : h + 1; len--; }   // (Q4)
@@ -408,8 +411,8 @@ struct EngineT {
     arrived(r, tr, ovl);
     bool was = lift(us);
     int st = FS_ST_ADMIT;
-    if (c->mode == FS_MODE_WI) {
-      const u32 tau_h = sh->tau_w ? sh->tau_w[r] : h.B.y + h.B.w;                           // R11
+    if (FWI || c->mode == FS_MODE_WI) {
+      const u32 tau_h = !FWI && sh->tau_w ? sh->tau_w[r] : h.B.y + h.B.w;                   // R11
       if (!static_heads && !ring_push(us, k, tr, tau_h, m_app(m), r)) return -1;           // l.19
       if (BASE && c->app_global) {                                                          // R10
         if (!ag_log(tr, m_app(m), tau_h, r)) return -1;
@@ -449,9 +452,9 @@ struct EngineT {
     UState& us = s.us[k];
     arrived(r, tr, ovl);
     bool was = lift(us);
-    if (c->mode == FS_MODE_WI && !c->heads_only) {          // l.19 (continuations are never throttled)
+    if (FWI || (c->mode == FS_MODE_WI && !c->heads_only)) {   // l.19 (continuations are never throttled)
       uint4 B = ldg4(&sh->recB[r]);
-      const u32 tau_c = sh->tau_w ? sh->tau_w[r] : B.y + B.w;                               // R11
+      const u32 tau_c = !FWI && sh->tau_w ? sh->tau_w[r] : B.y + B.w;                       // R11
       if (!ring_push(us, k, tr, tau_c, m_app(m), r)) return -1;
       if (BASE && c->app_global && !ag_log(tr, m_app(m), tau_c, r)) return -1;
     }
@@ -504,7 +507,7 @@ struct EngineT {
     if (cont) cs = s.cs[x];
     u32 r = cont ? us.cf : us.hf;                            // no dependent load on the slot
     uint4 A = ldg4(&sh->recA[r]), B = ldg4(&sh->recB[r]), Cc = ldg4(&sh->recC[r]);
-    u64 inc_pre = c->inc ? c->inc[r] : 0;
+    u64 inc_pre = FWI || c->inc ? c->inc[r] : 0;
     u64 need = (u64)B.y + B.w;
     us.nf = (u32)need;
     if ((u64)occ_now + need > C) return false;              // can_add_new_request: KV
@@ -546,7 +549,7 @@ struct EngineT {
     a->b.r = r; a->b.user = A.x; a->b.meta = A.z; a->b.link = A.w; a->b.think = B.x;
     a->b.rel = B.y + B.z;
     a->b.fi = iter + B.z - 1;
-    a->b.inc = c->inc ? inc_pre : increment(A.x, A.z, B, Cc);
+    a->b.inc = FWI || c->inc ? inc_pre : increment(A.x, A.z, B, Cc);
     return true;
   }
 
@@ -559,7 +562,7 @@ struct EngineT {
   __device__ __forceinline__ bool head_refill() {
     const u32 sub = threadIdx.x & (LPS - 1);
     const u32 gm = group_mask();
-    const bool win = c->mode == FS_MODE_WI && static_heads;
+    const bool win = FWI || (c->mode == FS_MODE_WI && static_heads);
     while (hp < sh->n_heads) {
       u64 j = hp + sub;
       bool ok = j < sh->n_heads;
@@ -1089,7 +1092,7 @@ struct SweepKArgs {
 // One scenario slot per group of LPS lanes.  Every lane of a group runs the (group-uniform)
 // engine: loads and stores of the replicated state are broadcast / merged, and head batch
 // refills use all LPS lanes.
-template <int MINB, int LPS, bool BASE, int TOUR>  // MINB CTAs per SM: caps registers (occupancy vs spills)
+template <int MINB, int LPS, bool BASE, int TOUR, bool FWI = false>  // MINB CTAs per SM: caps registers (occupancy vs spills)
 __global__ void __launch_bounds__(128, MINB) k_sweep(const __grid_constant__ SweepKArgs a) {
   __shared__ HEnt hbs[128];
   const u32 lane = threadIdx.x & 31, sub = threadIdx.x & (LPS - 1), lead = lane & ~(u32)(LPS - 1);
@@ -1113,7 +1116,7 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(const __grid_constant__ Swe
     __syncwarp(gm);
     __threadfence_block();
     {
-      EngineT<HS_WARP, LPS, BASE, TOUR> E;
+      EngineT<HS_WARP, LPS, BASE, TOUR, FWI> E;
       E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
       E.hb = &hbs[threadIdx.x & ~(u32)(LPS - 1)];
       E.run();
