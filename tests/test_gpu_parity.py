@@ -377,6 +377,61 @@ def test_act_c2_shape(F, ctx, mode, jacobi):
     assert s["n_block"] == esum["n_block"]
 
 
+def dense_user_trace(rng, n_heads=1800, span_ms=20_000, n_apps=3):
+    """One heavy user whose windows hold thousands of positions (the walk's global fallback beyond
+    its 1024-position ring) plus a light user; 1-4 calls per interaction."""
+    from paper_2411_15997_b200.tracegen import from_columns
+    rows = []
+    for x in range(n_heads):
+        u = 0 if rng.random() < 0.9 else 1
+        a = int(rng.integers(0, n_apps))
+        m = int(rng.choice((1, 1, 2, 3, 4)))
+        t0 = int(rng.integers(0, span_ms))
+        for s in range(1, m + 1):
+            if s > 1:
+                t0 += int(rng.integers(0, 400))
+            rows.append(dict(user=u, t_ms=t0, app=a, inter=x, stage=s, ncalls=m, len_in=int(rng.integers(1, 50)),
+                             len_sys=int(rng.integers(0, 5)), len_out=int(rng.integers(1, 30)),
+                             think_ms=int(rng.integers(0, 50)), tier=0))
+    rows.sort(key=lambda r: (r["t_ms"], r["inter"], r["stage"]))
+    ren = {}
+    for r in rows:
+        if r["stage"] == 1:
+            ren.setdefault(r["inter"], len(ren))
+    for r in rows:
+        r["inter"] = ren[r["inter"]]
+    return from_columns(2, n_apps, rows)
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("jmax", ["1", "2"])
+def test_act_walk_long_windows(F, ctx, monkeypatch, seed, jmax):
+    """ACT on a user whose windows span more positions than the walk's shared-memory ring (its global
+    prefix copies), with limits near the windows' counts so decisions chain through continuations."""
+    import torch
+    monkeypatch.setenv("FS_ACT_JACOBI_MAX", jmax)
+    rng = np.random.default_rng(9100 + seed)
+    A = 3
+    tr = dense_user_trace(rng, n_apps=A)
+    J, cnt, si, ss, so = tiny_profile(rng, A)
+    op = O.profile_from_host(A, J, cnt, si, ss, so)
+    gp = F.profile_from_host(ctx, A, J, cnt, si, ss, so)
+    n = tr["n_calls"]
+    W = 15_000
+    cfg = dict(window_ms=W, limits_from_profile=0, T_req_g=int(rng.integers(900, 1400)) if seed < 2 else 0,
+               T_req_a=[int(rng.integers(300, 500)) for _ in range(A)], T_tok_g=int(rng.integers(40_000, 60_000)),
+               T_tok_a=[int(rng.integers(12_000, 20_000)) for _ in range(A)], count_mode=0, tier_max=255)
+    ovl = None if seed % 2 == 0 else (rng.random(n) < 0.8).astype(np.uint8)
+    est, esum = O.act(tr, op, cfg, overloaded=ovl)
+    st, s = F.act_throttle(ctx, F.Trace(tr), gp, cfg, overloaded=None if ovl is None else torch.tensor(ovl, device="cuda"))
+    g = _np(st)
+    bad = np.nonzero(g != est)[0]
+    assert len(bad) == 0, (bad[:10], g[bad[:10]], est[bad[:10]])
+    assert s["n_block"] == esum["n_block"] and sum(esum["n_block"]) > 0
+    if jmax == "1":
+        assert s["n_fixup_users"] >= 1
+
+
 # ------------------------------------------------------------------ replay
 @pytest.mark.parametrize("seed", range(150))
 def test_replay_tiny(F, ctx, seed):
