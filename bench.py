@@ -475,6 +475,18 @@ def _stage_line(name, ms, n, algo_b, peaks, kt, reps, ncu):
             "frac": gbs / peaks["hbm_gbs"], "kernels": kern}
 
 
+NCU_TAGS = ("r02b", "r02")          # committed ncu captures, newest first (profiles/README.md)
+
+
+def ncu_path(name):
+    """The newest committed ncu capture `profiles/<tag>_<name>` (the same command bench.py times)."""
+    for tag in NCU_TAGS:
+        p = os.path.join(ROOT, "profiles", f"{tag}_{name}")
+        if os.path.exists(p):
+            return p
+    return os.path.join(ROOT, "profiles", f"{NCU_TAGS[-1]}_{name}")
+
+
 def ncu_bytes_per_call(path, n):
     """{kernel: DRAM bytes (read + write) per call per launch} from a committed ncu --csv capture."""
     import csv
@@ -521,7 +533,7 @@ def hbm_lines(ctx, F, G, T5, outs, eng, flush):
     ms, kt = _time_calls(ctx, lambda: F.build_app_profiles(ctx, T4, p4), flush, stream, reps)
     res["c4_profile"] = _stage_line("C4 fs_build_app_profiles, 100M calls (device-generated), tier_max 0",
                                     ms, T4.n, PROFILE_ALGO_B, peaks, kt, reps,
-                                    ncu_bytes_per_call(os.path.join(ROOT, "profiles", "r02_c4_dram.csv"), T4.n))
+                                    ncu_bytes_per_call(ncu_path("c4_dram.csv"), T4.n))
     del T4
     torch.cuda.synchronize()
     T3 = F.generate_trace(ctx, "c3")
@@ -533,7 +545,7 @@ def hbm_lines(ctx, F, G, T5, outs, eng, flush):
                          flush, stream, reps)
     res["c3_act_overload_always"] = _stage_line(
         "C3 fs_act_throttle, 10M calls (device-generated), overload always", ms, T3.n, ACT_ALGO_B, peaks, kt, reps,
-        ncu_bytes_per_call(os.path.join(ROOT, "profiles", "r02_c3_act_dram.csv"), T3.n))
+        ncu_bytes_per_call(ncu_path("c3_act_dram.csv"), T3.n))
     res["c3_act_overload_always"]["summary"] = summ
     del T3, prof3, st3
     # ACT on the C2 trace with the single replay's recorded arrival times and overload flags
@@ -584,12 +596,12 @@ def roofline(name, launches, ms, N, peaks, src, args, kt):
         if name == "wsc_replay":
             # dependent instruction chain: one engine warp (+ the head-prefetch warp) issuing at
             # most one warp-instruction per cycle each at the measured max SM clock.
-            prof = ncu_csv(os.path.join(ROOT, "profiles", "r02_replay.csv")) if args.workload == "c2" else {}
+            prof = ncu_csv(ncu_path("replay.csv")) if args.workload == "c2" else {}
             peak = 2 * ghz
             ncalls = 1_000_000
         else:
             # many independent one-lane replays: every SMSP can issue one warp-instruction per cycle
-            prof = ncu_csv(os.path.join(ROOT, "profiles", "r02_sweep.csv"))
+            prof = ncu_csv(ncu_path("sweep.csv"))
             peak = peaks.get("sm_count", 148) * 4 * ghz
             ncalls = 1_000_000 * int(prof.get("scenarios", 64))
             units = N * args.scenarios
