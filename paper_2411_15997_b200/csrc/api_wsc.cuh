@@ -559,7 +559,7 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   const bool base = any_dq || any_ag;
   // every scenario FS(W+I), all arrivals counted per (user, app), increments precomputed, unweighted
   // token loads: the engine with those tests compiled out (FS_SWEEP_FWI=0 disables, A/B)
-  static const int fwi_env = [] { const char* v = getenv("FS_SWEEP_FWI"); return v ? atoi(v) : 1; }();
+  const int fwi_env = getenv("FS_SWEEP_FWI") ? atoi(getenv("FS_SWEEP_FWI")) : 1;
   bool fwi = fwi_env != 0 && !base && W.sh.tau_w == nullptr;
   for (u32 s = 0; s < ns && fwi; s++)
     fwi = scen[s].mode == FS_MODE_WI && hc[s].heads_only == 0 && hc[s].app_global == 0 && hc[s].inc != nullptr;
@@ -583,7 +583,38 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   u64 by_mem = (u64)(free_b / 2) / std::max<size_t>(slot_bytes, 1);
   slots = std::max<u64>(1, std::min(slots, by_mem));
   slots = (slots + per_cta - 1) / per_cta * per_cta;   // whole CTAs
-  unsigned char* gm = S.alloc<unsigned char>(slots * slot_bytes + 256);
+  // up to 16 scenarios per SM (a strong-scaling slice: 512-2048 of the 4096 grid): one warp per CTA with
+  // the single replay's configuration instead -- state in shared memory first, no register cap, the
+  // warp-parallel pieces (512: 3.05 vs 4.19 s, 1024: 4.64 vs 5.21, 2048: 5.32 vs 6.48 s; FS_SWEEP_SOLO=0
+  // disables)
+  const char* solo_v = getenv("FS_SWEEP_SOLO");           // read per call: tests select either kernel
+  const int solo_env = solo_v ? atoi(solo_v) : 1;
+  // (the whole 4096 grid, 28 per SM, runs faster on the 16-per-SM regular kernel: 9.3-10.0 vs 10.3-11.5 s)
+  const u32 solo_max = getenv("FS_SWEEP_SOLO_MAX") ? (u32)atoi(getenv("FS_SWEEP_SOLO_MAX")) : 16u;
+  const int solo_all = getenv("FS_SWEEP_SOLO_ALL") ? atoi(getenv("FS_SWEEP_SOLO_ALL")) : 0;
+  const u32 want_per_sm = (u32)div_up(ns, (u64)ctx->sm_count);
+  const u32 solo_per_sm = std::min(want_per_sm, solo_max);
+  const bool solo = solo_env && !base && lps == 32 && Bmax <= 1024 && (want_per_sm <= solo_max || solo_all) &&
+                    ctx->smem_optin;
+  EngLayout Ls = L;
+  SweepFn kern_solo = nullptr;
+  size_t slot_solo = 0;
+  if (solo) {
+    const int tour_s = tour_bits(6);
+    size_t budget = std::min<size_t>((size_t)228 * 1024 / solo_per_sm - 4096, ctx->smem_optin - 512);
+    budget = std::min<size_t>(budget, 128 * 1024) - (sizeof(HEnt) * 32 + 64);
+    Ls = eng_layout(t.U, std::max<u32>(std::min<u32>(t.X, 8192), 1), W.n_heads, Bmax, p_cap, AJ, any_wi, W.ring_slots,
+                    false, budget, false, 0, t.A, 0, (tour_s & 2) != 0);
+    slot_solo = (Ls.bytes_glob + 255) / 256 * 256;
+    kern_solo = fwi ? (tour_s == 6 ? k_sweep_solo<6, true> : tour_s == 2 ? k_sweep_solo<2, true> :
+                       tour_s == 4 ? k_sweep_solo<4, true> : k_sweep_solo<0, true>)
+                    : (tour_s == 6 ? k_sweep_solo<6, false> : tour_s == 2 ? k_sweep_solo<2, false> :
+                       tour_s == 4 ? k_sweep_solo<4, false> : k_sweep_solo<0, false>);
+    cudaFuncSetAttribute(kern_solo, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ls.bytes_smem);
+  }
+  const u64 slots_run = solo ? std::min<u64>(ns, (u64)ctx->sm_count * solo_per_sm) : slots;
+  const size_t sb_run = solo ? slot_solo : slot_bytes;
+  unsigned char* gm = S.alloc<unsigned char>(slots_run * sb_run + 256);
   if (S.failed) return FS_E_NOMEM;
   // longest-processing-time order: scenarios with the most participating calls start first, so
   // the last wave holds the short ones (the cost of a replay grows with its calls)
@@ -601,8 +632,13 @@ extern "C" int fs_sweep(fs_ctx* ctx, const fs_trace* tr, const fs_profile* P, co
   u32* dord = S.alloc<u32>(ns);
   if (S.failed) return FS_E_NOMEM;
   cudaMemcpyAsync(dord, ord.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream);
-  SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next, dord};
-  FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / per_cta), 128, 0, a);
+  if (solo) {
+    SweepKArgs a{W.sh, dc, ns, Ls, t.U, gm, slot_solo, p_cap, dsum, dcodes, next, dord};
+    FS_LAUNCH(ctx, "wsc_sweep", kern_solo, (u32)slots_run, 32, Ls.bytes_smem, a);
+  } else {
+    SweepKArgs a{W.sh, dc, ns, L, t.U, gm, slot_bytes, p_cap, dsum, dcodes, next, dord};
+    FS_LAUNCH(ctx, "wsc_sweep", kern, (u32)(slots / per_cta), 128, 0, a);
+  }
   std::vector<int> hcodes(ns);
   cudaMemcpyAsync(hcodes.data(), dcodes, ns * 4, cudaMemcpyDeviceToHost, ctx->stream);
   rc = finish(ctx, &S);

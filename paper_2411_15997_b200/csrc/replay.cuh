@@ -1129,6 +1129,45 @@ __global__ void __launch_bounds__(128, MINB) k_sweep(const __grid_constant__ Swe
   }
 }
 
+// sweep of few scenarios (a strong-scaling slice: at most 4 per SM): one warp per CTA with the single
+// replay's configuration -- its state in shared memory first (L.bytes_smem per slot), no register cap,
+// the warp-parallel engine pieces -- taking scenarios from the same longest-first queue
+template <int TOUR, bool FWI>
+__global__ void __launch_bounds__(32) k_sweep_solo(const __grid_constant__ SweepKArgs a) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ HEnt hbs[32];
+  const u32 lane = threadIdx.x;
+  unsigned char* g = a.gmem + (size_t)blockIdx.x * a.slot_bytes;
+  EngState st0;
+  eng_bind(a.L, sm, g, a.p_cap, &st0, nullptr);
+  EngOut none;
+  memset(&none, 0, sizeof(none));
+  const u64 AJ = (u64)a.sh.A * a.sh.J1;
+  for (;;) {
+    u32 q = 0;
+    if (lane == 0) q = atomicAdd(a.next, 1u);
+    q = __shfl_sync(FULL_MASK, q, 0);
+    if (q >= a.n_scen) return;
+    const u32 sc = a.order ? a.order[q] : q;
+    EngState st = st0;
+    st.W = a.L.smem[L_W] ? st.W : (u64*)a.cfgs[sc].W;
+    eng_clear(st, a.sh, a.cfgs[sc].W, AJ, a.U, lane, 32);
+    __syncwarp();
+    __threadfence_block();
+    {
+      EngineT<HS_WARP, 32, false, TOUR, FWI> E;
+      E.init(&a.sh, &a.cfgs[sc], st, none, a.U);
+      E.hb = hbs;
+      E.run();
+      if (lane == 0) {
+        a.sums[sc] = E.sum;
+        a.codes[sc] = E.err_code ? E.err_code + 1 : 0;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // ------------------------------------------------------------------ online step (fs_wsc_step)
 struct StepKArgs {
   EngShared sh; EngCfg cfg; EngLayout L; u32 U; unsigned char* gmem; u32 p_cap;

@@ -513,7 +513,14 @@ def test_step_vs_oracle(F, ctx, seed):
 
 
 # ------------------------------------------------------------------ sweep
-def test_sweep_small(F, ctx):
+@pytest.mark.parametrize("kern", ["solo", "regular", "regular-generic"])
+def test_sweep_small(F, ctx, monkeypatch, kern):
+    """Small grids run on the solo-slot kernel (<= 16 scenarios per SM); the regular 16-per-SM kernel,
+    with and without the FS(W+I)-only instantiation, is forced here."""
+    if kern != "solo":
+        monkeypatch.setenv("FS_SWEEP_SOLO", "0")
+    if kern == "regular-generic":
+        monkeypatch.setenv("FS_SWEEP_FWI", "0")
     tr = G.generate(dict(G.CONFIGS["c2"], n_users=100, n_calls=20_000, seed=61))
     op = O.profile(tr, dict(tier_max=0))
     gp = F.build_app_profiles(ctx, F.Trace(tr), dict(tier_max=0))
@@ -532,7 +539,7 @@ def test_sweep_small(F, ctx):
         assert a == b
 
 
-def test_sweep_capacity_retry(F, ctx):
+def test_sweep_capacity_retry(F, ctx, monkeypatch):
     """Scenarios whose state outgrows the sweep's first capacities (a 512-entry ACT ring per user,
     a 65 536-entry RPM window log) run again with exact capacities: same summaries as the oracle,
     no FS_E_NOMEM.  Five users share 70 000 calls and the windows span the whole day."""
@@ -549,11 +556,13 @@ def test_sweep_capacity_retry(F, ctx):
             dict(base, mode=3, act=dict(window_ms=day, limits_from_profile=0, T_req_g=1 << 30, T_req_a=[1 << 30] * A))]
     es, ecodes = O.sweep(tr, op, scen)
     assert list(ecodes) == [0] * len(scen)
-    for sub in (scen[:3], scen):            # FairServe modes only (tournament engine), then with RPM
-        gs, gcodes = F.sweep(ctx, F.Trace(tr), gp, sub)
-        assert list(gcodes) == [0] * len(sub)
-        for a, b in zip(gs, es):
-            assert a == b
+    for solo in ("1", "0"):                  # the solo-slot and the regular kernel's retries
+        monkeypatch.setenv("FS_SWEEP_SOLO", solo)
+        for sub in (scen[:3], scen):        # FairServe modes only, then with RPM
+            gs, gcodes = F.sweep(ctx, F.Trace(tr), gp, sub)
+            assert list(gcodes) == [0] * len(sub)
+            for a, b in zip(gs, es):
+                assert a == b
 
 
 # ------------------------------------------------------------------ errors
