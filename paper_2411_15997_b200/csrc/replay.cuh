@@ -75,7 +75,12 @@ struct REnt { i64 t; u32 tau, app; };   // ACT ring entry: arrival, token load, 
 struct RPEnt { i64 t; u32 user, app; }; // RPM window log entry (16 B)
 struct AGEnt { i64 t; u32 app, tau; };  // app-global window log entry (16 B)
 struct AGSum { u64 tau; u32 n, pad; };  // live logged calls of one app (all users)
-struct HEnt { uint4 A, B, C; u32 r, ng, na, pad; u64 tg, ta; };          // head arrival (80 B)
+// head arrival (48 B): what a delivery reads -- user, time, meta, uh position, KV need (prompt + reserve),
+// id, static head windows -- so the sweep's per-warp batches take 6 KB of shared memory per CTA, not 10
+struct HEnt { u32 user, t_ms, meta, upos, need, r, ng, na; u64 tg, ta; };
+__device__ __forceinline__ void hent_set(HEnt& h, u32 r, const uint4& A, const uint4& B, const uint4& C) {
+  h.r = r; h.user = A.x; h.t_ms = A.y; h.meta = A.z; h.upos = C.y; h.need = B.y + B.w;
+}
 struct alignas(16) BKey { u64 fi; u32 r, pad; };      // warp batch: finish iteration and call of a B slot
 
 struct EngState {
@@ -404,15 +409,15 @@ struct EngineT {
   // ---------------------------------------------------------------- deliveries (l.11-25)
   // returns the arrival status (FS_ST_ADMIT or a BLOCK code), -1 on error
   __device__ __forceinline__ int deliver_head(const HEnt& h, i64 tr, bool ovl) {
-    u32 r = h.r, k = h.A.x, m = h.A.z;
-    u32 upos = h.C.y;
+    u32 r = h.r, k = h.user, m = h.meta;
+    u32 upos = h.upos;
     UState& us = s.us[k];
     if (upos != us.qh_next) { err_code = ERR_ORDER; err_idx = r; return -1; }   // (t, id) order per user
     arrived(r, tr, ovl);
     bool was = lift(us);
     int st = FS_ST_ADMIT;
     if (FWI || c->mode == FS_MODE_WI) {
-      const u32 tau_h = !FWI && sh->tau_w ? sh->tau_w[r] : h.B.y + h.B.w;                   // R11
+      const u32 tau_h = !FWI && sh->tau_w ? sh->tau_w[r] : h.need;                          // R11
       if (!static_heads && !ring_push(us, k, tr, tau_h, m_app(m), r)) return -1;           // l.19
       if (BASE && c->app_global) {                                                          // R10
         if (!ag_log(tr, m_app(m), tau_h, r)) return -1;
@@ -443,7 +448,7 @@ struct EngineT {
     if (!was) {                                             // newly queued, front = this head
       if (dq) us.tie = myseq;                               //   VTC / RPM / FCFS: no class
       else { us.u |= CLS_BIT; us.tie = r; }                 //   FS: class 1
-      us.nf = h.B.y + h.B.w;
+      us.nf = h.need;
       newly_queued(us, k);
     }
     return FS_ST_ADMIT;
@@ -567,24 +572,27 @@ struct EngineT {
       u64 j = hp + sub;
       bool ok = j < sh->n_heads;
       HEnt h;
+      u32 r = 0;
+      uint4 A = make_uint4(0, 0, 0, 0);
       if (ok) {
-        h.r = __ldg(&sh->heads[j]);
-        h.A = ldg4(&sh->recA[h.r]);
-        ok = m_tier(h.A.z) <= c->tier_max;
+        r = __ldg(&sh->heads[j]);
+        A = ldg4(&sh->recA[r]);
+        ok = m_tier(A.z) <= c->tier_max;
       }
       if (ok) {
-        h.B = ldg4(&sh->recB[h.r]); h.C = ldg4(&sh->recC[h.r]);
+        const uint4 B = ldg4(&sh->recB[r]), C = ldg4(&sh->recC[r]);
+        hent_set(h, r, A, B, C);
         if (win) {
-          u32 up = h.C.y;
+          u32 up = C.y;
           h.ng = __ldg(&sh->hw_ng[up]); h.na = __ldg(&sh->hw_na[up]); h.tg = __ldg(&sh->hw_tg[up]); h.ta = __ldg(&sh->hw_ta[up]);
         } else { h.ng = h.na = 0; h.tg = h.ta = 0; }
-        asm volatile("prefetch.global.L1 [%0];" :: "l"(&s.us[h.A.x]));
+        asm volatile("prefetch.global.L1 [%0];" :: "l"(&s.us[A.x]));
       }
       u32 mask = __ballot_sync(gm, ok) & gm;
       hp += LPS;
       if (ok) hb[__popc(mask & lanemask_lt())] = h;
       __syncwarp(gm);
-      if (mask) { hb_n = __popc(mask); hb_i = 0; hb_t = hb[0].A.y; hb_r = hb[0].r; return true; }
+      if (mask) { hb_n = __popc(mask); hb_i = 0; hb_t = hb[0].t_ms; hb_r = hb[0].r; return true; }
     }
     return false;
   }
@@ -613,9 +621,10 @@ struct EngineT {
         u32 r = sh->heads[hp];
         uint4 A = ldg4(&sh->recA[r]);
         if (m_tier(A.z) <= c->tier_max) {
-          cur.A = A; cur.B = ldg4(&sh->recB[r]); cur.C = ldg4(&sh->recC[r]); cur.r = r;
+          const uint4 B = ldg4(&sh->recB[r]), C = ldg4(&sh->recC[r]);
+          hent_set(cur, r, A, B, C);
           if (c->mode == FS_MODE_WI && static_heads) {
-            u32 up = cur.C.y;
+            u32 up = C.y;
             cur.ng = sh->hw_ng[up]; cur.na = sh->hw_na[up]; cur.tg = sh->hw_tg[up]; cur.ta = sh->hw_ta[up];
           } else { cur.ng = cur.na = 0; cur.tg = cur.ta = 0; }
           cur_ok = true;
@@ -625,13 +634,13 @@ struct EngineT {
       }
       if (!cur_ok) return false;
     }
-    *tms = cur.A.y; *rid = cur.r;
+    *tms = cur.t_ms; *rid = cur.r;
     return true;
   }
   __device__ __forceinline__ void head_take(HEnt* h) {   // by value: the engine stays in registers
     if (HS == HS_WARP) {
       *h = hb[hb_i];
-      if (++hb_i < hb_n) { hb_t = hb[hb_i].A.y; hb_r = hb[hb_i].r; }
+      if (++hb_i < hb_n) { hb_t = hb[hb_i].t_ms; hb_r = hb[hb_i].r; }
       return;
     }
     if (RING) { *h = ring.e[rc_cons % HRING]; return; }
@@ -904,15 +913,17 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
     bool ok = j < sh->n_heads;
     HEnt h;
     memset(&h, 0, sizeof(h));
+    u32 r = 0;
+    uint4 A = make_uint4(0, 0, 0, 0);
     if (ok) {
-      h.r = sh->heads[j];
-      h.A = ldg4(&sh->recA[h.r]);
-      ok = m_tier(h.A.z) <= c->tier_max;
+      r = sh->heads[j];
+      A = ldg4(&sh->recA[r]);
+      ok = m_tier(A.z) <= c->tier_max;
     }
     if (ok) {
-      h.B = ldg4(&sh->recB[h.r]);
-      h.C = ldg4(&sh->recC[h.r]);
-      if (windows) { u32 up = h.C.y; h.ng = sh->hw_ng[up]; h.na = sh->hw_na[up]; h.tg = sh->hw_tg[up]; h.ta = sh->hw_ta[up]; }
+      const uint4 B = ldg4(&sh->recB[r]), C = ldg4(&sh->recC[r]);
+      hent_set(h, r, A, B, C);
+      if (windows) { u32 up = C.y; h.ng = sh->hw_ng[up]; h.na = sh->hw_na[up]; h.tg = sh->hw_tg[up]; h.ta = sh->hw_ta[up]; }
     }
     u32 mask = __ballot_sync(FULL_MASK, ok);
     u32 cnt = __popc(mask);
@@ -926,7 +937,7 @@ __device__ void head_producer(const EngShared* sh, const EngCfg* c, HeadRing rin
     if (ok) {
       u32 slot = (prod + __popc(mask & lanemask_lt())) % HRING;
       ring.e[slot] = h;
-      ring.key[slot] = make_uint2(h.A.y, h.r);
+      ring.key[slot] = make_uint2(h.t_ms, h.r);
     }
     __threadfence_block();
     __syncwarp();
@@ -1213,7 +1224,7 @@ __global__ void k_step(const __grid_constant__ StepKArgs a) {
     if (m_stage(A.z) == 1) {
       HEnt h;
       memset(&h, 0, sizeof(h));
-      h.r = r; h.A = A; h.B = ldg4(&a.sh.recB[r]); h.C = ldg4(&a.sh.recC[r]);
+      hent_set(h, r, A, ldg4(&a.sh.recB[r]), ldg4(&a.sh.recC[r]));
       s = E.deliver_head(h, a.arr_t[q], ovl);
     } else {
       s = E.deliver_cont(r, A.x, A.z, a.arr_t[q], ovl);
