@@ -153,6 +153,8 @@ struct EngineT {
   u32 rf_head, rf_len;                   // RPM window log: oldest entry, live entries
   u32 ag_head, ag_len;                   // app-global window log
   u64 digest, n_adm;
+  u32 nblk[4], ndrop, novl;               // summary counts of the event loop, 32-bit (< n calls); the
+                                         // arrivals are n_adm + blocked at the end (everything else finishes)
   fs_replay_summary sum;
   int err_code; u64 err_idx;
   // TB: this lane's B slots {lane + 32 j}
@@ -226,6 +228,7 @@ struct EngineT {
     static_heads = true; cur_ok = false; rc_cons = rc_prod = 0;
     hb_i = hb_n = 0; rf_head = rf_len = 0; ag_head = ag_len = 0;
     memset(&sum, 0, sizeof(sum));
+    nblk[0] = nblk[1] = nblk[2] = nblk[3] = 0; ndrop = 0; novl = 0;
     err_code = 0; err_idx = 0;
     if constexpr (TB) { ls.lfi = ~0ull; ls.locc = 0; ls.bf_top = st.b_cap; }
   }
@@ -394,8 +397,7 @@ struct EngineT {
     return false;
   }
   __device__ __forceinline__ void arrived(u32 r, i64 tr, bool ovl) {
-    sum.n_arrived++;
-    if (ovl) sum.n_ovl_arrivals++;
+    if (ovl) novl++;
     if (o.arrive) { o.arrive[r] = tr; o.ovl[r] = ovl; }
   }
   __device__ __forceinline__ void newly_queued(UState& us, u32 k) {
@@ -433,10 +435,10 @@ struct EngineT {
       s.blocked[upos >> 5] |= 1u << (upos & 31);
       if (us.qh_cnt == 0) us.qh_front = upos + 1;
       switch (st) {                                        // constant indices keep sum in registers
-        case 1: sum.n_block[0]++; break; case 2: sum.n_block[1]++; break;
-        case 3: sum.n_block[2]++; break; default: sum.n_block[3]++; break;
+        case 1: nblk[0]++; break; case 2: nblk[1]++; break;
+        case 3: nblk[2]++; break; default: nblk[3]++; break;
       }
-      sum.n_dropped += m_ncalls(m) - 1;
+      ndrop += m_ncalls(m) - 1;
       if (o.status) o.status[r] = (uint8_t)st;
       return st;
     }
@@ -468,8 +470,8 @@ struct EngineT {
       if (st < 0) return -1;
       if (st != FS_ST_ADMIT) {                              // the interaction is aborted midway
         digest = sm64(digest ^ ((u64)r * 16 + (u64)st));
-        if (st == FS_ST_BLOCK_USER_REQ) sum.n_block[0]++; else sum.n_block[2]++;
-        sum.n_dropped += m_ncalls(m) - m_stage(m);
+        if (st == FS_ST_BLOCK_USER_REQ) nblk[0]++; else nblk[2]++;
+        ndrop += m_ncalls(m) - m_stage(m);
         if (o.status) o.status[r] = (uint8_t)st;
         return st;
       }
@@ -885,6 +887,9 @@ struct EngineT {
     }
     sum.n_iterations = iter;
     sum.n_admitted = n_adm;
+    for (int k = 0; k < 4; k++) sum.n_block[k] = nblk[k];
+    sum.n_dropped = ndrop; sum.n_ovl_arrivals = novl;
+    sum.n_arrived = n_adm + nblk[0] + nblk[1] + nblk[2] + nblk[3];
     sum.n_finished = n_adm;                                       // the loop ends with B empty
     // STOP: final digest, counters, summary
     for (u32 k = 0; k < U; k++) digest = sm64(digest ^ (s.us[k].u & ~CLS_BIT));
