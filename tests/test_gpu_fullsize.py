@@ -100,6 +100,33 @@ def test_sweep_c5_full():
         assert s["u_min"] <= s["u_max"]
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_sweep_c5_slices(world):
+    """The strong-scaling slices: the C5 grid split by fairserve.lpt_split over `world` ranks, each
+    rank's slice (2048 / 512 scenarios: the solo-slot kernel) swept on this GPU -- every summary equals
+    the oracle's golden for that scenario."""
+    path = os.path.join(GOLD, "full_c5.json")
+    assert os.path.exists(path), f"{path} missing (tools/make_goldens.py c5full)"
+    g = json.load(open(path))
+    import bench
+    from paper_2411_15997_b200 import build, fairserve as F
+    build.build()
+    ctx = F.Context(0)
+    tr = G.generate("c5")
+    T = F.Trace(tr)
+    _, eng, pcfg = bench.workload_cfg("c2")
+    prof = F.build_app_profiles(ctx, T, pcfg)
+    scen = bench.sweep_scenarios(eng, 4096)
+    parts = F.lpt_split(F.scenario_costs(tr["meta"], scen), world)
+    keys = g["keys"]
+    for r in (0, world - 1):
+        idx = parts[r]
+        sums, codes = F.sweep(ctx, T, prof, [scen[i] for i in idx])
+        bad = [j for j, i in enumerate(idx)
+               if int(codes[j]) != g["codes"][i] or [sums[j][k] for k in keys] != g["summaries"][i]]
+        assert not bad, (r, len(bad), bad[:5])
+
+
 def test_profile_c4_full():
     """The 100M-call C4 profile (bench.py --workload c4 at one GPU) against the oracle's golden:
     every table bit-exact (sha256), interpolated quantiles within 1e-6."""
