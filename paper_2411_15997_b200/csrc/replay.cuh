@@ -132,6 +132,44 @@ template <int HS, int LPS = 32, bool BASE = true, int TOUR = 0, bool FWI = false
 struct EngineT {
   static_assert(!TOUR || (HS == HS_WARP && LPS == 32 && !BASE), "warp tournament: FairServe modes on a full warp");
   static constexpr bool TB = (TOUR & 2) != 0, TA = (TOUR & 4) != 0;
+  // SQ (the warp-piece engines: single replay, solo-slot sweep): one queue heap per class of the front,
+  // keyed (u, tie) -- s.hk / hk_n hold class 0 (continuation fronts), s.hm / hm_n class 1 (heads) --
+  // instead of the pick heap keyed (class | u, tie) plus the lift heap keyed u: each queued user in one
+  // heap, one sift per charge / enqueue / exit (C2 replay 3.18 -> 3.06 s; the 16-per-SM sweep was
+  // slower with it, profiles/r02_ab_heap_split_*.log)
+  static constexpr bool SQ = TOUR != 0;
+  __device__ __forceinline__ HK* qh(u32 c) const { return c ? (HK*)s.hm : s.hk; }
+  __device__ __forceinline__ u32 qn(u32 c) const { return c ? hm_n : hk_n; }
+  __device__ __forceinline__ void q_up(u32 c, u32 i, HK x) {
+    HK* H = qh(c);
+    while (i > 0) {
+      u32 pi = (i - 1) >> 1;
+      HK p = H[pi];
+      if (!kl(x, p)) break;
+      H[i] = p; s.hpos[p.user].x = i; i = pi;
+    }
+    H[i] = x; s.hpos[x.user].x = i;
+  }
+  __device__ __forceinline__ void q_down(u32 c, u32 i, HK x) {
+    HK* H = qh(c);
+    const u32 n = qn(c);
+    for (;;) {
+      u32 l = 2 * i + 1;
+      if (l >= n) break;
+      HK cl = H[l];
+      if (l + 1 < n) { HK cr = H[l + 1]; if (kl(cr, cl)) { cl = cr; l++; } }
+      if (!kl(cl, x)) break;
+      H[i] = cl; s.hpos[cl.user].x = i; i = l;
+    }
+    H[i] = x; s.hpos[x.user].x = i;
+  }
+  __device__ __forceinline__ void q_push(u32 c, HK x) { const u32 i = c ? hm_n++ : hk_n++; q_up(c, i, x); }
+  __device__ __forceinline__ void q_remove(u32 c, u32 pos) {
+    HK* H = qh(c);
+    const u32 n = c ? --hm_n : --hk_n;
+    if (pos != n) { HK last = H[n]; if (pos > 0 && kl(last, H[(pos - 1) >> 1])) q_up(c, pos, last); else q_down(c, pos, last); }
+  }
+  __device__ __forceinline__ u32 queued() const { return SQ ? hk_n + hm_n : hk_n; }
   static constexpr bool RING = HS == HS_RING;
   const EngShared* sh;
   const EngCfg* c;
@@ -268,10 +306,15 @@ struct EngineT {
     if (us.qh_cnt + us.qc_cnt != 0) {                    // queued: both keys increased
       pick_blocked = false;
       uint2 ps = s.hpos[k];
-      HK x; x.key = nu; x.tie = us.tie; x.user = k;
-      hk_down(ps.x, x);
-      HM y; y.u = nu & ~CLS_BIT; y.user = k; y.pad = 0;
-      hm_down(ps.y, y);
+      if constexpr (SQ) {
+        HK x; x.key = nu & ~CLS_BIT; x.tie = us.tie; x.user = k;
+        q_down((u32)(nu >> 63), ps.x, x);
+      } else {
+        HK x; x.key = nu; x.tie = us.tie; x.user = k;
+        hk_down(ps.x, x);
+        HM y; y.u = nu & ~CLS_BIT; y.user = k; y.pad = 0;
+        hm_down(ps.y, y);
+      }
     }
     return true;
   }
@@ -391,7 +434,13 @@ struct EngineT {
   __device__ __forceinline__ bool lift(UState& us) {
     if (us.qh_cnt + us.qc_cnt != 0) return true;
     u64 l;
-    if (hm_n == 0) l = e >= 0 ? (s.us[(u32)e].u & ~CLS_BIT) : 0;   // l.13-15
+    if constexpr (SQ) {
+      if (hk_n + hm_n == 0) l = e >= 0 ? (s.us[(u32)e].u & ~CLS_BIT) : 0;   // l.13-15
+      else {                                                                // l.16-18
+        l = hk_n ? s.hk[0].key : ~0ull;
+        if (hm_n) l = mn64(l, ((const HK*)s.hm)[0].key);
+      }
+    } else if (hm_n == 0) l = e >= 0 ? (s.us[(u32)e].u & ~CLS_BIT) : 0;   // l.13-15
     else l = s.hm[0].u;                                             // l.16-18
     if (l > (us.u & ~CLS_BIT)) us.u = (us.u & CLS_BIT) | l;
     return false;
@@ -402,6 +451,11 @@ struct EngineT {
   }
   __device__ __forceinline__ void newly_queued(UState& us, u32 k) {
     pick_blocked = false;
+    if constexpr (SQ) {
+      HK x; x.key = us.u & ~CLS_BIT; x.tie = us.tie; x.user = k;
+      q_push((u32)(us.u >> 63), x);
+      return;
+    }
     HK x; x.key = us.u; x.tie = us.tie; x.user = k;
     hk_up(hk_n++, x);
     HM y; y.u = us.u & ~CLS_BIT; y.user = k; y.pad = 0;
@@ -491,9 +545,11 @@ struct EngineT {
       newly_queued(us, k);
     } else if ((!BASE || c->mode <= FS_MODE_WI) && us.qc_cnt == 1) {   // FS: class 1 -> 0, key decreased
       pick_blocked = false;
+      if constexpr (SQ) q_remove(1, s.hpos[k].x);
       us.u &= ~CLS_BIT; us.tie = myseq; us.nf = NONE32;
       HK x; x.key = us.u; x.tie = myseq; x.user = k;
-      hk_up(s.hpos[k].x, x);
+      if constexpr (SQ) q_push(0, x);
+      else hk_up(s.hpos[k].x, x);
     }
     return FS_ST_ADMIT;
   }
@@ -502,8 +558,9 @@ struct EngineT {
   struct Adm { u32 r; u64 prompt; BEnt b; i64 arr; };
   // Returns false if Q is empty or the candidate does not fit (Q16, Q17).
   __device__ __forceinline__ bool pick(i64 occ_now, u32 nb, u64 C, u32 Bmax, Adm* a) {
-    if (hk_n == 0 || nb >= Bmax) return false;             // can_add_new_request: batch slots
-    u32 k = s.hk[0].user;
+    if (queued() == 0 || nb >= Bmax) return false;          // can_add_new_request: batch slots
+    const u32 c0 = SQ && hk_n == 0 ? 1u : 0u;               // (SQ) class 0 first (l.31-35)
+    u32 k = SQ ? qh(c0)[0].user : s.hk[0].user;
     UState& us = s.us[k];
     u32 nfk = us.nf;                                         // cached need of the front: a failing
     if (nfk != NONE32 && (u64)occ_now + nfk > C) return false;      // candidate costs no global load
@@ -540,16 +597,23 @@ struct EngineT {
       } else us.qh_front = us.qh_next;
     }
     if (us.qh_cnt + us.qc_cnt == 0) {                        // user leaves Q: e <- k
-      uint2 ps = s.hpos[k];
-      heaps_remove(k, ps.x, ps.y);
+      if constexpr (SQ) q_remove(c0, 0);
+      else { uint2 ps = s.hpos[k]; heaps_remove(k, ps.x, ps.y); }
       us.u &= ~CLS_BIT;
       e = k;
     } else {                                                 // front changed: key increased
       if (dq) us.tie = (us.qc_cnt && (us.qh_cnt == 0 || us.cs < us.hs)) ? us.cs : us.hs;
       else if (us.qc_cnt) { us.u &= ~CLS_BIT; us.tie = nseq; } else { us.u |= CLS_BIT; us.tie = us.hf; }
       us.nf = NONE32;
-      HK x; x.key = us.u; x.tie = us.tie; x.user = k;
-      hk_down(0, x);
+      if constexpr (SQ) {                                    // same class: sift down; 0 -> 1: move heaps
+        HK x; x.key = us.u & ~CLS_BIT; x.tie = us.tie; x.user = k;
+        const u32 c1 = (u32)(us.u >> 63);
+        if (c1 == c0) q_down(c0, 0, x);
+        else { q_remove(c0, 0); q_push(c1, x); }
+      } else {
+        HK x; x.key = us.u; x.tie = us.tie; x.user = k;
+        hk_down(0, x);
+      }
     }
     a->r = r;
     a->prompt = B.y;
@@ -762,7 +826,7 @@ struct EngineT {
     next_arrival();
     for (;;) {
       if (HS == HS_WARP) __syncwarp(group_mask());                // the group's lanes stay in lockstep
-      if (b_n == 0 && hk_n == 0) {                                // 1: idle engine restarts at the arrival
+      if (b_n == 0 && queued() == 0) {                                // 1: idle engine restarts at the arrival
         if (!pend) break;
         if (tn > clock) clock = tn;
       }
