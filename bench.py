@@ -475,7 +475,7 @@ def _stage_line(name, ms, n, algo_b, peaks, kt, reps, ncu):
             "frac": gbs / peaks["hbm_gbs"], "kernels": kern}
 
 
-NCU_TAGS = ("r02c", "r02b", "r02")          # committed ncu captures, newest first (profiles/README.md)
+NCU_TAGS = ("r02d", "r02c", "r02b", "r02")          # committed ncu captures, newest first (profiles/README.md)
 
 
 def ncu_path(name):
