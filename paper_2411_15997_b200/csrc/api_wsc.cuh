@@ -416,9 +416,10 @@ extern "C" int fs_wsc_replay(fs_ctx* ctx, const fs_trace* tr, const fs_profile* 
   if (eo.admit && !eo.order) eo.admit = nullptr;
   static const int rwarp = [] { const char* v = getenv("FS_REPLAY_WARP"); return v ? atoi(v) : 1; }();
   size_t budget = ctx->smem_optin ? ctx->smem_optin - 512 : 100 * 1024;
-  // at most 128 KB of shared memory: the rest of the SM's 256 KB stays L1 for the state that spills to
-  // global memory (C3-shaped 10k users: 3.36 -> 3.18-3.25 us/call; C2 unchanged; profiles/r02_ab_replay_smem.log)
-  static const long smem_kb = [] { const char* v = getenv("FS_REPLAY_SMEM_KB"); return v ? atol(v) : 128; }();
+  // at most 160 KB of shared memory: the rest of the SM's 256 KB stays L1 for the state that spills to
+  // global memory (C3-shaped 10k users: 227 KB 3.36 us/call, 128-160 KB 3.0 us/call with the per-class
+  // heaps, 200 KB 3.17; C2 2.85 s at 160 KB vs 2.94-2.97 at 128; profiles/r02_ab_replay_smem*.log)
+  static const long smem_kb = [] { const char* v = getenv("FS_REPLAY_SMEM_KB"); return v ? atol(v) : 160; }();
   if (smem_kb >= 0) budget = std::min<size_t>(budget, (size_t)smem_kb * 1024);
   if (rwarp) budget -= std::min<size_t>(budget, sizeof(HEnt) * 32 + 64);   // the warp engine's static head batch
   fs_replay_summary* dsum = S.alloc<fs_replay_summary>(1);
