@@ -33,3 +33,15 @@ def test_ncu_csv_parser(tmp_path):
     p.write_text('==PROF== hello\n"ID","Kernel Name","Metric Name","Metric Unit","Metric Value"\n'
                  '"0","k","smsp__inst_executed.sum","inst","1,234"\n')
     assert bench.ncu_csv(str(p)) == {"smsp__inst_executed.sum": 1234.0}
+
+
+def test_ncu_captures_newest_first():
+    """bench.py reads the newest committed ncu capture of each kind (profiles/<tag>_<name>), and the
+    sweep capture it reads carries the instruction count the C5 roofline divides by."""
+    import os
+    p = bench.ncu_path("sweep.csv")
+    assert os.path.exists(p) and os.path.basename(p).startswith(bench.NCU_TAGS[0] + "_")
+    m = bench.ncu_csv(p)
+    assert m.get("smsp__inst_executed.sum", 0) > 0 and m.get("gpu__time_duration.sum", 0) > 0
+    for name in ("c4_dram.csv", "c3_act_dram.csv", "replay.csv"):
+        assert os.path.exists(bench.ncu_path(name)), name
